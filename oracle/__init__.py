@@ -1,0 +1,221 @@
+"""CPU oracle of the guiding-map ray march — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this package.  The
+product (``paper_2604_03748_b200``) never imports it, and it never imports
+the product: the two share no code (DESIGN.md §3 "Oracle independence").
+
+The arithmetic lives in ``nsl_oracle.c`` (plain single-threaded C, fp64
+values, prescribed fp32 index ops, built with ``-ffp-contract=off``), written
+from DESIGN.md §2, which restates PAPER.md Algorithm 1 (L394-407), eq:approx
+(L361-365) and §4.2 (L410).  This module is ctypes marshalling only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "nsl_oracle.c")
+_HDR = os.path.join(_HERE, "nsl_oracle.h")
+LIB_PATH = os.path.join(_HERE, "libnsl_oracle.so")
+CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
+          "-D_GNU_SOURCE"]
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        subprocess.check_call(["gcc", *CFLAGS, "-o", LIB_PATH, _SRC, "-lm"])
+    return LIB_PATH
+
+
+class OrcGrid(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("origin", ctypes.c_float * 3), ("voxel_width", ctypes.c_float)]
+
+
+class OrcCamera(ctypes.Structure):
+    _fields_ = [("projection", ctypes.c_int32), ("position", ctypes.c_float * 3),
+                ("forward", ctypes.c_float * 3), ("up", ctypes.c_float * 3),
+                ("extent", ctypes.c_float), ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class OrcLight(ctypes.Structure):
+    _fields_ = [("to_light", ctypes.c_float * 3), ("rgb", ctypes.c_float * 3)]
+
+
+class OrcMedium(ctypes.Structure):
+    _fields_ = [("extinction", ctypes.c_float), ("albedo", ctypes.c_float), ("hg_g", ctypes.c_float)]
+
+
+class OrcMarch(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_float), ("light_step", ctypes.c_float),
+                ("max_steps", ctypes.c_int32), ("depth_tau", ctypes.c_float),
+                ("t_min", ctypes.c_float), ("opacity_form", ctypes.c_int32),
+                ("jitter", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("guide_axis", ctypes.c_float * 3)]
+
+
+class OrcFrameConstants(ctypes.Structure):
+    _fields_ = [("inv_dx", ctypes.c_float), ("B", ctypes.c_float * 3), ("Ex", ctypes.c_float * 3),
+                ("Ey", ctypes.c_float * 3), ("Dg", ctypes.c_float * 3), ("Oe", ctypes.c_float * 3),
+                ("F0", ctypes.c_float * 3), ("fwd", ctypes.c_float * 3),
+                ("Ln", (ctypes.c_float * 3) * 4), ("Lg", (ctypes.c_float * 3) * 4),
+                ("P", ctypes.c_float * 4), ("P64", ctypes.c_double * 4)]
+
+
+DENSITY_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.POINTER(ctypes.c_float), ctypes.c_void_p)
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        lib.orc_hg.argtypes = [ctypes.c_double, ctypes.c_double]
+        lib.orc_hg.restype = ctypes.c_double
+        lib.orc_fmix32.argtypes = [ctypes.c_uint32]
+        lib.orc_fmix32.restype = ctypes.c_uint32
+        lib.orc_jitter_hash.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
+        lib.orc_jitter_hash.restype = ctypes.c_uint32
+        lib.orc_jitter_delta.argtypes = [P(OrcMarch), ctypes.c_uint32, ctypes.c_uint32]
+        lib.orc_jitter_delta.restype = ctypes.c_float
+        lib.orc_sample.argtypes = [P(OrcGrid), ctypes.c_void_p, P(ctypes.c_float)]
+        lib.orc_sample.restype = ctypes.c_double
+        lib.orc_frame_constants_compute.argtypes = [P(OrcGrid), P(OrcCamera), P(OrcLight), ctypes.c_int32,
+                                                    ctypes.c_int32, P(OrcMedium), P(OrcMarch),
+                                                    P(OrcFrameConstants)]
+        lib.orc_frame_constants_compute.restype = ctypes.c_int
+        lib.orc_guiding_map.argtypes = [P(OrcGrid), ctypes.c_void_p, DENSITY_FN, ctypes.c_void_p,
+                                        P(OrcCamera), P(OrcLight), ctypes.c_int32, ctypes.c_int32,
+                                        P(OrcMedium), P(OrcMarch), ctypes.c_uint32, ctypes.c_int64,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int32]
+        lib.orc_guiding_map.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+# ------------------------------------------------------------------ marshalling
+def _grid(g) -> OrcGrid:
+    return OrcGrid(g.nx, g.ny, g.nz, (ctypes.c_float * 3)(*g.origin), g.voxel_width)
+
+
+def _camera(c) -> OrcCamera:
+    f3 = ctypes.c_float * 3
+    return OrcCamera(c.projection, f3(*c.position), f3(*c.forward), f3(*c.up), c.extent, c.width, c.height)
+
+
+def _lights(ls):
+    arr = (OrcLight * max(1, len(ls)))()
+    for i, l in enumerate(ls):
+        arr[i].to_light = (ctypes.c_float * 3)(*l.to_light)
+        arr[i].rgb = (ctypes.c_float * 3)(*l.rgb)
+    return arr
+
+
+def _medium(m) -> OrcMedium:
+    return OrcMedium(m.extinction, m.albedo, m.hg_g)
+
+
+def _march(m) -> OrcMarch:
+    return OrcMarch(m.step, m.light_step, m.max_steps, m.depth_tau, m.t_min, m.opacity_form,
+                    m.jitter, m.seed & 0xFFFFFFFFFFFFFFFF, (ctypes.c_float * 3)(*m.guide_axis))
+
+
+def hg(g: float, cos_theta: float) -> float:
+    return _load().orc_hg(g, cos_theta)
+
+
+def fmix32(h: int) -> int:
+    return _load().orc_fmix32(h & 0xFFFFFFFF)
+
+
+def jitter_hash(seed: int, frame_id: int, pixel: int) -> int:
+    return _load().orc_jitter_hash(seed & 0xFFFFFFFFFFFFFFFF, frame_id, pixel)
+
+
+def jitter_delta(march, frame_id: int, pixel: int) -> float:
+    m = _march(march)
+    return _load().orc_jitter_delta(ctypes.byref(m), frame_id, pixel)
+
+
+def sample(grid, vals: np.ndarray, u) -> float:
+    v = np.ascontiguousarray(vals, dtype=np.float32)
+    g = _grid(grid)
+    uu = (ctypes.c_float * 3)(*u)
+    return _load().orc_sample(ctypes.byref(g), v.ctypes.data, uu)
+
+
+def frame_constants(grid, cam, lights, light_mode, medium, march) -> dict:
+    out = OrcFrameConstants()
+    ls = _lights(lights)
+    rc = _load().orc_frame_constants_compute(ctypes.byref(_grid(grid)), ctypes.byref(_camera(cam)), ls,
+                                             len(lights), light_mode, ctypes.byref(_medium(medium)),
+                                             ctypes.byref(_march(march)), ctypes.byref(out))
+    if rc:
+        raise ValueError("orc_frame_constants_compute rejected its arguments")
+    n = len(lights)
+    return {
+        "inv_dx": np.float32(out.inv_dx),
+        "B": np.array(out.B, np.float32), "Ex": np.array(out.Ex, np.float32),
+        "Ey": np.array(out.Ey, np.float32), "Dg": np.array(out.Dg, np.float32),
+        "Oe": np.array(out.Oe, np.float32), "F0": np.array(out.F0, np.float32),
+        "fwd": np.array(out.fwd, np.float32),
+        "Ln": np.array([list(out.Ln[i]) for i in range(n)], np.float32),
+        "Lg": np.array([list(out.Lg[i]) for i in range(n)], np.float32),
+        "P": np.array(list(out.P)[:n], np.float32),
+        "P64": np.array(list(out.P64)[:n], np.float64),
+    }
+
+
+def guiding_map(grid, vals: Optional[np.ndarray], cam, lights, light_mode, medium, march,
+                frame_id: int = 0, pixels: Optional[Sequence[int]] = None, density_fn=None,
+                forced_hit=None, forced_term=None, no_clip_n: int = 0) -> dict:
+    """Run the oracle on one frame.  Returns rgbt (n,4) f64, depth (n,) f32,
+    debug (n,6) u32, margin (n,2) f64, and the pixel list used."""
+    lib = _load()
+    W, H = cam.width, cam.height
+    if pixels is None:
+        pix = None
+        n = W * H
+    else:
+        pix = np.ascontiguousarray(np.asarray(pixels, dtype=np.int64))
+        n = int(pix.size)
+    rgbt = np.zeros((n, 4), np.float64)
+    depth = np.zeros((n,), np.float32)
+    debug = np.zeros((n, 6), np.uint32)
+    margin = np.zeros((n, 2), np.float64)
+    v = None
+    if vals is not None:
+        v = np.ascontiguousarray(vals, dtype=np.float32)
+        assert v.size == grid.nx * grid.ny * grid.nz
+    fh = None if forced_hit is None else np.ascontiguousarray(np.asarray(forced_hit, np.int32))
+    ft = None if forced_term is None else np.ascontiguousarray(np.asarray(forced_term, np.int32))
+    cb = DENSITY_FN(density_fn) if density_fn is not None else DENSITY_FN()
+    ls = _lights(lights)
+    rc = lib.orc_guiding_map(ctypes.byref(_grid(grid)), None if v is None else v.ctypes.data, cb, None,
+                             ctypes.byref(_camera(cam)), ls, len(lights), light_mode,
+                             ctypes.byref(_medium(medium)), ctypes.byref(_march(march)), frame_id, n,
+                             None if pix is None else pix.ctypes.data,
+                             rgbt.ctypes.data, depth.ctypes.data, debug.ctypes.data, margin.ctypes.data,
+                             None if fh is None else fh.ctypes.data,
+                             None if ft is None else ft.ctypes.data, no_clip_n)
+    if rc:
+        raise ValueError("orc_guiding_map rejected its arguments")
+    return {"rgbt": rgbt, "depth": depth, "debug": debug, "margin": margin,
+            "pixels": np.arange(n, dtype=np.int64) if pix is None else pix}
+
+
+def run_workload_frame(w, f: int, pixels=None, **kw) -> dict:
+    """Oracle on frame f (local index) of an nsl_inputs.Workload."""
+    return guiding_map(w.grid, w.volume(w.frame_vol[f]), w.cameras[f], w.lights[f], w.light_mode,
+                       w.medium, w.march, frame_id=w.frame_ids[f], pixels=pixels, **kw)

@@ -1,0 +1,369 @@
+/* oracle/nsl_oracle.c — plain, slow, single-threaded CPU oracle of the
+ * guiding-map ray march.  TEST INFRASTRUCTURE ONLY (see nsl_oracle.h).
+ *
+ * Written step by step from DESIGN.md §2 (canonical C1-C14), which restates
+ * PAPER.md Algorithm 1 (L394-407), eq:approx (L361-365) and §4.2 (L410).
+ * Build with -ffp-contract=off so that every fp32 expression below is
+ * evaluated exactly as written (fmaf() is the C99 correctly-rounded fma).
+ */
+#include "nsl_oracle.h"
+
+#include <math.h>
+#include <stddef.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- C10 HG */
+/* Henyey-Greenstein phase ("Henyey-Greenstein phase function
+ * with g=0"; formula SPEC S:59): (1-g^2) / (4 pi (1+g^2-2 g c)^(3/2)). */
+double orc_hg(double g, double c) {
+    double d = (1.0 + g * g) - 2.0 * g * c;
+    return (1.0 - g * g) / ((4.0 * M_PI) * (d * sqrt(d)));
+}
+
+/* ---------------------------------------------------------------- C4 jitter */
+/* MurmurHash3 finaliser. */
+uint32_t orc_fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+/* Alg. 1 line "x0 <- x0 + delta; delta: random jitter",
+ * keyed per (seed, frame, pixel) — DESIGN.md C4. */
+uint32_t orc_jitter_hash(uint64_t seed, uint32_t frame_id, uint32_t pixel) {
+    uint32_t lo = (uint32_t)(seed & 0xffffffffu), hi = (uint32_t)(seed >> 32);
+    uint32_t h = orc_fmix32(lo ^ 0x9E3779B9u);
+    h = orc_fmix32(h ^ hi);
+    h = orc_fmix32(h ^ frame_id);
+    h = orc_fmix32(h ^ pixel);
+    return h;
+}
+
+float orc_jitter_delta(const orc_march* m, uint32_t frame_id, uint32_t pixel) {
+    if (!m->jitter) return 0.0f;
+    uint32_t h = orc_jitter_hash(m->seed, frame_id, pixel);
+    float u = (float)(h >> 8) * (1.0f / 16777216.0f);   /* exact: 24-bit integer times 2^-24 */
+    return u * m->step;                                  /* one fp32 multiply */
+}
+
+/* ---------------------------------------------------------------- C1 sampler */
+/* Voxel (i,j,k) (0-based) of the x-fastest grid; padded index 0 and n+1 are
+ * the zero apron ("outside the grid is vacuum", DESIGN.md ledger #15). */
+static double padded_voxel(const orc_grid* g, const float* vals, int i, int j, int k) {
+    if (i < 1 || j < 1 || k < 1 || i > g->nx || j > g->ny || k > g->nz) return 0.0;
+    size_t idx = ((size_t)(k - 1) * (size_t)g->ny + (size_t)(j - 1)) * (size_t)g->nx + (size_t)(i - 1);
+    return (double)vals[idx];
+}
+
+static int inside_support(const orc_grid* g, const float u[3]) {
+    return u[0] > 0.0f && u[0] < (float)(g->nx + 1) &&
+           u[1] > 0.0f && u[1] < (float)(g->ny + 1) &&
+           u[2] > 0.0f && u[2] < (float)(g->nz + 1);
+}
+
+static double lerp64(double a, double b, double t) { return a + t * (b - a); }
+
+/* Trilinear reconstruction of sigma_s's carrier "in a 3D texture"
+ * (PAPER.md L410), border-zero, interpolating x, then y, then z (C1). */
+double orc_sample(const orc_grid* g, const float* vals, const float u[3]) {
+    if (!inside_support(g, u)) return 0.0;
+    float fl0 = floorf(u[0]), fl1 = floorf(u[1]), fl2 = floorf(u[2]);
+    int i = (int)fl0, j = (int)fl1, k = (int)fl2;
+    double fx = (double)(u[0] - fl0), fy = (double)(u[1] - fl1), fz = (double)(u[2] - fl2);
+    double c000 = padded_voxel(g, vals, i, j, k), c100 = padded_voxel(g, vals, i + 1, j, k);
+    double c010 = padded_voxel(g, vals, i, j + 1, k), c110 = padded_voxel(g, vals, i + 1, j + 1, k);
+    double c001 = padded_voxel(g, vals, i, j, k + 1), c101 = padded_voxel(g, vals, i + 1, j, k + 1);
+    double c011 = padded_voxel(g, vals, i, j + 1, k + 1), c111 = padded_voxel(g, vals, i + 1, j + 1, k + 1);
+    double x00 = lerp64(c000, c100, fx), x10 = lerp64(c010, c110, fx);
+    double x01 = lerp64(c001, c101, fx), x11 = lerp64(c011, c111, fx);
+    double y0 = lerp64(x00, x10, fy), y1 = lerp64(x01, x11, fy);
+    return lerp64(y0, y1, fz);
+}
+
+/* ---------------------------------------------------------------- C3 frame constants */
+static double dot3(const double a[3], const double b[3]) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+static void cross3(const double a[3], const double b[3], double o[3]) {
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
+static double norm3(const double a[3]) { return sqrt(dot3(a, a)); }
+
+int orc_frame_constants_compute(const orc_grid* g, const orc_camera* cam,
+                                const orc_light* lights, int32_t n_lights, int32_t light_mode,
+                                const orc_medium* med, const orc_march* m,
+                                orc_frame_constants* out) {
+    (void)m;
+    if (!g || !cam || !med || !out || n_lights < 1 || n_lights > 4) return 1;
+    memset(out, 0, sizeof(*out));
+    double dx = (double)g->voxel_width;
+    double F[3] = {cam->forward[0], cam->forward[1], cam->forward[2]};
+    double Up[3] = {cam->up[0], cam->up[1], cam->up[2]};
+    double nf = norm3(F);
+    double f[3] = {F[0] / nf, F[1] / nf, F[2] / nf};
+    double c[3];
+    cross3(f, Up, c);
+    double nc = norm3(c);
+    double r[3] = {c[0] / nc, c[1] / nc, c[2] / nc};
+    double u[3];
+    cross3(r, f, u);
+    double W = (double)cam->width, H = (double)cam->height;
+    double ay = (double)cam->extent * 0.5;
+    double ax = (ay * W) / H;
+    double cx = 1.0 / W - 1.0, cy = 1.0 - 1.0 / H;
+    double ex = 2.0 / W, ey = -2.0 / H;
+    out->inv_dx = (float)(1.0 / dx);
+    for (int a = 0; a < 3; ++a) {
+        double P = (double)cam->position[a], o = (double)g->origin[a];
+        /* ortho: origin(px,py) = P + s_x ax r + s_y ay u, to padded index space */
+        double w = P + (cx * ax) * r[a];
+        w = w + (cy * ay) * u[a];
+        out->B[a] = (float)((w - o) / dx + 0.5);
+        out->Dg[a] = (float)(f[a] / dx);
+        /* persp */
+        out->Oe[a] = (float)((P - o) / dx + 0.5);
+        out->F0[a] = (float)((f[a] + (cx * ax) * r[a]) + (cy * ay) * u[a]);
+        out->fwd[a] = (float)f[a];
+        if (cam->projection == 0) {
+            out->Ex[a] = (float)(((ex * ax) * r[a]) / dx);
+            out->Ey[a] = (float)(((ey * ay) * u[a]) / dx);
+        } else {
+            out->Ex[a] = (float)((ex * ax) * r[a]);
+            out->Ey[a] = (float)((ey * ay) * u[a]);
+        }
+    }
+    /* lights: explicit list, or the surrogate set of eq:approx:
+     * front = omega = -f, top = omega x z, bottom = -omega x z (normalised; #8) */
+    double Ln[4][3];
+    if (light_mode == 1) {
+        if (n_lights > 3) return 1;
+        double om[3] = {-f[0], -f[1], -f[2]};
+        double A[3] = {m ? m->guide_axis[0] : 0.0, m ? m->guide_axis[1] : 0.0, m ? m->guide_axis[2] : 0.0};
+        if (A[0] == 0.0 && A[1] == 0.0 && A[2] == 0.0) { A[2] = 1.0; }
+        double nA = norm3(A);
+        double a[3] = {A[0] / nA, A[1] / nA, A[2] / nA};
+        double s[3];
+        cross3(om, a, s);
+        double ns = norm3(s);
+        if (ns < 1e-6) {
+            double xh[3] = {1.0, 0.0, 0.0};
+            cross3(om, xh, s);
+            ns = norm3(s);
+        }
+        double t[3] = {s[0] / ns, s[1] / ns, s[2] / ns};
+        for (int q = 0; q < 3; ++q) {
+            Ln[0][q] = om[q];
+            Ln[1][q] = t[q];
+            Ln[2][q] = -t[q];
+        }
+    } else {
+        if (!lights) return 1;
+        for (int l = 0; l < n_lights; ++l) {
+            double L[3] = {lights[l].to_light[0], lights[l].to_light[1], lights[l].to_light[2]};
+            double nl = norm3(L);
+            for (int q = 0; q < 3; ++q) Ln[l][q] = L[q] / nl;
+        }
+    }
+    for (int l = 0; l < n_lights; ++l) {
+        for (int q = 0; q < 3; ++q) {
+            out->Ln[l][q] = (float)Ln[l][q];
+            out->Lg[l][q] = (float)(Ln[l][q] / dx);
+        }
+        /* phase angle between incoming propagation (-to_light) and outgoing (-dir): cos = to_light . dir */
+        double P = orc_hg((double)med->hg_g, dot3(Ln[l], f));
+        out->P64[l] = P;
+        out->P[l] = (float)P;
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- C5-C12 march */
+typedef struct {
+    const orc_grid* g;
+    const float* vals;
+    orc_density_fn fn;
+    void* ctx;
+} dens_t;
+
+static double density(const dens_t* d, const float u[3]) {
+    if (!inside_support(d->g, u)) return 0.0;
+    if (d->fn) return d->fn(u, d->ctx);
+    return orc_sample(d->g, d->vals, u);
+}
+
+/* C8: light transmittance from U along light l, right-endpoint rule, no jitter,
+ * to the support exit.  Returns T^l; *M gets the number of samples. */
+static double light_march(const dens_t* d, const float U[3], const float Lg[3], float hl,
+                          double kappa, uint32_t* M) {
+    double sum_sigma_t = 0.0;
+    uint32_t j = 1;
+    for (;; ++j) {
+        float s = (float)j * hl;
+        float Y[3] = {fmaf(s, Lg[0], U[0]), fmaf(s, Lg[1], U[1]), fmaf(s, Lg[2], U[2])};
+        if (!inside_support(d->g, Y)) break;
+        sum_sigma_t += kappa * density(d, Y);
+        if (j > 100000000u) break;   /* unreachable for |Lg| = 1/dx; guards a corrupt input */
+    }
+    *M = j - 1;
+    return exp(-(double)hl * sum_sigma_t);
+}
+
+/* Conservative upper bound on the primary step index whose sample can lie in
+ * the support box (fp64 slab test on a 1-voxel-expanded box). */
+static int64_t primary_upper_bound(const orc_grid* g, const float O[3], const float D[3],
+                                   float delta, float h) {
+    double t0 = -1e300, t1 = 1e300;
+    double n[3] = {g->nx, g->ny, g->nz};
+    for (int a = 0; a < 3; ++a) {
+        double lo = -1.0, hi = n[a] + 2.0;
+        if (D[a] == 0.0f) {
+            if (!((double)O[a] > lo && (double)O[a] < hi)) return 0;
+            continue;
+        }
+        double ta = (lo - (double)O[a]) / (double)D[a], tb = (hi - (double)O[a]) / (double)D[a];
+        if (ta > tb) { double tt = ta; ta = tb; tb = tt; }
+        if (ta > t0) t0 = ta;
+        if (tb < t1) t1 = tb;
+    }
+    if (t1 < t0 || t1 <= 0.0) return 0;
+    double nmax = floor((t1 - (double)delta) / (double)h) + 2.0;
+    if (nmax < 0.0) return 0;
+    if (nmax > 1e8) nmax = 1e8;
+    return (int64_t)nmax;
+}
+
+int orc_guiding_map(const orc_grid* g, const float* vals,
+                    orc_density_fn density_fn, void* density_ctx,
+                    const orc_camera* cam, const orc_light* lights, int32_t n_lights,
+                    int32_t light_mode, const orc_medium* med, const orc_march* m,
+                    uint32_t frame_id, int64_t n_pix, const int64_t* pix,
+                    double* out_rgbt, float* out_depth, uint32_t* out_debug, double* out_margin,
+                    const int32_t* forced_hit, const int32_t* forced_term, int32_t no_clip_n) {
+    if (!g || (!vals && !density_fn) || !cam || !lights || !med || !m || !out_rgbt || !out_depth) return 1;
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1 || !(g->voxel_width > 0.0f)) return 1;
+    if (cam->width < 1 || cam->height < 1 || !(m->step > 0.0f)) return 1;
+    orc_frame_constants fc;
+    if (orc_frame_constants_compute(g, cam, lights, n_lights, light_mode, med, m, &fc)) return 1;
+    const int W = cam->width, H = cam->height;
+    if (!pix) n_pix = (int64_t)W * H;
+    const float h = m->step;
+    const float hl = m->light_step > 0.0f ? m->light_step : m->step;
+    const double kappa = (double)med->extinction, alpha = (double)med->albedo;
+    const double g_hg = (double)med->hg_g;
+    const dens_t dens = {g, vals, density_fn, density_ctx};
+
+    for (int64_t q = 0; q < n_pix; ++q) {
+        int64_t p = pix ? pix[q] : q;
+        int px = (int)(p % W), py = (int)(p / W);
+        /* C3: per-pixel ray in padded index space */
+        float O[3], D[3], dir[3];
+        if (cam->projection == 0) {
+            for (int a = 0; a < 3; ++a) {
+                O[a] = fmaf((float)py, fc.Ey[a], fmaf((float)px, fc.Ex[a], fc.B[a]));
+                D[a] = fc.Dg[a];
+                dir[a] = fc.fwd[a];
+            }
+        } else {
+            float d[3];
+            for (int a = 0; a < 3; ++a) d[a] = fmaf((float)py, fc.Ey[a], fmaf((float)px, fc.Ex[a], fc.F0[a]));
+            float qn = fmaf(d[2], d[2], fmaf(d[1], d[1], d[0] * d[0]));
+            float inv = 1.0f / sqrtf(qn);
+            for (int a = 0; a < 3; ++a) {
+                dir[a] = d[a] * inv;
+                D[a] = dir[a] * fc.inv_dx;
+                O[a] = fc.Oe[a];
+            }
+        }
+        double P[4];
+        for (int l = 0; l < n_lights; ++l) {
+            if (cam->projection == 0) P[l] = fc.P64[l];
+            else P[l] = orc_hg(g_hg, ((double)fc.Ln[l][0] * dir[0] + (double)fc.Ln[l][1] * dir[1]) +
+                                         (double)fc.Ln[l][2] * dir[2]);
+        }
+        /* C4 */
+        const float delta = orc_jitter_delta(m, frame_id, (uint32_t)((uint32_t)py * (uint32_t)W + (uint32_t)px));
+
+        /* C5: n = 1 .. n_max, every n tested (the clip only bounds the loop) */
+        int64_t n_max = no_clip_n > 0 ? (int64_t)no_clip_n : primary_upper_bound(g, O, D, delta, h);
+        if (m->max_steps > 0 && n_max > m->max_steps) n_max = m->max_steps;
+        int32_t f_hit = forced_hit ? forced_hit[q] : -1;
+        int32_t f_term = forced_term ? forced_term[q] : -1;
+
+        uint32_t n_lo = 0, n_hi = 0, n_hit = 0, n_term = 0, n_occ = 0, lsamp = 0;
+        double S[4] = {0, 0, 0, 0};
+        double tau = 0.0, T = 1.0;
+        float Dout = 0.0f;
+        double hit_margin = INFINITY, term_margin = INFINITY;
+        int terminated = 0;
+        for (int64_t n = 1; n <= n_max; ++n) {
+            float t = fmaf((float)n, h, delta);
+            float U[3] = {fmaf(t, D[0], O[0]), fmaf(t, D[1], O[1]), fmaf(t, D[2], O[2])};
+            if (!inside_support(g, U)) continue;
+            if (!n_lo) n_lo = (uint32_t)n;
+            n_hi = (uint32_t)n;
+            if (terminated) continue;              /* keep scanning only for n_hi (debug) */
+            n_term = (uint32_t)n;
+            double rho = density(&dens, U);
+            if (rho > 0.0) {
+                ++n_occ;
+                double sigma_t = kappa * rho, sigma_s = alpha * sigma_t;
+                /* C6 depth: first n with sigma_s > tau (Alg. 1 "if D = 0 and sigma_n > tau") */
+                if (f_hit < 0) {
+                    if (!n_hit) {
+                        double mg = m->depth_tau > 0.0f ? fabs(sigma_s - (double)m->depth_tau) / (double)m->depth_tau
+                                                        : fabs(sigma_s);
+                        if (mg < hit_margin) hit_margin = mg;
+                        if ((float)sigma_s > m->depth_tau) { n_hit = (uint32_t)n; Dout = t; }
+                    }
+                } else if ((int64_t)f_hit == n) {
+                    n_hit = (uint32_t)n; Dout = t;
+                }
+                /* C7 transmittance and opacity */
+                double s = sigma_t * (double)h;
+                double T_prev = T;
+                tau += s;
+                T = exp(-tau);
+                double A;
+                if (m->opacity_form == 0) A = alpha * T_prev * (1.0 - exp(-s));
+                else if (m->opacity_form == 1) A = alpha * T_prev * s;
+                else A = T_prev * sigma_s;
+                /* C8 + C10: L_n = sum_l T^l P_l (rgb applied at the end), L += A_n L_n */
+                for (int l = 0; l < n_lights; ++l) {
+                    uint32_t M = 0;
+                    double Tl = light_march(&dens, U, fc.Lg[l], hl, kappa, &M);
+                    lsamp += M;
+                    S[l] += A * Tl;
+                }
+                /* C11 early termination */
+                if (m->t_min > 0.0f) {
+                    double mg = fabs(T - (double)m->t_min) / (double)m->t_min;
+                    if (mg < term_margin) term_margin = mg;
+                }
+                if (f_term < 0) {
+                    if ((float)T < m->t_min) terminated = 1;
+                }
+            }
+            if (f_term >= 0 && (int64_t)f_term == n) terminated = 1;
+        }
+        double L[3] = {0, 0, 0};
+        for (int c = 0; c < 3; ++c)
+            for (int l = 0; l < n_lights; ++l) L[c] += (double)lights[l].rgb[c] * P[l] * S[l];
+        out_rgbt[4 * q + 0] = L[0];
+        out_rgbt[4 * q + 1] = L[1];
+        out_rgbt[4 * q + 2] = L[2];
+        out_rgbt[4 * q + 3] = T;
+        out_depth[q] = Dout;
+        if (out_debug) {
+            uint32_t* o = out_debug + 6 * q;
+            o[0] = n_lo; o[1] = n_hi; o[2] = n_hit; o[3] = n_term; o[4] = n_occ; o[5] = lsamp;
+        }
+        if (out_margin) {
+            out_margin[2 * q + 0] = hit_margin;
+            out_margin[2 * q + 1] = term_margin;
+        }
+    }
+    return 0;
+}

@@ -1,0 +1,97 @@
+/* oracle/nsl_oracle.h — CPU ORACLE for the guiding-map ray march.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2604_03748_b200, libnsl.so) never links, loads or
+ * calls it, and this oracle shares no code, header, table or helper with it.
+ *
+ * What it computes: Algorithm 1 of PAPER.md ("Ray-marching for Guiding Map",
+ * L394-407) with h = 10 dx (L410) and the surrogate light set of eq:approx
+ * (L361-365), in the canonical reading written out in DESIGN.md §2 (C1-C14).
+ * Everything that decides an index (frame constants, jitter, sample
+ * positions, floors, inside tests) is fp32 with exactly the prescribed
+ * operations (C14); everything after the positions (trilinear
+ * weights, sigma, exp, sums) is fp64.  Threshold decisions (depth tau,
+ * early termination T_min) compare the fp32-rounded fp64 value with the
+ * fp32 threshold, i.e. in the kernel's precision (C14).
+ *
+ * Pins: see tests/test_oracle_*.py (closed forms P2-P4, invariants P5-P8,
+ * brute force P10-P11, HG P12, sampler P13, hash P14).  No function here is
+ * "parity unpinned" except the literal reproduction of the paper's own
+ * implementation, for which the paper prints no values.
+ */
+#ifndef NSL_ORACLE_H
+#define NSL_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { int32_t nx, ny, nz; float origin[3]; float voxel_width; } orc_grid;
+typedef struct {
+    int32_t projection;               /* 0 orthographic, 1 perspective */
+    float position[3], forward[3], up[3];
+    float extent;                     /* ortho: image-plane height; persp: 2 tan(fov_y/2) */
+    int32_t width, height;
+} orc_camera;
+typedef struct { float to_light[3]; float rgb[3]; } orc_light;
+typedef struct { float extinction, albedo, hg_g; } orc_medium;
+typedef struct {
+    float step, light_step;           /* h, h_l (0 -> h) */
+    int32_t max_steps;                /* N, 0 -> unbounded */
+    float depth_tau, t_min;
+    int32_t opacity_form;             /* 0 EXP, 1 RIEMANN, 2 LITERAL */
+    int32_t jitter;                   /* 0 off, 1 per-ray hash */
+    uint64_t seed;
+    float guide_axis[3];              /* world axis "z" of eq:approx; (0,0,0) -> (0,0,1) */
+} orc_march;
+
+/* Frame constants of DESIGN.md C3 (fp64 evaluation, rounded once to fp32). */
+typedef struct {
+    float inv_dx;
+    float B[3], Ex[3], Ey[3], Dg[3];  /* ortho (index space) */
+    float Oe[3], F0[3];               /* persp: eye (index space), pixel-(0,0) world dir */
+    float fwd[3];                     /* normalised forward, fp32 */
+    float Ln[4][3];                   /* normalised to_light per light, fp32 */
+    float Lg[4][3];                   /* to_light / dx per light, fp32 */
+    float P[4];                       /* ortho phase per light, fp32 rounding of the fp64 value */
+    double P64[4];                    /* the same in fp64 (used by the oracle's values) */
+} orc_frame_constants;
+
+typedef double (*orc_density_fn)(const float u[3], void* ctx);
+
+double   orc_hg(double g, double cos_theta);
+uint32_t orc_fmix32(uint32_t h);
+uint32_t orc_jitter_hash(uint64_t seed, uint32_t frame_id, uint32_t pixel);
+float    orc_jitter_delta(const orc_march* m, uint32_t frame_id, uint32_t pixel);
+/* Trilinear border-zero sampler of C1 at padded index position u (fp32). */
+double   orc_sample(const orc_grid* g, const float* vals, const float u[3]);
+
+int orc_frame_constants_compute(const orc_grid* g, const orc_camera* cam,
+                                const orc_light* lights, int32_t n_lights, int32_t light_mode,
+                                const orc_medium* med, const orc_march* m,
+                                orc_frame_constants* out);
+
+/* One frame.  pix: NULL -> all W*H pixels in row-major order, else n_pix
+ * pixel indices (py*W+px); outputs are indexed by position in that list.
+ *   out_rgbt   n_pix*4 doubles  (L_r, L_g, L_b, T)
+ *   out_depth  n_pix floats     (D, fp32 t value; 0 = no hit)
+ *   out_debug  n_pix*6 u32 or NULL (n_lo, n_hi, n_hit, n_term, n_occ, light_samples)
+ *   out_margin n_pix*2 doubles or NULL (depth-threshold margin, T_min margin; relative)
+ *   forced_hit / forced_term: NULL or n_pix int32 (-1 = not forced)
+ *   density_fn: NULL -> sample `vals`; else analytic density at padded index position
+ *   no_clip_n: 0 -> conservative clip; >0 -> test every n in [1, no_clip_n] (pin P10)
+ * Returns 0 on success, nonzero on invalid arguments. */
+int orc_guiding_map(const orc_grid* g, const float* vals,
+                    orc_density_fn density_fn, void* density_ctx,
+                    const orc_camera* cam, const orc_light* lights, int32_t n_lights,
+                    int32_t light_mode, const orc_medium* med, const orc_march* m,
+                    uint32_t frame_id, int64_t n_pix, const int64_t* pix,
+                    double* out_rgbt, float* out_depth, uint32_t* out_debug, double* out_margin,
+                    const int32_t* forced_hit, const int32_t* forced_term, int32_t no_clip_n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
