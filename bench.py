@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 guiding-map ray march (Algorithm 1) — see DESIGN.md §7.
+
+One *step* = one pass of the whole hot path over one batch: the volume
+layout (row a1, from the device-resident raw grid) plus the batched march of
+all frames of BASELINE.json configs[1] (C2: chimney plume 128^3, 60 frames of
+512x512, rotating camera, guide lights), rows a2-a9, in 3 kernel launches.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
+
+Multi-GPU (torchrun, one process per GPU): frames are independent, so each
+rank marches its own 60 frames (global frame ids rank + N*k, weak scaling)
+with no data-path collective; time = max over ranks of the device-timed loop.
+Rank 0 prints ONE JSON line.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "guiding-map rays/s and march samples/s; ms/frame at 512² over 128³; frames/s @1/2/4/8 GPU"
+CONFIG_TEXT = {
+    "C1": "C1: puff 64^3, 1 frame 128x128, guide lights",
+    "C2": "C2: chimney plume 128^3, 60 frames x 512x512, rotating camera, guide lights",
+    "C3": "C3: obstacle-carved plume 256^3, 60 frames x 1024x1024, moving light",
+    "C4": "C4: animated plume 256^3 (distinct volume per frame), 1024x1024, guide lights",
+    "C5": "C5: plume 512^3, 2048x2048 frames, guide lights",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="nsl", choices=["nsl", "reference"])
+    p.add_argument("--config", default="C2")
+    p.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
+    p.add_argument("--layout", default="quad_f32", choices=["linear_f32", "quad_f32", "corner_f16"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    REASONS = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+               "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons, self.max_mhz = index, [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: report nothing rather than guess
+            self.error = str(e)
+            return self
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for k, bit in self.REASONS.items():
+                        if r & bit and k != "gpu_idle":
+                            self.reasons.add(k)
+                except Exception:
+                    pass
+                time.sleep(0.02)
+
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "n_samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workload
+def rank_workload(cfg, rank, world, frames_per_rank):
+    """Weak scaling: rank r marches frames_per_rank frames with global ids r + world*k."""
+    import nsl_inputs as I
+    base = I.make_workload(cfg, frames=[0])
+    n_cfg = {"C1": 1, "C2": 60, "C3": 60, "C4": 240, "C5": 1024}[cfg]
+    F = frames_per_rank or n_cfg
+    gids = [rank + world * k for k in range(F)]
+    full = I.make_workload(cfg, frames=None) if cfg in ("C1", "C2", "C3") else None
+    if cfg in ("C2", "C3") or cfg == "C1":
+        # extend the camera/light path periodically to world*F global frames
+        idx = [g % n_cfg for g in gids]
+        w = full.subset(idx)
+        w.frame_ids = gids
+        return w
+    return I.make_workload(cfg, frames=[g % n_cfg for g in gids])
+
+
+def algorithmic_counts(nsl, w, vols, layout):
+    """Canonical march-sample counts from the debug counters (equal to the oracle's by parity),
+    plus the samples the kernel actually gathers (the C9 front-light shortcut skips the front march)."""
+    import torch
+    from dataclasses import replace
+    rgbt, depth, dbg = nsl.run_workload(w, layout=layout, debug=True, vols=vols)
+    torch.cuda.synchronize()
+    d = dbg.cpu().numpy().reshape(-1, 6).astype(np.int64)
+    prim = np.where(d[:, 0] > 0, d[:, 3] - d[:, 0] + 1, 0).sum()
+    light = d[:, 5].sum()
+    canonical = int(prim + light)
+    executed = canonical
+    if w.light_mode == 1 and w.cameras[0].projection == 0:
+        # front-light march lengths alone (n_lights = 1 guide = front only): skipped by C9 where n_lo >= 2
+        w1 = replace(w, lights=[row[:1] for row in w.lights], _cache=w._cache)
+        _, _, dbg1 = nsl.run_workload(w1, layout=layout, debug=True, vols=vols)
+        torch.cuda.synchronize()
+        d1 = dbg1.cpu().numpy().reshape(-1, 6).astype(np.int64)
+        executed = int(canonical - d1[d1[:, 0] >= 2, 5].sum())
+    occ = int(d[:, 4].sum())
+    return {"canonical_samples": canonical, "primary_samples": int(prim), "light_samples": int(light),
+            "executed_samples": executed, "occupied_samples": occ,
+            "pixels_in_support": int((d[:, 0] > 0).sum())}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def time_oracle(cfg, seconds, max_frames=None):
+    """The oracle, as it stands (single-threaded C), on whole frames of the workload until
+    ~`seconds` of CPU work; returns rays/s, samples/s and the sample description."""
+    import oracle
+    import nsl_inputs as I
+    w = I.make_workload(cfg, frames=[0])
+    n_cfg = {"C1": 1, "C2": 60, "C3": 60, "C4": 240, "C5": 1024}[cfg]
+    rays = samples = 0
+    t_total = 0.0
+    frames = []
+    stride = 4
+    f = 0
+    while (len(frames) < max_frames) if max_frames is not None else (t_total < seconds or not frames):
+        wf = I.make_workload(cfg, frames=[f % n_cfg])
+        if cfg in ("C4", "C5"):
+            pix = np.arange(0, wf.width * wf.height, 16 if cfg == "C4" else 64)
+        else:
+            pix = None
+        wf.volume(0)                        # generation is not oracle work
+        t0 = time.perf_counter()
+        r = oracle.run_workload_frame(wf, 0, pixels=pix)
+        dt = time.perf_counter() - t0
+        d = r["debug"].astype(np.int64)
+        samples += int(np.where(d[:, 0] > 0, d[:, 3] - d[:, 0] + 1, 0).sum() + d[:, 5].sum())
+        rays += len(r["pixels"])
+        t_total += dt
+        frames.append(f % n_cfg)
+        f += stride
+    desc = (f"oracle (plain C, fp64, 1 thread) on {len(frames)} frame(s) {frames[:6]}{'...' if len(frames) > 6 else ''}"
+            f" of {cfg}" + (" (pixel subsample)" if cfg in ("C4", "C5") else " (all pixels)"))
+    return {"rays_per_s": rays / t_total, "samples_per_s": samples / t_total, "seconds": t_total,
+            "sample": desc, "rays": rays}
+
+
+def host_cpu_name():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = args.config
+    for _ in range(args.warmup):
+        time_oracle(cfg, 0.0, max_frames=1)
+    res = time_oracle(cfg, 0.0, max_frames=max(1, args.steps))
+    v = res["rays_per_s"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "rays/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * res["seconds"] / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT[cfg], "reference": "CPU oracle (no upstream code exists)",
+                       "step": "one frame of the workload per step"},
+            "samples_per_s": res["samples_per_s"],
+            "cpu_baseline": {"value": v, "unit": "rays/s", "cores": 1, "kind": "oracle", "sample": res["sample"],
+                             "cpu": host_cpu_name()},
+            "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2604_03748_b200 as nsl
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    layout = nsl.LAYOUTS[args.layout]
+    cfg = args.config
+    w = rank_workload(cfg, rank, world, args.frames)
+    F, H, W = w.n_frames, w.height, w.width
+    stream = torch.cuda.current_stream()
+
+    # inputs resident in HBM before timing: raw density grids + layout storage + outputs
+    raw = [torch.from_numpy(w.volume(i)).cuda() for i in range(len(w.volume_specs))]
+    storage = [torch.empty(nsl.volume_bytes(w.grid, layout), dtype=torch.uint8, device="cuda") for _ in raw]
+    outputs = nsl.alloc_outputs(F, H, W, debug=False)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step():
+        vols = [nsl.Volume(w.grid, r, layout, storage=s) for r, s in zip(raw, storage)]       # a1
+        nsl.guiding_map_batch(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                              w.frame_ids, *outputs)                                           # a2-a9
+        return vols
+
+    vols = step()
+    torch.cuda.synchronize()
+    counts = algorithmic_counts(nsl, w, vols, layout)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = ClockSampler(local).start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(K):
+        flush.zero_()                       # L2 flushed between timed iterations (outside the events)
+        e0, e1, e2 = ev[i]
+        e0.record(stream)
+        vols = [nsl.Volume(w.grid, r, layout, storage=s) for r, s in zip(raw, storage)]
+        e1.record(stream)
+        nsl.guiding_map_batch(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                              w.frame_ids, *outputs)
+        e2.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(c) for a, b, c in ev]
+    march_ms = [b.elapsed_time(c) for a, b, c in ev]
+    layout_ms = [a.elapsed_time(b) for a, b, c in ev]
+    t_loop = sum(step_ms) / 1e3
+    if world > 1:
+        t = torch.tensor([t_loop], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_loop = float(t.item())
+    total_rays = W * H * F * world * K
+    value = total_rays / t_loop
+    ms_step = 1e3 * t_loop / K
+
+    # roofline of the dominant kernel (march_kernel): executed trilinear gathers x 32 B (fp32) or 16 B (fp16)
+    peaks = load_peaks()
+    bytes_per_sample = 16 if layout == 2 else 32
+    march_s = statistics.mean(march_ms) / 1e3
+    achieved = counts["executed_samples"] * bytes_per_sample / march_s / 1e9
+    sm_mhz = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e9          # GB/s: 148 SMs x 128 B/clk L1 x max SM clock
+    roof = {"bound": "l1tex", "achieved": achieved, "peak": l1_peak, "unit": "GB/s", "frac": achieved / l1_peak,
+            "traffic": None,
+            "peak_source": "derived: 148 SMs x 128 B/clk (B300_MICROARCH L1 line/cycle) x sm_max_mhz",
+            "kernel": "march_kernel", "kernel_ms": march_s * 1e3,
+            "algorithmic_bytes_per_launch": counts["executed_samples"] * bytes_per_sample,
+            "hbm_peak_gbs": peaks.get("hbm_gbs")}
+
+    line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16" if layout == 2 else "f32", "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT[cfg], "frames_per_rank": F, "frames_total": F * world,
+                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": args.layout,
+                       "l2": "flushed (512 MiB write) between timed steps, outside the events",
+                       "parallelism": f"frame-sharded x{world}, no data-path collective"},
+            "samples_per_s": counts["canonical_samples"] * world * K / t_loop,
+            "ms_per_frame": ms_step / F, "frames_per_s": F * world * K / t_loop,
+            "march_ms_per_step": statistics.mean(march_ms), "layout_ms_per_step": statistics.mean(layout_ms),
+            "counts_per_rank_step": counts, "gpu_launches": 3 * K, "clocks": clk, "roofline": roof}
+
+    # end-to-end through the public host API: pinned host density in, pinned host guiding maps out
+    if not args.no_e2e:
+        hd = torch.from_numpy(w.volume(0)).pin_memory() if len(raw) == 1 else None
+        if hd is not None:
+            hr = torch.empty((F, H, W, 4), dtype=torch.float32).pin_memory()
+            hdep = torch.empty((F, H, W), dtype=torch.float32).pin_memory()
+            for _ in range(max(1, args.warmup)):
+                nsl.guiding_map_host(w.grid, hd, layout, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                                     w.frame_ids, hr, hdep)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ke = max(1, min(K, 5))
+            es.record(stream)
+            for _ in range(ke):
+                nsl.guiding_map_host(w.grid, hd, layout, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                                     w.frame_ids, hr, hdep)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            te = es.elapsed_time(ee) / 1e3
+            if world > 1:
+                t = torch.tensor([te], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                te = float(t.item())
+            line["e2e"] = {"value": W * H * F * world * ke / te, "unit": "rays/s",
+                           "h2d_bytes_per_step": int(hd.numel() * 4 + F * (40 + 24 * w.n_lights + 8)),
+                           "d2h_bytes_per_step": int(hr.numel() * 4 + hdep.numel() * 4),
+                           "ms_per_step": 1e3 * te / ke, "api": "nsl_guiding_map_host"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res = time_oracle(cfg, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": res["rays_per_s"], "unit": "rays/s", "cores": 1, "kind": "oracle",
+                                "sample": res["sample"], "samples_per_s": res["samples_per_s"],
+                                "cpu": host_cpu_name(), "seconds": res["seconds"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

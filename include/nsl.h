@@ -1,0 +1,212 @@
+/* include/nsl.h — C ABI of the B200-native guiding-map ray march.
+ *
+ * Operation: Algorithm 1 of "Real-time Neural Six-way Lightmaps"
+ * (arXiv 2604.03748; "Ray-marching for Guiding Map
+ * L~_scattering"), with h = 10 dx on sigma_s "in a 3D texture" (L410) and
+ * the surrogate lights front = omega, top = omega x z, bottom = -omega x z of
+ * eq:approx (L361-365).  The precise canonical definition (C1-C14) that the
+ * kernels implement is DESIGN.md §2; each entry point below cites it.
+ *
+ * Conventions shared by every entry point
+ *   - Plain C; every function returns nsl_status and never aborts/throws.
+ *     On failure nsl_last_error() returns a thread-local message.
+ *   - Arguments are validated on the host BEFORE anything is enqueued;
+ *     invalid input -> NSL_ERR_INVALID_ARG, nothing enqueued.
+ *   - Device pointers are plain CUDA device addresses (e.g. torch tensors'
+ *     data_ptr()); `stream` is a cudaStream_t (nsl_stream is ABI-identical).
+ *     All device work is enqueued asynchronously on `stream`; asynchronous
+ *     device faults surface at the caller's next synchronisation.
+ *   - Host structs are read only during the call and never retained.
+ *   - Output buffers are caller-owned; the library never allocates outputs.
+ *     Transient per-call workspaces (frame tables) are taken from the
+ *     device's stream-ordered pool (cudaMallocAsync) and freed on `stream`.
+ *   - The current CUDA device is used; buffers must live on it.
+ */
+#ifndef NSL_H
+#define NSL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* nsl_stream;          /* == cudaStream_t */
+
+typedef enum {
+    NSL_OK = 0,
+    NSL_ERR_INVALID_ARG = 1,
+    NSL_ERR_UNSUPPORTED = 2,
+    NSL_ERR_OUT_OF_MEMORY = 3,
+    NSL_ERR_CUDA = 4
+} nsl_status;
+
+/* Thread-local text of the last non-OK status ("" if none). */
+const char* nsl_last_error(void);
+/* Library version string (static storage). */
+const char* nsl_version(void);
+
+/* ------------------------------------------------------------------ volume (row a1)
+ * Density grid sigma_s carrier ("smoke data sigma_s in a 3D
+ * texture"; C1): nx*ny*nz finite values >= 0,
+ * x-fastest, voxel (i,j,k) centred at origin + (i+.5, j+.5, k+.5)*voxel_width.
+ * Requires nx,ny,nz >= 1, voxel_width > 0, (nx+2)(ny+2)(nz+2) < 2^31. */
+typedef struct {
+    int32_t nx, ny, nz;
+    float origin[3];
+    float voxel_width;
+} nsl_grid_desc;
+
+/* Device layouts.  All carry the 1-voxel zero apron of C1.
+ *  LINEAR_F32 : (nx+2)(ny+2)(nz+2) floats, x-fastest (8 scalar gathers/sample)
+ *  QUAD_F32   : per padded cell (i,j,k), i<=nx, j<=ny, k<=nz+1, a float4 of the
+ *               x/y 2x2 corner quad (2 x 16-B gathers/sample), exact fp32 values
+ *  CORNER_F16 : per padded cell (i,j,k), i<=nx, j<=ny, k<=nz, all 8 corners as
+ *               fp16 (1 x 16-B gather/sample); values rounded RNE to fp16  */
+typedef enum {
+    NSL_LAYOUT_LINEAR_F32 = 0,
+    NSL_LAYOUT_QUAD_F32 = 1,
+    NSL_LAYOUT_CORNER_F16 = 2,
+    NSL_LAYOUT_DEFAULT = 1
+} nsl_layout;
+
+typedef struct nsl_volume nsl_volume;             /* opaque, immutable after upload */
+
+/* Device bytes the caller must provide as `device_storage` for `layout`
+ * (0 on invalid arguments). */
+size_t nsl_volume_bytes(const nsl_grid_desc* g, int32_t layout);
+
+/* Build the device layout from `density` (x-fastest nx*ny*nz floats) into the
+ * caller-owned `device_storage` (>= nsl_volume_bytes, 16-B aligned) on
+ * `stream`, and return a handle in *out.
+ *   density_on_device = 0: `density` is host memory (pinned or pageable);
+ *     values are validated on the host (finite, >= 0) before enqueueing.
+ *   density_on_device = 1: `density` is device memory; values are checked by
+ *     the layout kernel, and nsl_volume_check() reports the result.
+ * The handle does not own `device_storage`; the storage (and, for host
+ * input, nothing else) must outlive every call that reads the volume. */
+nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32_t density_on_device,
+                             int32_t layout, void* device_storage, size_t storage_bytes,
+                             nsl_stream stream, nsl_volume** out);
+/* Synchronises `stream` and reports whether the layout kernel saw a
+ * non-finite or negative input value (*n_invalid = count). */
+nsl_status nsl_volume_check(const nsl_volume* v, nsl_stream stream, uint64_t* n_invalid);
+/* Frees the handle (never the caller's storage).  NULL is a no-op. */
+nsl_status nsl_volume_release(nsl_volume* v);
+
+/* ------------------------------------------------------------------ frame parameters
+ * Camera (C3).  forward and up must be finite,
+ * |forward| within 1e-3 of 1 (renormalised), up not parallel to forward.
+ *   projection 0 = orthographic (billboard, canonical), 1 = perspective;
+ *   extent: ortho image-plane height (world units, > 0); persp 2*tan(fov_y/2).
+ *   position: ortho image-plane centre; persp eye. */
+typedef struct {
+    int32_t projection;
+    float position[3], forward[3], up[3];
+    float extent;
+    int32_t width, height;
+} nsl_camera;
+
+/* Directional light (eq:approx L_s): to_light unit (scene -> light,
+ * |.| within 1e-3 of 1), rgb radiance >= 0.  In guide mode to_light is
+ * ignored and derived from the camera (C3b). */
+typedef struct {
+    float to_light[3];
+    float rgb[3];
+} nsl_light;
+
+enum { NSL_LIGHTS_EXPLICIT = 0, NSL_LIGHTS_GUIDE = 1 };
+enum { NSL_OPACITY_EXP = 0, NSL_OPACITY_RIEMANN = 1, NSL_OPACITY_LITERAL = 2 };
+
+/* Medium (C2): sigma_t = extinction*rho, sigma_s = albedo*sigma_t;
+ * extinction >= 0, albedo in [0,1], hg_g in (-1,1) (HG phase). */
+typedef struct {
+    float extinction, albedo, hg_g;
+} nsl_medium;
+
+/* March parameters (Alg. 1 inputs "step size h, number of steps N", P:374;
+ * DESIGN.md C4-C13).  step > 0 (paper: 10*voxel_width); light_step
+ * >= 0 (0 -> step); max_steps >= 0 (0 -> to the support exit); depth_tau >= 0
+ * compared with sigma_s; t_min in [0,1) (0 = no early termination);
+ * opacity_form NSL_OPACITY_*; jitter 0/1; guide_axis: the world "z" of
+ * omega x z ((0,0,0) -> (0,0,1)); front_identity 0/1 allows the C9 shortcut. */
+typedef struct {
+    float step, light_step;
+    int32_t max_steps;
+    float depth_tau, t_min;
+    int32_t opacity_form;
+    int32_t jitter;
+    uint64_t seed;
+    float guide_axis[3];
+    int32_t front_identity;
+} nsl_march;
+
+/* ------------------------------------------------------------------ the march (rows a2-a8)
+ * One frame of Algorithm 1 for every pixel of cam (C3-C12).
+ *   lights: n_lights (1..4) entries; light_mode NSL_LIGHTS_* (guide: n_lights <= 3).
+ *   frame_id: jitter key (C4).
+ *   out_rgbt:  device, H*W float4 (L_r, L_g, L_b, T), row-major, row 0 = top, 16-B aligned
+ *   out_depth: device, H*W floats (D; 0 = no hit)
+ *   out_debug: device, H*W*6 u32 (n_lo, n_hi, n_hit, n_term, n_occ, light_samples) or NULL;
+ *              when non-NULL the C9 shortcut is disabled (counters are the canonical ones). */
+nsl_status nsl_guiding_map(const nsl_volume* vol, const nsl_camera* cam,
+                           const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                           const nsl_medium* med, const nsl_march* m, uint32_t frame_id,
+                           float* out_rgbt, float* out_depth, uint32_t* out_debug,
+                           nsl_stream stream);
+
+/* A batch of F independent frames in ONE launch (row a9; frames are
+ * independent, "streamed directly into the guiding map generation").
+ *   vols[n_vols]; frame_vol[F] indexes vols; cams[F] (all the same W, H);
+ *   lights[F*n_lights]; frame_ids[F] jitter keys (global frame ids, so that
+ *   sharded runs equal the unsharded one bit for bit).
+ *   out_rgbt F*H*W float4, out_depth F*H*W floats, out_debug F*H*W*6 u32 or NULL. */
+nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                                 const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
+                                 int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                                 const uint32_t* frame_ids, int32_t F,
+                                 float* out_rgbt, float* out_depth, uint32_t* out_debug,
+                                 nsl_stream stream);
+
+/* End-to-end convenience call with HOST buffers: uploads the host density
+ * grid, lays it out, marches the F frames and copies the results back into
+ * host out_rgbt (F*H*W*4 floats) / out_depth (F*H*W floats); synchronises
+ * `stream` before returning.  All device memory is transient (stream-ordered
+ * pool).  Host buffers may be pageable; pinned memory makes the copies
+ * asynchronous DMA. */
+nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_density, int32_t layout,
+                                const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
+                                int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                                const uint32_t* frame_ids, int32_t F,
+                                float* host_rgbt, float* host_depth, nsl_stream stream);
+
+/* ------------------------------------------------------------------ debug / verification
+ * Frame constants of DESIGN.md C3/C3b/C10 as the device computes them
+ * (fp64 evaluation rounded once to fp32), for bitwise comparison with the
+ * oracle (pin P15).  Synchronises `stream`; `out` is host memory. */
+typedef struct {
+    float inv_dx;
+    float B[3], Ex[3], Ey[3], Dg[3];
+    float Oe[3], F0[3];
+    float fwd[3];
+    float Ln[4][3];
+    float Lg[4][3];
+    float P[4];
+    int32_t front_identity_ok;
+} nsl_frame_constants;
+
+nsl_status nsl_debug_frame_constants(const nsl_grid_desc* g, const nsl_camera* cam,
+                                     const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                                     const nsl_medium* med, const nsl_march* m,
+                                     nsl_frame_constants* out, nsl_stream stream);
+
+/* The C4 jitter chain on the device: for pixels 0..n-1 of a row-major
+ * image, out_hash[p] = h32, out_delta[p] = delta (device buffers). */
+nsl_status nsl_debug_jitter(const nsl_march* m, uint32_t frame_id, int32_t n,
+                            uint32_t* out_hash, float* out_delta, nsl_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSL_H */

@@ -1,0 +1,315 @@
+"""paper_2604_03748_b200 — B200-native guiding-map ray march (Neural Six-way
+Lightmaps, arXiv 2604.03748, Algorithm 1).
+
+Thin ctypes binding over the C-ABI library ``lib/libnsl.so`` declared in
+``include/nsl.h``: argument marshalling only.  Every step of the path runs in
+the library's CUDA kernels (csrc/*.cu, sm_100a).  PyTorch supplies device
+memory, the current CUDA stream and (in ``parallel``) torch.distributed.
+There is NO CPU fallback: if the library is missing or cannot be loaded the
+calls raise ``NslError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+LIB_PATH = os.path.join(_HERE, "lib", "libnsl.so")
+CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu")]
+HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_ROOT, "include", "nsl.h")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+
+LAYOUT_LINEAR_F32, LAYOUT_QUAD_F32, LAYOUT_CORNER_F16 = 0, 1, 2
+LAYOUT_DEFAULT = LAYOUT_QUAD_F32
+LAYOUTS = {"linear_f32": 0, "quad_f32": 1, "corner_f16": 2}
+LIGHTS_EXPLICIT, LIGHTS_GUIDE = 0, 1
+
+
+class NslError(RuntimeError):
+    pass
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libnsl.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    newest = max(os.path.getmtime(p) for p in CSRC + HEADERS)
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        cmd = ["nvcc", *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", LIB_PATH, *CSRC]
+        subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+# ---------------------------------------------------------------- ABI structs (include/nsl.h)
+class GridDesc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("origin", ctypes.c_float * 3), ("voxel_width", ctypes.c_float)]
+
+
+class CameraS(ctypes.Structure):
+    _fields_ = [("projection", ctypes.c_int32), ("position", ctypes.c_float * 3),
+                ("forward", ctypes.c_float * 3), ("up", ctypes.c_float * 3), ("extent", ctypes.c_float),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class LightS(ctypes.Structure):
+    _fields_ = [("to_light", ctypes.c_float * 3), ("rgb", ctypes.c_float * 3)]
+
+
+class MediumS(ctypes.Structure):
+    _fields_ = [("extinction", ctypes.c_float), ("albedo", ctypes.c_float), ("hg_g", ctypes.c_float)]
+
+
+class MarchS(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_float), ("light_step", ctypes.c_float), ("max_steps", ctypes.c_int32),
+                ("depth_tau", ctypes.c_float), ("t_min", ctypes.c_float), ("opacity_form", ctypes.c_int32),
+                ("jitter", ctypes.c_int32), ("seed", ctypes.c_uint64), ("guide_axis", ctypes.c_float * 3),
+                ("front_identity", ctypes.c_int32)]
+
+
+class FrameConstantsS(ctypes.Structure):
+    _fields_ = [("inv_dx", ctypes.c_float), ("B", ctypes.c_float * 3), ("Ex", ctypes.c_float * 3),
+                ("Ey", ctypes.c_float * 3), ("Dg", ctypes.c_float * 3), ("Oe", ctypes.c_float * 3),
+                ("F0", ctypes.c_float * 3), ("fwd", ctypes.c_float * 3), ("Ln", (ctypes.c_float * 3) * 4),
+                ("Lg", (ctypes.c_float * 3) * 4), ("P", ctypes.c_float * 4), ("front_identity_ok", ctypes.c_int32)]
+
+
+EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_upload", "nsl_volume_check",
+           "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_host",
+           "nsl_debug_frame_constants", "nsl_debug_jitter"]
+
+_lib = None
+
+
+def lib():
+    """Load libnsl.so (raises NslError if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NslError(f"{LIB_PATH} not built; run __graft_entry__.build() (no CPU fallback exists)")
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as e:
+        raise NslError(f"cannot load {LIB_PATH}: {e}") from e
+    P, vp, i32, u32 = ctypes.POINTER, ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32
+    L.nsl_last_error.restype = ctypes.c_char_p
+    L.nsl_version.restype = ctypes.c_char_p
+    L.nsl_volume_bytes.argtypes = [P(GridDesc), i32]
+    L.nsl_volume_bytes.restype = ctypes.c_size_t
+    L.nsl_volume_upload.argtypes = [P(GridDesc), vp, i32, i32, vp, ctypes.c_size_t, vp, P(vp)]
+    L.nsl_volume_check.argtypes = [vp, vp, P(ctypes.c_uint64)]
+    L.nsl_volume_release.argtypes = [vp]
+    L.nsl_guiding_map.argtypes = [vp, P(CameraS), P(LightS), i32, i32, P(MediumS), P(MarchS), u32,
+                                  vp, vp, vp, vp]
+    L.nsl_guiding_map_batch.argtypes = [P(vp), i32, P(i32), P(CameraS), P(LightS), i32, i32, P(MediumS),
+                                        P(MarchS), P(u32), i32, vp, vp, vp, vp]
+    L.nsl_guiding_map_host.argtypes = [P(GridDesc), vp, i32, P(CameraS), P(LightS), i32, i32, P(MediumS),
+                                       P(MarchS), P(u32), i32, vp, vp, vp]
+    L.nsl_debug_frame_constants.argtypes = [P(GridDesc), P(CameraS), P(LightS), i32, i32, P(MediumS),
+                                            P(MarchS), P(FrameConstantsS), vp]
+    L.nsl_debug_jitter.argtypes = [P(MarchS), u32, i32, vp, vp, vp]
+    for name in EXPORTS[2:]:
+        if name != "nsl_volume_bytes":
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def version() -> str:
+    return lib().nsl_version().decode()
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().nsl_last_error().decode()
+        raise NslError(f"{what} failed (status {rc}): {msg}")
+
+
+# ---------------------------------------------------------------- marshalling
+def _f3(v):
+    return (ctypes.c_float * 3)(*[float(x) for x in v])
+
+
+def grid_desc(g) -> GridDesc:
+    return GridDesc(g.nx, g.ny, g.nz, _f3(g.origin), g.voxel_width)
+
+
+def camera_s(c) -> CameraS:
+    return CameraS(c.projection, _f3(c.position), _f3(c.forward), _f3(c.up), c.extent, c.width, c.height)
+
+
+def lights_s(rows) -> ctypes.Array:
+    """rows: list (frames) of lists (lights) of objects with to_light/rgb -> flat LightS array."""
+    flat = [l for row in rows for l in row]
+    arr = (LightS * len(flat))()
+    for i, l in enumerate(flat):
+        arr[i].to_light = _f3(l.to_light)
+        arr[i].rgb = _f3(l.rgb)
+    return arr
+
+
+def medium_s(m) -> MediumS:
+    return MediumS(m.extinction, m.albedo, m.hg_g)
+
+
+def march_s(m) -> MarchS:
+    return MarchS(m.step, m.light_step, m.max_steps, m.depth_tau, m.t_min, m.opacity_form, m.jitter,
+                  m.seed & 0xFFFFFFFFFFFFFFFF, _f3(m.guide_axis), getattr(m, "front_identity", 1))
+
+
+def _stream_handle(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def volume_bytes(grid, layout: int = LAYOUT_DEFAULT) -> int:
+    n = lib().nsl_volume_bytes(ctypes.byref(grid_desc(grid)), layout)
+    if n == 0:
+        raise NslError("nsl_volume_bytes: invalid grid/layout")
+    return n
+
+
+class Volume:
+    """A device volume in a sampler layout (row a1).  Owns its storage tensor."""
+
+    def __init__(self, grid, density, layout: int = LAYOUT_DEFAULT, stream=None, storage=None):
+        import torch
+        self.grid = grid
+        self.layout = layout
+        nbytes = volume_bytes(grid, layout)
+        if storage is None:
+            storage = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        assert storage.numel() >= nbytes and storage.is_cuda
+        self.storage = storage
+        self._density = density                       # keep the source alive until the copy is done
+        on_dev = 1 if (hasattr(density, "is_cuda") and density.is_cuda) else 0
+        if hasattr(density, "data_ptr"):
+            assert density.dtype == torch.float32 and density.is_contiguous()
+            ptr = density.data_ptr()
+        else:
+            import numpy as np
+            assert density.dtype == np.float32 and density.flags["C_CONTIGUOUS"]
+            ptr = density.ctypes.data
+        h = ctypes.c_void_p()
+        _check(lib().nsl_volume_upload(ctypes.byref(grid_desc(grid)), ptr, on_dev, layout,
+                                       storage.data_ptr(), storage.numel(), _stream_handle(stream),
+                                       ctypes.byref(h)), "nsl_volume_upload")
+        self.handle = h
+
+    def check(self, stream=None) -> int:
+        n = ctypes.c_uint64()
+        _check(lib().nsl_volume_check(self.handle, _stream_handle(stream), ctypes.byref(n)), "nsl_volume_check")
+        return n.value
+
+    def release(self):
+        if getattr(self, "handle", None) is not None and _lib is not None:
+            _lib.nsl_volume_release(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def guiding_map(vol: Volume, cam, lights, light_mode, medium, march, frame_id: int, out_rgbt, out_depth,
+                out_debug=None, stream=None):
+    """One frame (rows a2-a8).  out_rgbt: cuda float32 [H,W,4]; out_depth [H,W]; out_debug [H,W,6] int32 or None."""
+    ls = lights_s([lights])
+    _check(lib().nsl_guiding_map(vol.handle, ctypes.byref(camera_s(cam)), ls, len(lights), light_mode,
+                                 ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)), frame_id,
+                                 _ptr(out_rgbt), _ptr(out_depth), _ptr(out_debug), _stream_handle(stream)),
+           "nsl_guiding_map")
+
+
+def guiding_map_batch(vols: Sequence[Volume], frame_vol: Sequence[int], cams, lights, light_mode, medium, march,
+                      frame_ids: Sequence[int], out_rgbt, out_depth, out_debug=None, stream=None):
+    """F frames in one launch (row a9).  lights: F rows of n_lights.  Outputs [F,H,W,4], [F,H,W], [F,H,W,6]."""
+    F = len(cams)
+    n_l = len(lights[0])
+    hv = (ctypes.c_void_p * len(vols))(*[v.handle.value for v in vols])
+    fv = (ctypes.c_int32 * F)(*frame_vol)
+    cs = (CameraS * F)(*[camera_s(c) for c in cams])
+    fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+    _check(lib().nsl_guiding_map_batch(hv, len(vols), fv, cs, lights_s(lights), n_l, light_mode,
+                                       ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)), fid, F,
+                                       _ptr(out_rgbt), _ptr(out_depth), _ptr(out_debug), _stream_handle(stream)),
+           "nsl_guiding_map_batch")
+
+
+def guiding_map_host(grid, host_density, layout, cams, lights, light_mode, medium, march, frame_ids,
+                     host_rgbt, host_depth, stream=None):
+    """End-to-end with HOST buffers (torch CPU tensors, pinned for async DMA): upload + layout + march + download."""
+    F = len(cams)
+    cs = (CameraS * F)(*[camera_s(c) for c in cams])
+    fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+    _check(lib().nsl_guiding_map_host(ctypes.byref(grid_desc(grid)), host_density.data_ptr(), layout, cs,
+                                      lights_s(lights), len(lights[0]), light_mode, ctypes.byref(medium_s(medium)),
+                                      ctypes.byref(march_s(march)), fid, F, host_rgbt.data_ptr(),
+                                      host_depth.data_ptr(), _stream_handle(stream)), "nsl_guiding_map_host")
+
+
+def debug_frame_constants(grid, cam, lights, light_mode, medium, march, stream=None) -> dict:
+    import numpy as np
+    out = FrameConstantsS()
+    _check(lib().nsl_debug_frame_constants(ctypes.byref(grid_desc(grid)), ctypes.byref(camera_s(cam)),
+                                           lights_s([lights]), len(lights), light_mode,
+                                           ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)),
+                                           ctypes.byref(out), _stream_handle(stream)), "nsl_debug_frame_constants")
+    n = len(lights)
+    return {"inv_dx": np.float32(out.inv_dx),
+            "B": np.array(out.B, np.float32), "Ex": np.array(out.Ex, np.float32),
+            "Ey": np.array(out.Ey, np.float32), "Dg": np.array(out.Dg, np.float32),
+            "Oe": np.array(out.Oe, np.float32), "F0": np.array(out.F0, np.float32),
+            "fwd": np.array(out.fwd, np.float32),
+            "Ln": np.array([list(out.Ln[i]) for i in range(n)], np.float32),
+            "Lg": np.array([list(out.Lg[i]) for i in range(n)], np.float32),
+            "P": np.array(list(out.P)[:n], np.float32), "front_identity_ok": out.front_identity_ok}
+
+
+def debug_jitter(march, frame_id: int, out_hash, out_delta, stream=None):
+    _check(lib().nsl_debug_jitter(ctypes.byref(march_s(march)), frame_id, out_hash.numel(), out_hash.data_ptr(),
+                                  out_delta.data_ptr(), _stream_handle(stream)), "nsl_debug_jitter")
+
+
+# ---------------------------------------------------------------- workload driver (marshalling only)
+def upload_workload_volumes(w, layout: int = LAYOUT_DEFAULT, vol_indices=None, stream=None) -> List[Volume]:
+    """Upload the workload's distinct volumes (host -> device layout kernel)."""
+    import torch
+    idx = range(len(w.volume_specs)) if vol_indices is None else vol_indices
+    vols = []
+    for i in idx:
+        d = torch.from_numpy(w.volume(i)).cuda(non_blocking=False)
+        vols.append(Volume(w.grid, d, layout, stream=stream))
+    return vols
+
+
+def alloc_outputs(F: int, H: int, W: int, debug: bool = False):
+    import torch
+    rgbt = torch.empty((F, H, W, 4), dtype=torch.float32, device="cuda")
+    depth = torch.empty((F, H, W), dtype=torch.float32, device="cuda")
+    dbg = torch.empty((F, H, W, 6), dtype=torch.int32, device="cuda") if debug else None
+    return rgbt, depth, dbg
+
+
+def run_workload(w, layout: int = LAYOUT_DEFAULT, debug: bool = False, vols=None, outputs=None, march=None,
+                 stream=None):
+    """March every frame of an nsl_inputs.Workload in one batched call; returns (rgbt, depth, debug)."""
+    if vols is None:
+        vols = upload_workload_volumes(w, layout, stream=stream)
+    if outputs is None:
+        outputs = alloc_outputs(w.n_frames, w.height, w.width, debug)
+    rgbt, depth, dbg = outputs
+    guiding_map_batch(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, march or w.march,
+                      w.frame_ids, rgbt, depth, dbg, stream=stream)
+    return rgbt, depth, dbg

@@ -1,0 +1,421 @@
+// capi.cu — the C ABI of include/nsl.h: argument validation, volume handles,
+// per-call frame tables, kernel dispatch.  Host code only; every step of the
+// guiding-map path runs in the kernels of volume.cu / setup.cu / march.cu.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nsl_internal.cuh"
+
+using namespace nsl;
+
+struct nsl_volume {
+    nsl_grid_desc g;
+    int32_t layout;
+    void* data;                       // caller-owned storage
+    unsigned long long* invalid;      // counter in the storage tail
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+nsl_status fail(nsl_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+nsl_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(e == cudaErrorMemoryAllocation ? NSL_ERR_OUT_OF_MEMORY : NSL_ERR_CUDA, "%s: %s", what,
+                cudaGetErrorString(e));
+}
+
+#define NSL_CUDA(call, what)                       \
+    do {                                           \
+        cudaError_t e_ = (call);                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+bool finite3(const float v[3]) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
+double norm3(const float v[3]) {
+    return std::sqrt((double)v[0] * v[0] + (double)v[1] * v[1] + (double)v[2] * v[2]);
+}
+
+constexpr size_t kTail = 256;  // counter area after the layout (keeps 16-B alignment)
+
+size_t body_bytes(const nsl_grid_desc* g, int layout) {
+    return layout_elems(layout, g->nx, g->ny, g->nz) * layout_elem_bytes(layout);
+}
+
+nsl_status check_grid(const nsl_grid_desc* g) {
+    if (!g) return fail(NSL_ERR_INVALID_ARG, "grid descriptor is NULL");
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1) return fail(NSL_ERR_INVALID_ARG, "grid dims must be >= 1");
+    if (!(g->voxel_width > 0.0f) || !std::isfinite(g->voxel_width))
+        return fail(NSL_ERR_INVALID_ARG, "voxel_width must be finite and > 0");
+    if (!finite3(g->origin)) return fail(NSL_ERR_INVALID_ARG, "grid origin must be finite");
+    double cells = (double)(g->nx + 2) * (g->ny + 2) * (g->nz + 2);
+    if (cells >= 2147483647.0) return fail(NSL_ERR_UNSUPPORTED, "grid too large for 32-bit indexing");
+    return NSL_OK;
+}
+
+nsl_status check_layout(int layout) {
+    if (layout != kLinearF32 && layout != kQuadF32 && layout != kCornerF16)
+        return fail(NSL_ERR_INVALID_ARG, "unknown layout %d", layout);
+    return NSL_OK;
+}
+
+nsl_status check_camera(const nsl_camera* c, int idx) {
+    if (c->projection != 0 && c->projection != 1) return fail(NSL_ERR_INVALID_ARG, "camera[%d]: bad projection", idx);
+    if (c->width < 1 || c->height < 1) return fail(NSL_ERR_INVALID_ARG, "camera[%d]: width/height must be >= 1", idx);
+    if ((double)c->width * c->height >= 2147483647.0)
+        return fail(NSL_ERR_UNSUPPORTED, "camera[%d]: image too large", idx);
+    if (!finite3(c->position) || !finite3(c->forward) || !finite3(c->up))
+        return fail(NSL_ERR_INVALID_ARG, "camera[%d]: non-finite vector", idx);
+    if (!(c->extent > 0.0f) || !std::isfinite(c->extent))
+        return fail(NSL_ERR_INVALID_ARG, "camera[%d]: extent must be finite and > 0", idx);
+    double nf = norm3(c->forward);
+    if (std::fabs(nf - 1.0) > 1e-3) return fail(NSL_ERR_INVALID_ARG, "camera[%d]: |forward| = %g is not unit", idx, nf);
+    double nu = norm3(c->up);
+    if (!(nu > 0.0)) return fail(NSL_ERR_INVALID_ARG, "camera[%d]: up is zero", idx);
+    double cx = (double)c->forward[1] * c->up[2] - (double)c->forward[2] * c->up[1];
+    double cy = (double)c->forward[2] * c->up[0] - (double)c->forward[0] * c->up[2];
+    double cz = (double)c->forward[0] * c->up[1] - (double)c->forward[1] * c->up[0];
+    if (std::sqrt(cx * cx + cy * cy + cz * cz) < 1e-4 * nf * nu)
+        return fail(NSL_ERR_INVALID_ARG, "camera[%d]: up is parallel to forward", idx);
+    return NSL_OK;
+}
+
+nsl_status check_lights(const nsl_light* l, int n, int mode, int idx) {
+    for (int i = 0; i < n; ++i) {
+        if (!finite3(l[i].rgb) || l[i].rgb[0] < 0 || l[i].rgb[1] < 0 || l[i].rgb[2] < 0)
+            return fail(NSL_ERR_INVALID_ARG, "light[%d][%d]: rgb must be finite and >= 0", idx, i);
+        if (mode == NSL_LIGHTS_EXPLICIT) {
+            if (!finite3(l[i].to_light)) return fail(NSL_ERR_INVALID_ARG, "light[%d][%d]: non-finite direction", idx, i);
+            double nl = norm3(l[i].to_light);
+            if (std::fabs(nl - 1.0) > 1e-3)
+                return fail(NSL_ERR_INVALID_ARG, "light[%d][%d]: |to_light| = %g is not unit", idx, i, nl);
+        }
+    }
+    return NSL_OK;
+}
+
+nsl_status check_common(const nsl_light* lights, int n_lights, int light_mode, const nsl_medium* med,
+                        const nsl_march* m) {
+    if (!lights) return fail(NSL_ERR_INVALID_ARG, "lights is NULL");
+    if (!med || !m) return fail(NSL_ERR_INVALID_ARG, "medium/march is NULL");
+    if (light_mode != NSL_LIGHTS_EXPLICIT && light_mode != NSL_LIGHTS_GUIDE)
+        return fail(NSL_ERR_INVALID_ARG, "bad light_mode %d", light_mode);
+    if (n_lights < 1 || n_lights > 4) return fail(NSL_ERR_INVALID_ARG, "n_lights must be in [1,4]");
+    if (light_mode == NSL_LIGHTS_GUIDE && n_lights > 3) return fail(NSL_ERR_INVALID_ARG, "guide set has at most 3 lights");
+    if (!(med->extinction >= 0.0f) || !std::isfinite(med->extinction))
+        return fail(NSL_ERR_INVALID_ARG, "extinction must be finite and >= 0");
+    if (!(med->albedo >= 0.0f && med->albedo <= 1.0f)) return fail(NSL_ERR_INVALID_ARG, "albedo must be in [0,1]");
+    if (!(med->hg_g > -1.0f && med->hg_g < 1.0f)) return fail(NSL_ERR_INVALID_ARG, "hg_g must be in (-1,1)");
+    if (!(m->step > 0.0f) || !std::isfinite(m->step)) return fail(NSL_ERR_INVALID_ARG, "step must be finite and > 0");
+    if (!(m->light_step >= 0.0f) || !std::isfinite(m->light_step))
+        return fail(NSL_ERR_INVALID_ARG, "light_step must be finite and >= 0");
+    if (m->max_steps < 0 || m->max_steps > (1 << 24)) return fail(NSL_ERR_INVALID_ARG, "max_steps out of range");
+    if (!(m->depth_tau >= 0.0f) || !std::isfinite(m->depth_tau))
+        return fail(NSL_ERR_INVALID_ARG, "depth_tau must be finite and >= 0");
+    if (!(m->t_min >= 0.0f && m->t_min < 1.0f)) return fail(NSL_ERR_INVALID_ARG, "t_min must be in [0,1)");
+    if (m->opacity_form < 0 || m->opacity_form > 2) return fail(NSL_ERR_INVALID_ARG, "bad opacity_form");
+    if (m->jitter != 0 && m->jitter != 1) return fail(NSL_ERR_INVALID_ARG, "jitter must be 0 or 1");
+    if (!finite3(m->guide_axis)) return fail(NSL_ERR_INVALID_ARG, "guide_axis must be finite");
+    return NSL_OK;
+}
+
+MarchConst make_const(int n_lights, int light_mode, const nsl_medium* med, const nsl_march* m) {
+    MarchConst mc;
+    mc.h = m->step;
+    mc.hl = m->light_step > 0.0f ? m->light_step : m->step;
+    mc.tau_d = m->depth_tau;
+    mc.t_min = m->t_min;
+    mc.kappa = med->extinction;
+    mc.alpha = med->albedo;
+    mc.g = med->hg_g;
+    mc.Ncap = m->max_steps > 0 ? m->max_steps : (1 << 24);
+    mc.form = m->opacity_form;
+    mc.jitter = m->jitter;
+    mc.n_lights = n_lights;
+    mc.light_mode = light_mode;
+    mc.seed_lo = (uint32_t)(m->seed & 0xffffffffu);
+    mc.seed_hi = (uint32_t)(m->seed >> 32);
+    mc.front_identity = m->front_identity ? 1 : 0;
+    mc.axis[0] = m->guide_axis[0];
+    mc.axis[1] = m->guide_axis[1];
+    mc.axis[2] = m->guide_axis[2];
+    return mc;
+}
+
+VolDesc desc_of(const nsl_volume* v) {
+    VolDesc d;
+    d.data = v->data;
+    d.nx = v->g.nx;
+    d.ny = v->g.ny;
+    d.nz = v->g.nz;
+    d.layout = v->layout;
+    d.origin[0] = v->g.origin[0];
+    d.origin[1] = v->g.origin[1];
+    d.origin[2] = v->g.origin[2];
+    d.dx = v->g.voxel_width;
+    return d;
+}
+
+// Frame tables: FrameIn[F] | lights[F*nl] | FrameParams[F] in one stream-ordered allocation.
+struct Workspace {
+    void* base = nullptr;
+    FrameIn* in = nullptr;
+    nsl_light* lights = nullptr;
+    FrameParams* params = nullptr;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
+                        const MarchConst& mc, cudaStream_t s, Workspace& ws) {
+    const int F = (int)frames.size();
+    const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
+    const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
+    const size_t b_p = sizeof(FrameParams) * F;
+    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_p, s), "cudaMallocAsync(frame tables)");
+    ws.in = reinterpret_cast<FrameIn*>(ws.base);
+    ws.lights = reinterpret_cast<nsl_light*>(static_cast<char*>(ws.base) + b_in);
+    ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l);
+    std::vector<char> host(b_in + b_l);
+    memcpy(host.data(), frames.data(), sizeof(FrameIn) * F);
+    memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
+    NSL_CUDA(cudaMemcpyAsync(ws.base, host.data(), host.size(), cudaMemcpyHostToDevice, s), "frame table upload");
+    NSL_CUDA(launch_frame_setup(ws.in, ws.lights, F, mc, ws.params, s), "frame_setup_kernel launch");
+    return NSL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nsl_last_error(void) { return g_err.c_str(); }
+const char* nsl_version(void) { return "nsl-b200 0.1 (sm_100a)"; }
+
+size_t nsl_volume_bytes(const nsl_grid_desc* g, int32_t layout) {
+    if (check_grid(g) != NSL_OK || check_layout(layout) != NSL_OK) return 0;
+    return align_up(body_bytes(g, layout), 256) + kTail;
+}
+
+nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32_t density_on_device, int32_t layout,
+                             void* device_storage, size_t storage_bytes, nsl_stream stream, nsl_volume** out) {
+    g_err.clear();
+    if (nsl_status st = check_grid(g)) return st;
+    if (nsl_status st = check_layout(layout)) return st;
+    if (!density || !device_storage || !out) return fail(NSL_ERR_INVALID_ARG, "NULL density/storage/out");
+    if (reinterpret_cast<uintptr_t>(device_storage) % 16) return fail(NSL_ERR_INVALID_ARG, "storage must be 16-B aligned");
+    const size_t need = nsl_volume_bytes(g, layout);
+    if (storage_bytes < need) return fail(NSL_ERR_INVALID_ARG, "storage_bytes %zu < required %zu", storage_bytes, need);
+    const size_t n = (size_t)g->nx * g->ny * g->nz;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!density_on_device) {
+        for (size_t i = 0; i < n; ++i)
+            if (!(density[i] >= 0.0f) || !std::isfinite(density[i]))
+                return fail(NSL_ERR_INVALID_ARG, "density[%zu] = %g is not finite and >= 0", i, (double)density[i]);
+    }
+    nsl_volume* v = new nsl_volume;
+    v->g = *g;
+    v->layout = layout;
+    v->data = device_storage;
+    v->invalid = reinterpret_cast<unsigned long long*>(static_cast<char*>(device_storage) + align_up(body_bytes(g, layout), 256));
+    auto bail = [&](nsl_status st) { delete v; return st; };
+    cudaError_t e = cudaMemsetAsync(v->invalid, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemsetAsync"));
+    const float* raw = density;
+    void* staging = nullptr;
+    if (!density_on_device) {
+        e = cudaMallocAsync(&staging, n * sizeof(float), s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMallocAsync(staging)"));
+        e = cudaMemcpyAsync(staging, density, n * sizeof(float), cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "density upload"));
+        raw = static_cast<const float*>(staging);
+    }
+    e = launch_layout(raw, desc_of(v), device_storage, v->invalid, s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "layout kernel launch"));
+    if (staging) {
+        e = cudaFreeAsync(staging, s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaFreeAsync(staging)"));
+    }
+    *out = v;
+    return NSL_OK;
+}
+
+nsl_status nsl_volume_check(const nsl_volume* v, nsl_stream stream, uint64_t* n_invalid) {
+    g_err.clear();
+    if (!v || !n_invalid) return fail(NSL_ERR_INVALID_ARG, "NULL volume/out");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    unsigned long long h = 0;
+    NSL_CUDA(cudaMemcpyAsync(&h, v->invalid, sizeof h, cudaMemcpyDeviceToHost, s), "invalid counter read");
+    NSL_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    *n_invalid = h;
+    return NSL_OK;
+}
+
+nsl_status nsl_volume_release(nsl_volume* v) {
+    delete v;
+    return NSL_OK;
+}
+
+nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                                 const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                                 const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                                 float* out_rgbt, float* out_depth, uint32_t* out_debug, nsl_stream stream) {
+    g_err.clear();
+    if (F < 1 || F > 65535) return fail(NSL_ERR_INVALID_ARG, "F must be in [1, 65535]");
+    if (!vols || n_vols < 1 || !frame_vol || !cams || !frame_ids)
+        return fail(NSL_ERR_INVALID_ARG, "NULL vols/frame_vol/cams/frame_ids");
+    if (!out_rgbt || !out_depth) return fail(NSL_ERR_INVALID_ARG, "NULL output");
+    if (reinterpret_cast<uintptr_t>(out_rgbt) % 16) return fail(NSL_ERR_INVALID_ARG, "out_rgbt must be 16-B aligned");
+    if (nsl_status st = check_common(lights, n_lights, light_mode, med, m)) return st;
+    for (int i = 0; i < n_vols; ++i)
+        if (!vols[i]) return fail(NSL_ERR_INVALID_ARG, "vols[%d] is NULL", i);
+    const int layout = vols[0]->layout;
+    for (int i = 1; i < n_vols; ++i)
+        if (vols[i]->layout != layout) return fail(NSL_ERR_UNSUPPORTED, "all volumes of a batch must share a layout");
+    const int W = cams[0].width, H = cams[0].height, proj = cams[0].projection;
+    std::vector<FrameIn> frames((size_t)F);
+    for (int f = 0; f < F; ++f) {
+        if (nsl_status st = check_camera(&cams[f], f)) return st;
+        if (cams[f].width != W || cams[f].height != H) return fail(NSL_ERR_INVALID_ARG, "camera[%d]: size differs", f);
+        if (cams[f].projection != proj) return fail(NSL_ERR_UNSUPPORTED, "camera[%d]: mixed projections", f);
+        if (frame_vol[f] < 0 || frame_vol[f] >= n_vols) return fail(NSL_ERR_INVALID_ARG, "frame_vol[%d] out of range", f);
+        if (nsl_status st = check_lights(lights + (size_t)f * n_lights, n_lights, light_mode, f)) return st;
+        FrameIn& fi = frames[f];
+        memset(&fi, 0, sizeof fi);
+        fi.cam = cams[f];
+        fi.vol = desc_of(vols[frame_vol[f]]);
+        fi.frame_id = frame_ids[f];
+    }
+    const MarchConst mc = make_const(n_lights, light_mode, med, m);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Workspace ws;
+    if (nsl_status st = build_frames(frames, lights, n_lights, mc, s, ws)) return st;
+    cudaError_t e = launch_march(ws.params, mc, F, W, H, proj, layout, reinterpret_cast<float4*>(out_rgbt), out_depth,
+                                 out_debug, s);
+    cudaError_t e2 = cudaFreeAsync(ws.base, s);
+    if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(frame tables)");
+    return NSL_OK;
+}
+
+nsl_status nsl_guiding_map(const nsl_volume* vol, const nsl_camera* cam, const nsl_light* lights, int32_t n_lights,
+                           int32_t light_mode, const nsl_medium* med, const nsl_march* m, uint32_t frame_id,
+                           float* out_rgbt, float* out_depth, uint32_t* out_debug, nsl_stream stream) {
+    if (!vol || !cam) {
+        g_err = "NULL volume/camera";
+        return NSL_ERR_INVALID_ARG;
+    }
+    const int32_t zero = 0;
+    return nsl_guiding_map_batch(&vol, 1, &zero, cam, lights, n_lights, light_mode, med, m, &frame_id, 1, out_rgbt,
+                                 out_depth, out_debug, stream);
+}
+
+nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_density, int32_t layout,
+                                const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                                const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                                float* host_rgbt, float* host_depth, nsl_stream stream) {
+    g_err.clear();
+    if (nsl_status st = check_grid(g)) return st;
+    if (nsl_status st = check_layout(layout)) return st;
+    if (!host_density || !cams || !host_rgbt || !host_depth) return fail(NSL_ERR_INVALID_ARG, "NULL host buffer");
+    if (F < 1) return fail(NSL_ERR_INVALID_ARG, "F must be >= 1");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t vb = nsl_volume_bytes(g, layout);
+    const size_t npix = (size_t)F * cams[0].width * cams[0].height;
+    void *vstore = nullptr, *dout = nullptr;
+    NSL_CUDA(cudaMallocAsync(&vstore, vb, s), "cudaMallocAsync(volume)");
+    cudaError_t e = cudaMallocAsync(&dout, npix * 20, s);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(vstore, s);
+        return cuda_fail(e, "cudaMallocAsync(outputs)");
+    }
+    float* d_rgbt = static_cast<float*>(dout);
+    float* d_depth = d_rgbt + npix * 4;
+    nsl_volume* vol = nullptr;
+    std::vector<int32_t> fv((size_t)F, 0);
+    nsl_status st = nsl_volume_upload(g, host_density, 0, layout, vstore, vb, stream, &vol);
+    if (st == NSL_OK) {
+        const nsl_volume* vp = vol;
+        st = nsl_guiding_map_batch(&vp, 1, fv.data(), cams, lights, n_lights, light_mode, med, m, frame_ids, F, d_rgbt,
+                                   d_depth, nullptr, stream);
+    }
+    if (st == NSL_OK) {
+        e = cudaMemcpyAsync(host_rgbt, d_rgbt, npix * 16, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(host_depth, d_depth, npix * 4, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) st = cuda_fail(e, "result download");
+    }
+    cudaFreeAsync(dout, s);
+    cudaFreeAsync(vstore, s);
+    nsl_volume_release(vol);
+    if (st != NSL_OK) return st;
+    NSL_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return NSL_OK;
+}
+
+nsl_status nsl_debug_frame_constants(const nsl_grid_desc* g, const nsl_camera* cam, const nsl_light* lights,
+                                     int32_t n_lights, int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                                     nsl_frame_constants* out, nsl_stream stream) {
+    g_err.clear();
+    if (nsl_status st = check_grid(g)) return st;
+    if (!cam || !out) return fail(NSL_ERR_INVALID_ARG, "NULL camera/out");
+    if (nsl_status st = check_camera(cam, 0)) return st;
+    if (nsl_status st = check_common(lights, n_lights, light_mode, med, m)) return st;
+    if (nsl_status st = check_lights(lights, n_lights, light_mode, 0)) return st;
+    std::vector<FrameIn> frames(1);
+    memset(frames.data(), 0, sizeof(FrameIn));
+    frames[0].cam = *cam;
+    frames[0].vol.nx = g->nx;
+    frames[0].vol.ny = g->ny;
+    frames[0].vol.nz = g->nz;
+    frames[0].vol.layout = kQuadF32;
+    for (int a = 0; a < 3; ++a) frames[0].vol.origin[a] = g->origin[a];
+    frames[0].vol.dx = g->voxel_width;
+    const MarchConst mc = make_const(n_lights, light_mode, med, m);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Workspace ws;
+    if (nsl_status st = build_frames(frames, lights, n_lights, mc, s, ws)) return st;
+    FrameParams p;
+    cudaError_t e = cudaMemcpyAsync(&p, ws.params, sizeof p, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(ws.base, s);
+    if (e != cudaSuccess) return cuda_fail(e, "frame constants download");
+    NSL_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    out->inv_dx = p.inv_dx;
+    memcpy(out->B, p.B, sizeof p.B);
+    memcpy(out->Ex, p.Ex, sizeof p.Ex);
+    memcpy(out->Ey, p.Ey, sizeof p.Ey);
+    memcpy(out->Dg, p.Dg, sizeof p.Dg);
+    memcpy(out->Oe, p.Oe, sizeof p.Oe);
+    memcpy(out->F0, p.F0, sizeof p.F0);
+    memcpy(out->fwd, p.fwd, sizeof p.fwd);
+    memcpy(out->Ln, p.Ln, sizeof p.Ln);
+    memcpy(out->Lg, p.Lg, sizeof p.Lg);
+    memcpy(out->P, p.P, sizeof p.P);
+    out->front_identity_ok = p.front_ok;
+    return NSL_OK;
+}
+
+nsl_status nsl_debug_jitter(const nsl_march* m, uint32_t frame_id, int32_t n, uint32_t* out_hash, float* out_delta,
+                            nsl_stream stream) {
+    g_err.clear();
+    if (!m || !out_hash || !out_delta || n < 0) return fail(NSL_ERR_INVALID_ARG, "bad arguments");
+    if (n == 0) return NSL_OK;
+    nsl_medium med{0.0f, 1.0f, 0.0f};
+    const MarchConst mc = make_const(1, 0, &med, m);
+    NSL_CUDA(launch_jitter_debug(mc, frame_id, n, out_hash, out_delta, reinterpret_cast<cudaStream_t>(stream)),
+             "jitter kernel launch");
+    return NSL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// nsl_internal.cuh — device-side types of libnsl (B200 guiding-map ray march).
+// Not part of the ABI.  See include/nsl.h for the boundary and DESIGN.md §2
+// for the canonical definition every kernel follows.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/nsl.h"
+
+namespace nsl {
+
+// Per-volume description handed to the frame-setup kernel.
+struct VolDesc {
+    const void* data;
+    int32_t nx, ny, nz, layout;
+    float origin[3];
+    float dx;
+};
+
+// Raw per-frame input (host -> device, one memcpy per call).
+struct FrameIn {
+    nsl_camera cam;
+    VolDesc vol;
+    uint32_t frame_id;
+    int32_t pad;
+};
+
+// Per-frame constants produced by frame_setup_kernel (C3/C3b/C10),
+// consumed by march_kernel.  Plain words: copied to shared memory per CTA.
+struct FrameParams {
+    const void* data;          // volume layout base
+    int32_t layout, nx, ny, nz;
+    int32_t sy, sz;            // strides in layout elements (y, z)
+    float supp[3];             // n_a + 1 (support upper bound in padded index space)
+    int32_t projection, W, H;
+    float inv_dx;
+    float B[3], Ex[3], Ey[3], Dg[3];
+    float Oe[3], F0[3], fwd[3];
+    float Ln[4][3], Lg[4][3], P[4], rgb[4][3];
+    uint32_t frame_id;
+    int32_t front_ok;          // C9 preconditions hold for this frame
+    int32_t pad[2];
+};
+static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
+
+// Parameters common to every frame of a call (kernel argument).
+struct MarchConst {
+    float h, hl, tau_d, t_min;
+    float kappa, alpha, g;
+    int32_t Ncap;              // N or 2^24 (unbounded)
+    int32_t form, jitter, n_lights, light_mode;
+    uint32_t seed_lo, seed_hi;
+    int32_t front_identity;
+    float axis[3];
+};
+
+// layouts
+constexpr int kLinearF32 = NSL_LAYOUT_LINEAR_F32;
+constexpr int kQuadF32 = NSL_LAYOUT_QUAD_F32;
+constexpr int kCornerF16 = NSL_LAYOUT_CORNER_F16;
+
+// Launch helpers implemented in the .cu files.
+cudaError_t launch_layout(const float* raw, const VolDesc& v, void* storage, unsigned long long* invalid,
+                          cudaStream_t s);
+cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
+                               FrameParams* out, cudaStream_t s);
+cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection,
+                         int layout, float4* rgbt, float* depth, uint32_t* debug, cudaStream_t s);
+cudaError_t launch_jitter_debug(const MarchConst& mc, uint32_t frame_id, int n, uint32_t* hash, float* delta,
+                                cudaStream_t s);
+
+size_t layout_elems(int layout, int nx, int ny, int nz);
+size_t layout_elem_bytes(int layout);
+
+}  // namespace nsl

@@ -1,0 +1,161 @@
+// setup.cu — rows a2/a3 per frame: camera frame constants, guide-light frame
+// and phase (C3, C3b, C10), one thread per frame.
+//
+// Evaluated in fp64 with explicitly rounded operations (__dmul_rn, __dadd_rn,
+// __dsub_rn, __ddiv_rn, __dsqrt_rn: no FMA contraction) in exactly the
+// operation order DESIGN.md C3 prescribes, then rounded once to fp32, so that
+// the per-pixel ray positions downstream are reproducible bit for bit.
+#include "nsl_internal.cuh"
+
+namespace nsl {
+namespace {
+
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dd(double a, double b) { return __ddiv_rn(a, b); }
+
+// |a| = sqrt((ax ax + ay ay) + az az)
+__device__ __forceinline__ double norm3(const double a[3]) {
+    return __dsqrt_rn(da(da(dm(a[0], a[0]), dm(a[1], a[1])), dm(a[2], a[2])));
+}
+// (a x b)_x = ay bz - az by (cyclic)
+__device__ __forceinline__ void cross3(const double a[3], const double b[3], double o[3]) {
+    o[0] = ds(dm(a[1], b[2]), dm(a[2], b[1]));
+    o[1] = ds(dm(a[2], b[0]), dm(a[0], b[2]));
+    o[2] = ds(dm(a[0], b[1]), dm(a[1], b[0]));
+}
+__device__ __forceinline__ double dot3(const double a[3], const double b[3]) {
+    return da(da(dm(a[0], b[0]), dm(a[1], b[1])), dm(a[2], b[2]));
+}
+
+// Henyey-Greenstein (C10): (1-g^2) / (4 pi d sqrt d),
+// d = (1 + g^2) - 2 g c
+__device__ __forceinline__ double hg64(double g, double c) {
+    double d = ds(da(1.0, dm(g, g)), dm(dm(2.0, g), c));
+    return dd(ds(1.0, dm(g, g)), dm(dm(4.0, 3.141592653589793), dm(d, __dsqrt_rn(d))));
+}
+
+__global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_light* __restrict__ lights, int F,
+                                   MarchConst mc, FrameParams* __restrict__ out) {
+    int fi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fi >= F) return;
+    const FrameIn& fr = in[fi];
+    const nsl_camera& cam = fr.cam;
+    FrameParams p;
+    // ---- volume
+    p.data = fr.vol.data;
+    p.layout = fr.vol.layout;
+    p.nx = fr.vol.nx;
+    p.ny = fr.vol.ny;
+    p.nz = fr.vol.nz;
+    if (p.layout == kLinearF32) {
+        p.sy = p.nx + 2;
+        p.sz = (p.nx + 2) * (p.ny + 2);
+    } else {
+        p.sy = p.nx + 1;
+        p.sz = (p.nx + 1) * (p.ny + 1);
+    }
+    p.supp[0] = (float)(p.nx + 1);
+    p.supp[1] = (float)(p.ny + 1);
+    p.supp[2] = (float)(p.nz + 1);
+    p.projection = cam.projection;
+    p.W = cam.width;
+    p.H = cam.height;
+    p.frame_id = fr.frame_id;
+    p.pad[0] = p.pad[1] = 0;
+
+    // ---- camera basis (C3)
+    const double dx = (double)fr.vol.dx;
+    double Fw[3] = {cam.forward[0], cam.forward[1], cam.forward[2]};
+    double Up[3] = {cam.up[0], cam.up[1], cam.up[2]};
+    double nf = norm3(Fw);
+    double f[3] = {dd(Fw[0], nf), dd(Fw[1], nf), dd(Fw[2], nf)};
+    double c[3];
+    cross3(f, Up, c);
+    double nc = norm3(c);
+    double r[3] = {dd(c[0], nc), dd(c[1], nc), dd(c[2], nc)};
+    double u[3];
+    cross3(r, f, u);
+    const double W = (double)cam.width, H = (double)cam.height;
+    const double ay = dm((double)cam.extent, 0.5);
+    const double ax = dd(dm(ay, W), H);
+    const double cx = ds(dd(1.0, W), 1.0), cy = ds(1.0, dd(1.0, H));
+    const double ex = dd(2.0, W), ey = dd(-2.0, H);
+    p.inv_dx = (float)dd(1.0, dx);
+    for (int a = 0; a < 3; ++a) {
+        const double P = (double)cam.position[a], o = (double)fr.vol.origin[a];
+        double w = da(P, dm(dm(cx, ax), r[a]));
+        w = da(w, dm(dm(cy, ay), u[a]));
+        p.B[a] = (float)da(dd(ds(w, o), dx), 0.5);
+        p.Dg[a] = (float)dd(f[a], dx);
+        p.Oe[a] = (float)da(dd(ds(P, o), dx), 0.5);
+        p.F0[a] = (float)da(da(f[a], dm(dm(cx, ax), r[a])), dm(dm(cy, ay), u[a]));
+        p.fwd[a] = (float)f[a];
+        if (cam.projection == 0) {
+            p.Ex[a] = (float)dd(dm(dm(ex, ax), r[a]), dx);
+            p.Ey[a] = (float)dd(dm(dm(ey, ay), u[a]), dx);
+        } else {
+            p.Ex[a] = (float)dm(dm(ex, ax), r[a]);
+            p.Ey[a] = (float)dm(dm(ey, ay), u[a]);
+        }
+    }
+
+    // ---- lights (C3b): explicit, or the surrogate set of eq:approx
+    double Ln[4][3] = {};
+    const nsl_light* L = lights + (size_t)fi * mc.n_lights;
+    if (mc.light_mode == NSL_LIGHTS_GUIDE) {
+        double om[3] = {-f[0], -f[1], -f[2]};
+        double A[3] = {mc.axis[0], mc.axis[1], mc.axis[2]};
+        if (A[0] == 0.0 && A[1] == 0.0 && A[2] == 0.0) A[2] = 1.0;
+        double nA = norm3(A);
+        double an[3] = {dd(A[0], nA), dd(A[1], nA), dd(A[2], nA)};
+        double s[3];
+        cross3(om, an, s);
+        double ns = norm3(s);
+        if (ns < 1e-6) {
+            const double xh[3] = {1.0, 0.0, 0.0};
+            cross3(om, xh, s);
+            ns = norm3(s);
+        }
+        double t[3] = {dd(s[0], ns), dd(s[1], ns), dd(s[2], ns)};
+        for (int q = 0; q < 3; ++q) {
+            Ln[0][q] = om[q];
+            Ln[1][q] = t[q];
+            Ln[2][q] = -t[q];
+        }
+    } else {
+        for (int l = 0; l < mc.n_lights; ++l) {
+            double v[3] = {L[l].to_light[0], L[l].to_light[1], L[l].to_light[2]};
+            double nl = norm3(v);
+            for (int q = 0; q < 3; ++q) Ln[l][q] = dd(v[q], nl);
+        }
+    }
+    for (int l = 0; l < 4; ++l) {
+        const bool on = l < mc.n_lights;
+        for (int q = 0; q < 3; ++q) {
+            p.Ln[l][q] = on ? (float)Ln[l][q] : 0.0f;
+            p.Lg[l][q] = on ? (float)dd(Ln[l][q], dx) : 0.0f;
+            p.rgb[l][q] = on ? L[l].rgb[q] : 0.0f;
+        }
+        // cos theta = to_light . dir (C10); per frame for ortho (dir = f)
+        p.P[l] = on ? (float)hg64((double)mc.g, dot3(Ln[l], f)) : 0.0f;
+    }
+    // ---- C9 preconditions: front light is exactly -D_g, orthographic, h_l == h
+    bool ok = mc.front_identity && mc.light_mode == NSL_LIGHTS_GUIDE && cam.projection == 0 && mc.hl == mc.h;
+    for (int q = 0; q < 3; ++q) ok = ok && (p.Lg[0][q] == -p.Dg[q]);
+    p.front_ok = ok ? 1 : 0;
+    out[fi] = p;
+}
+
+}  // namespace
+
+cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
+                               FrameParams* out, cudaStream_t s) {
+    int threads = 64;
+    int blocks = (F + threads - 1) / threads;
+    frame_setup_kernel<<<blocks, threads, 0, s>>>(in, lights, F, mc, out);
+    return cudaGetLastError();
+}
+
+}  // namespace nsl

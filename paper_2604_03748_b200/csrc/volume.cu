@@ -1,0 +1,125 @@
+// volume.cu — row a1: density grid -> device sampler layout.
+//
+// Every layout carries the 1-voxel zero apron of the canonical sampler
+// (C1: padded index 0 and n+1 are vacuum), so the march kernel
+// never bounds-checks a corner.  One thread per output element: the writes
+// are fully coalesced, the gathers from the x-fastest raw grid are
+// sector-coalesced along x.  HBM-bound: bytes = raw read + layout write.
+#include <cuda_fp16.h>
+
+#include "nsl_internal.cuh"
+
+namespace nsl {
+
+size_t layout_elems(int layout, int nx, int ny, int nz) {
+    switch (layout) {
+        case kLinearF32: return (size_t)(nx + 2) * (ny + 2) * (nz + 2);
+        case kQuadF32: return (size_t)(nx + 1) * (ny + 1) * (nz + 2);
+        case kCornerF16: return (size_t)(nx + 1) * (ny + 1) * (nz + 1);
+    }
+    return 0;
+}
+
+size_t layout_elem_bytes(int layout) {
+    switch (layout) {
+        case kLinearF32: return 4;
+        case kQuadF32: return 16;
+        case kCornerF16: return 16;
+    }
+    return 0;
+}
+
+namespace {
+
+struct Raw {
+    const float* __restrict__ v;
+    int nx, ny, nz;
+    // padded-index read: 0 outside [1, n]
+    __device__ __forceinline__ float at(int i, int j, int k) const {
+        if (i < 1 || j < 1 || k < 1 || i > nx || j > ny || k > nz) return 0.0f;
+        return __ldg(v + ((size_t)(k - 1) * ny + (j - 1)) * nx + (i - 1));
+    }
+};
+
+__device__ __forceinline__ void check(float x, unsigned long long* invalid) {
+    if (!(x >= 0.0f) || isinf(x)) atomicAdd(invalid, 1ull);
+}
+
+__global__ void layout_linear_kernel(Raw r, float* __restrict__ out, unsigned long long* invalid, size_t total) {
+    const int px = r.nx + 2, py = r.ny + 2;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        int i = (int)(e % px);
+        size_t rest = e / px;
+        int j = (int)(rest % py), k = (int)(rest / py);
+        float x = r.at(i, j, k);
+        if (i >= 1 && j >= 1 && k >= 1 && i <= r.nx && j <= r.ny && k <= r.nz) check(x, invalid);
+        out[e] = x;
+    }
+}
+
+__global__ void layout_quad_kernel(Raw r, float4* __restrict__ out, unsigned long long* invalid, size_t total) {
+    const int qx = r.nx + 1, qy = r.ny + 1;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        int i = (int)(e % qx);
+        size_t rest = e / qx;
+        int j = (int)(rest % qy), k = (int)(rest / qy);
+        float4 q;
+        q.x = r.at(i, j, k);
+        q.y = r.at(i + 1, j, k);
+        q.z = r.at(i, j + 1, k);
+        q.w = r.at(i + 1, j + 1, k);
+        if (i >= 1 && j >= 1 && k >= 1 && k <= r.nz) check(q.x, invalid);
+        out[e] = q;
+    }
+}
+
+__global__ void layout_corner_f16_kernel(Raw r, uint4* __restrict__ out, unsigned long long* invalid, size_t total) {
+    const int qx = r.nx + 1, qy = r.ny + 1;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        int i = (int)(e % qx);
+        size_t rest = e / qx;
+        int j = (int)(rest % qy), k = (int)(rest / qy);
+        float c[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) c[b] = r.at(i + (b & 1), j + ((b >> 1) & 1), k + (b >> 2));
+        if (i >= 1 && j >= 1 && k >= 1) check(c[0], invalid);
+        __half2 h0 = __floats2half2_rn(c[0], c[1]), h1 = __floats2half2_rn(c[2], c[3]);
+        __half2 h2 = __floats2half2_rn(c[4], c[5]), h3 = __floats2half2_rn(c[6], c[7]);
+        uint4 u;
+        u.x = *reinterpret_cast<unsigned*>(&h0);
+        u.y = *reinterpret_cast<unsigned*>(&h1);
+        u.z = *reinterpret_cast<unsigned*>(&h2);
+        u.w = *reinterpret_cast<unsigned*>(&h3);
+        out[e] = u;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_layout(const float* raw, const VolDesc& v, void* storage, unsigned long long* invalid,
+                          cudaStream_t s) {
+    Raw r{raw, v.nx, v.ny, v.nz};
+    size_t total = layout_elems(v.layout, v.nx, v.ny, v.nz);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    size_t want = (total + 255) / 256;
+    unsigned blocks = (unsigned)(want < (size_t)sms * 16 ? want : (size_t)sms * 16);
+    if (blocks == 0) blocks = 1;
+    switch (v.layout) {
+        case kLinearF32:
+            layout_linear_kernel<<<blocks, 256, 0, s>>>(r, static_cast<float*>(storage), invalid, total);
+            break;
+        case kQuadF32:
+            layout_quad_kernel<<<blocks, 256, 0, s>>>(r, static_cast<float4*>(storage), invalid, total);
+            break;
+        case kCornerF16:
+            layout_corner_f16_kernel<<<blocks, 256, 0, s>>>(r, static_cast<uint4*>(storage), invalid, total);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace nsl

@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path, called through the C ABI, against the CPU oracle
+(DESIGN.md §3), on the BASELINE.json configs and on edge and random cases."""
+import math
+import os
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import nsl_inputs as I
+import oracle
+from parity import compare_frame, value_ok
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def nsl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    import paper_2604_03748_b200 as nsl
+    nsl.lib()
+    return nsl
+
+
+def run(nsl, w, layout=1, debug=True, march=None):
+    import torch
+    rgbt, depth, dbg = nsl.run_workload(w, layout=layout, debug=debug, march=march)
+    torch.cuda.synchronize()
+    return (rgbt.cpu().numpy(), depth.cpu().numpy(), None if dbg is None else dbg.cpu().numpy())
+
+
+def bits(a):
+    return np.ascontiguousarray(np.asarray(a, np.float32)).view(np.uint32)
+
+
+# ------------------------------------------------------------------ P15 frame constants, P14 jitter
+@pytest.mark.parametrize("cfg,kw", [("C1", {}), ("C1", {"perspective": True}), ("C1", {"single_light": True}),
+                                    ("C2", {}), ("C3", {})])
+def test_frame_constants_bitwise(nsl, cfg, kw):
+    w = I.make_workload(cfg, frames=None if cfg == "C1" else [0, 7, 29, 59], **kw)
+    for f in range(w.n_frames):
+        a = nsl.debug_frame_constants(w.grid, w.cameras[f], w.lights[f], w.light_mode, w.medium, w.march)
+        b = oracle.frame_constants(w.grid, w.cameras[f], w.lights[f], w.light_mode, w.medium, w.march)
+        for k in ("inv_dx", "B", "Ex", "Ey", "Dg", "Oe", "F0", "fwd", "Ln", "Lg", "P"):
+            assert np.array_equal(bits(a[k]), bits(b[k])), (cfg, f, k, a[k], b[k])
+        if w.light_mode == I.LIGHTS_GUIDE and w.cameras[f].projection == I.ORTHO:
+            assert a["front_identity_ok"] == 1
+
+
+def test_frame_constants_random_cameras(nsl):
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        n = int(rng.integers(4, 40))
+        grid = I.Grid(n, int(rng.integers(3, 40)), int(rng.integers(3, 40)),
+                      tuple(float(np.float32(x)) for x in rng.normal(size=3)), float(np.float32(rng.uniform(0.01, 0.5))))
+        f = I._f32t(I._unit(tuple(rng.normal(size=3))))
+        cam = I.Camera(int(rng.integers(0, 2)), I._f32t(rng.normal(size=3) * 3), f, I._f32t(rng.normal(size=3)),
+                       float(np.float32(rng.uniform(0.2, 3.0))), int(rng.integers(1, 300)), int(rng.integers(1, 300)))
+        mode = int(rng.integers(0, 2))
+        nl = int(rng.integers(1, 4 if mode else 5))
+        lights = [I.Light(I._f32t(I._unit(tuple(rng.normal(size=3)))), I._f32t(rng.uniform(0, 2, 3))) for _ in range(nl)]
+        med = I.Medium(float(np.float32(rng.uniform(0, 50))), float(np.float32(rng.uniform(0, 1))),
+                       float(np.float32(rng.uniform(-0.9, 0.9))))
+        m = I.March(step=float(np.float32(0.1)), guide_axis=I._f32t(rng.normal(size=3)))
+        a = nsl.debug_frame_constants(grid, cam, lights, mode, med, m)
+        b = oracle.frame_constants(grid, cam, lights, mode, med, m)
+        for k in ("inv_dx", "B", "Ex", "Ey", "Dg", "Oe", "F0", "fwd", "Ln", "Lg", "P"):
+            assert np.array_equal(bits(a[k]), bits(b[k])), (trial, k, a[k], b[k])
+
+
+def test_jitter_matches_golden_and_oracle(nsl):
+    import torch
+    rows = [l.split() for l in open(os.path.join(HERE, "golden", "jitter_hash.txt")) if not l.startswith("#")]
+    m = I.March(step=0.078125, seed=0x26040374, jitter=1)
+    h = torch.empty(4096, dtype=torch.int32, device="cuda")
+    d = torch.empty(4096, dtype=torch.float32, device="cuda")
+    nsl.debug_jitter(m, 7, h, d)
+    hh = h.cpu().numpy().view(np.uint32)
+    dd = d.cpu().numpy()
+    for p, hx in rows:
+        assert hh[int(p)] == int(hx, 16)
+    for p in range(0, 4096, 37):
+        assert hh[p] == oracle.jitter_hash(m.seed, 7, p)
+        assert dd[p] == np.float32(oracle.jitter_delta(m, 7, p))
+
+
+# ------------------------------------------------------------------ C1 full frames
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("kw", [{}, {"single_light": True}, {"perspective": True},
+                                {"perspective": True, "single_light": True}])
+def test_parity_C1(nsl, layout, kw):
+    w = I.make_workload("C1", **kw)
+    g, gd, gdbg = run(nsl, w, layout=layout, debug=True)
+    rep = compare_frame(w, 0, g[0], gd[0], gdbg[0])
+    assert rep["samples"] > 50000
+
+
+def test_parity_C1_nondebug_front_identity(nsl):
+    """The timed path (no debug counters, C9 front-light shortcut) meets the value bar too."""
+    w = I.make_workload("C1")
+    g, gd, _ = run(nsl, w, debug=False)
+    compare_frame(w, 0, g[0], gd[0], None)
+
+
+def test_parity_C1_corner_f16(nsl):
+    """fp16 layout vs the oracle fed the RNE-fp16-rounded grid."""
+    w = I.make_workload("C1")
+    g, gd, gdbg = run(nsl, w, layout=2, debug=True)
+    v16 = w.volume(0).astype(np.float16).astype(np.float32)
+    compare_frame(w, 0, g[0], gd[0], gdbg[0], vals=v16)
+
+
+def test_layouts_agree_bitwise(nsl):
+    w = I.make_workload("C2", frames=[3])
+    a = run(nsl, w, layout=0)
+    b = run(nsl, w, layout=1)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+# ------------------------------------------------------------------ C2/C3 (frames 0 and 30), C4, C5 (subsampled)
+@pytest.mark.parametrize("debug", [True, False])
+def test_parity_C2(nsl, debug):
+    w = I.make_workload("C2", frames=[0, 30])
+    g, gd, gdbg = run(nsl, w, debug=debug)
+    for f in range(2):
+        compare_frame(w, f, g[f], gd[f], None if gdbg is None else gdbg[f])
+
+
+def test_parity_C2_density_sweep(nsl):
+    for kappa in (16.0, 64.0):
+        w = I.make_workload("C2", frames=[12], kappa=kappa)
+        g, gd, gdbg = run(nsl, w)
+        compare_frame(w, 0, g[0], gd[0], gdbg[0])
+
+
+def test_parity_C3(nsl):
+    w = I.make_workload("C3", frames=[0, 30])
+    g, gd, gdbg = run(nsl, w)
+    for f in range(2):
+        compare_frame(w, f, g[f], gd[f], gdbg[f])
+
+
+def _subsample(H, W, step):
+    ys, xs = np.meshgrid(np.arange(0, H, step), np.arange(0, W, step), indexing="ij")
+    return (ys * W + xs).reshape(-1)
+
+
+def test_parity_C4_subsampled(nsl):
+    w = I.make_workload("C4", frames=[0, 120, 239])
+    g, gd, gdbg = run(nsl, w, debug=True)
+    pix = _subsample(w.height, w.width, 4)
+    for f in range(3):
+        compare_frame(w, f, g[f], gd[f], gdbg[f], pixels=pix)
+
+
+def test_parity_C5_subsampled_full_size(nsl):
+    """512^3, 2048^2 in the bench launch configuration (no debug), sampled 1/64."""
+    w = I.make_workload("C5", frames=[0, 512])
+    g, gd, _ = run(nsl, w, debug=False)
+    pix = _subsample(w.height, w.width, 8)
+    for f in range(2):
+        compare_frame(w, f, g[f], gd[f], None, pixels=pix)
+
+
+# ------------------------------------------------------------------ batch / determinism / sharding / host API
+def test_batch_equals_single_frames_and_is_deterministic(nsl):
+    import torch
+    w = I.make_workload("C2", frames=[0, 1, 2, 3])
+    a = run(nsl, w, debug=False)
+    b = run(nsl, w, debug=False)
+    for x, y in zip(a[:2], b[:2]):
+        assert np.array_equal(x, y)
+    vols = nsl.upload_workload_volumes(w)
+    for f in range(4):
+        rgbt = torch.empty((w.height, w.width, 4), device="cuda")
+        depth = torch.empty((w.height, w.width), device="cuda")
+        nsl.guiding_map(vols[0], w.cameras[f], w.lights[f], w.light_mode, w.medium, w.march, w.frame_ids[f],
+                        rgbt, depth)
+        torch.cuda.synchronize()
+        assert np.array_equal(rgbt.cpu().numpy(), a[0][f])
+        assert np.array_equal(depth.cpu().numpy(), a[1][f])
+
+
+def test_frame_sharding_is_bitwise_invariant(nsl):
+    """Cyclic shards (rank::P) of a batch equal the unsharded batch: jitter is keyed by global frame id."""
+    w = I.make_workload("C2", frames=list(range(8)))
+    full = run(nsl, w, debug=False)
+    for P in (2, 4):
+        for r in range(P):
+            frames = list(range(r, 8, P))
+            part = run(nsl, w.subset(frames), debug=False)
+            assert np.array_equal(part[0], full[0][frames])
+            assert np.array_equal(part[1], full[1][frames])
+
+
+def test_host_api_equals_device_api(nsl):
+    import torch
+    w = I.make_workload("C2", frames=[5, 6])
+    dev = run(nsl, w, debug=False)
+    dens = torch.from_numpy(w.volume(0)).pin_memory()
+    hr = torch.empty((2, w.height, w.width, 4)).pin_memory()
+    hd = torch.empty((2, w.height, w.width)).pin_memory()
+    nsl.guiding_map_host(w.grid, dens, 1, w.cameras, w.lights, w.light_mode, w.medium, w.march, w.frame_ids, hr, hd)
+    assert np.array_equal(hr.numpy(), dev[0])
+    assert np.array_equal(hd.numpy(), dev[1])
+
+
+def test_device_upload_reports_invalid_values(nsl):
+    import torch
+    g = I.Grid(8, 8, 8, (0, 0, 0), 0.125)
+    d = torch.ones((8, 8, 8), device="cuda")
+    d[1, 2, 3] = float("nan")
+    d[4, 4, 4] = -2.0
+    for layout in (0, 1, 2):
+        v = nsl.Volume(g, d, layout)
+        assert v.check() == 2
+    v = nsl.Volume(g, torch.ones((8, 8, 8), device="cuda"), 1)
+    assert v.check() == 0
+
+
+# ------------------------------------------------------------------ edge cases
+def _case(grid, vals, cam, lights, mode, med, march, frame_id=0):
+    return I.Workload(name="edge", grid=grid, volume_specs=[("given", 0)], frame_vol=[0], cameras=[cam],
+                      light_mode=mode, lights=[lights], medium=med, march=march, frame_ids=[frame_id],
+                      _cache={0: np.ascontiguousarray(vals, np.float32)})
+
+
+def test_edge_cases(nsl):
+    base = I.make_workload("C1")
+    v = base.volume(0)
+    cam = base.cameras[0]
+    L = base.lights[0]
+    cases = {
+        "zero_grid": _case(base.grid, np.zeros_like(v), cam, L, 1, base.medium, base.march),
+        "one_pixel": _case(base.grid, v, replace(cam, width=1, height=1, extent=0.05), L, 1, base.medium, base.march),
+        "ragged_13x7": _case(base.grid, v, replace(cam, width=13, height=7), L, 1, base.medium, base.march),
+        "miss": _case(base.grid, v, replace(cam, forward=tuple(-c for c in cam.forward)), L, 1, base.medium, base.march),
+        "opaque": _case(base.grid, v, cam, L, 1, I.Medium(5000.0, 1.0, 0.0), replace(base.march, depth_tau=0.0)),
+        "cap_N3": _case(base.grid, v, cam, L, 1, base.medium, replace(base.march, max_steps=3)),
+        "light_step": _case(base.grid, v, cam, L, 1, base.medium, replace(base.march, light_step=0.05)),
+        "no_jitter_riemann": _case(base.grid, v, cam, L, 1, base.medium, replace(base.march, jitter=0, opacity_form=1)),
+        "literal_g": _case(base.grid, v, cam, L, 1, I.Medium(32.0, 0.7, 0.6), replace(base.march, opacity_form=2)),
+        "no_term": _case(base.grid, v, cam, L, 1, I.Medium(200.0, 1.0, 0.0), replace(base.march, t_min=0.0)),
+        "eye_inside": _case(base.grid, v, I.Camera(1, (0.5, 0.45, 0.5), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0),
+                                                   1.2, 40, 30), L, 1, base.medium, base.march),
+        "axis_degenerate": _case(base.grid, v, replace(cam, forward=(0.0, 0.0, -1.0), up=(0.0, 1.0, 0.0)), L, 1,
+                                 base.medium, base.march),
+        "four_lights": _case(base.grid, v, cam, [I.Light(I._f32t(I._unit(d)), (0.5, 1.0, 0.2)) for d in
+                                                 [(1, 0, 0), (0, 1, 0), (0, 0, 1), (-1, -1, 1)]], 0,
+                             base.medium, base.march),
+        "single_voxel_grid": _case(I.Grid(1, 1, 1, (0.4, 0.4, 0.4), 0.2), np.ones((1, 1, 1), np.float32), cam, L,
+                                   1, base.medium, base.march),
+    }
+    for name, w in cases.items():
+        g, gd, gdbg = run(nsl, w)
+        compare_frame(w, 0, g[0], gd[0], gdbg[0])
+        g2, gd2, _ = run(nsl, w, debug=False)
+        compare_frame(w, 0, g2[0], gd2[0], None)
+    # the miss case touches nothing; the zero grid is transparent
+    g, _, gdbg = run(nsl, cases["miss"])
+    assert np.all(g[0][..., 3] == 1.0) and not gdbg.any()
+
+
+def test_random_tiny_cases(nsl):
+    rng = np.random.default_rng(2604)
+    for trial in range(50):
+        nx, ny, nz = (int(x) for x in rng.integers(4, 17, 3))
+        dxw = float(np.float32(1.0 / max(nx, ny, nz)))
+        grid = I.Grid(nx, ny, nz, (0.0, 0.0, 0.0), dxw)
+        vals = (rng.random((nz, ny, nx)) * (rng.random((nz, ny, nx)) < 0.6)).astype(np.float32)
+        proj = int(rng.integers(0, 2))
+        yaw, el = rng.uniform(0, 360), rng.uniform(-60, 60)
+        cam = I.orbit_camera(yaw, int(rng.integers(3, 40)), int(rng.integers(3, 40)), elev_deg=el,
+                             distance=float(rng.uniform(1.2, 3.0)), projection=proj,
+                             fov_deg=float(rng.uniform(20, 70)), extent=float(rng.uniform(0.5, 2.0)))
+        mode = int(rng.integers(0, 2))
+        nl = int(rng.integers(1, 4 if mode else 5))
+        lights = [I.Light(I._f32t(I._unit(tuple(rng.normal(size=3)))), I._f32t(rng.uniform(0, 1.5, 3)))
+                  for _ in range(nl)]
+        med = I.Medium(float(np.float32(rng.uniform(1, 120))), float(np.float32(rng.uniform(0.2, 1))),
+                       float(np.float32(rng.uniform(-0.8, 0.8))))
+        m = I.March(step=float(np.float32(dxw * rng.choice([2.5, 5.0, 10.0, 17.3]))),
+                    light_step=float(np.float32(dxw * rng.choice([0.0, 3.0, 10.0]))),
+                    max_steps=int(rng.choice([0, 0, 0, 4])), depth_tau=float(np.float32(rng.uniform(0, 2))),
+                    t_min=float(np.float32(rng.choice([0.0, 1e-4, 1e-2]))), opacity_form=int(rng.integers(0, 3)),
+                    jitter=int(rng.integers(0, 2)), seed=int(rng.integers(0, 2 ** 63)),
+                    guide_axis=I._f32t(rng.normal(size=3)))
+        w = _case(grid, vals, cam, lights, mode, med, m, frame_id=int(rng.integers(0, 1000)))
+        g, gd, gdbg = run(nsl, w)
+        compare_frame(w, 0, g[0], gd[0], gdbg[0])
