@@ -40,7 +40,7 @@ CONFIG_TEXT = {
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="nsl", choices=["nsl", "reference"])
     p.add_argument("--config", default="C2")
@@ -83,7 +83,7 @@ class ClockSampler:
                             self.reasons.add(k)
                 except Exception:
                     pass
-                time.sleep(0.02)
+                time.sleep(0.005)
 
         self._t = threading.Thread(target=loop, daemon=True)
         self._t.start()

@@ -169,6 +169,21 @@ VolDesc desc_of(const nsl_volume* v) {
     return d;
 }
 
+// Keep the device's stream-ordered pool from returning freed blocks to the OS at
+// every synchronisation (default release threshold 0), so transient frame tables
+// and host-API staging buffers are recycled instead of re-mapped each call.
+void retain_pool_once() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 // Frame tables: FrameIn[F] | lights[F*nl] | FrameParams[F] in one stream-ordered allocation.
 struct Workspace {
     void* base = nullptr;
@@ -185,6 +200,7 @@ nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lig
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
     const size_t b_p = sizeof(FrameParams) * F;
+    retain_pool_once();
     NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_p, s), "cudaMallocAsync(frame tables)");
     ws.in = reinterpret_cast<FrameIn*>(ws.base);
     ws.lights = reinterpret_cast<nsl_light*>(static_cast<char*>(ws.base) + b_in);
@@ -236,6 +252,7 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     const float* raw = density;
     void* staging = nullptr;
     if (!density_on_device) {
+        retain_pool_once();
         e = cudaMallocAsync(&staging, n * sizeof(float), s);
         if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMallocAsync(staging)"));
         e = cudaMemcpyAsync(staging, density, n * sizeof(float), cudaMemcpyHostToDevice, s);
@@ -335,6 +352,7 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     const size_t vb = nsl_volume_bytes(g, layout);
     const size_t npix = (size_t)F * cams[0].width * cams[0].height;
     void *vstore = nullptr, *dout = nullptr;
+    retain_pool_once();
     NSL_CUDA(cudaMallocAsync(&vstore, vb, s), "cudaMallocAsync(volume)");
     cudaError_t e = cudaMallocAsync(&dout, npix * 20, s);
     if (e != cudaSuccess) {

@@ -65,7 +65,7 @@ def test_frame_constants_random_cameras(nsl):
         lights = [I.Light(I._f32t(I._unit(tuple(rng.normal(size=3)))), I._f32t(rng.uniform(0, 2, 3))) for _ in range(nl)]
         med = I.Medium(float(np.float32(rng.uniform(0, 50))), float(np.float32(rng.uniform(0, 1))),
                        float(np.float32(rng.uniform(-0.9, 0.9))))
-        m = I.March(step=float(np.float32(0.1)), guide_axis=I._f32t(rng.normal(size=3)))
+        m = I.March(step=float(np.float32(0.1)), depth_tau=0.0, guide_axis=I._f32t(rng.normal(size=3)))
         a = nsl.debug_frame_constants(grid, cam, lights, mode, med, m)
         b = oracle.frame_constants(grid, cam, lights, mode, med, m)
         for k in ("inv_dx", "B", "Ex", "Ey", "Dg", "Oe", "F0", "fwd", "Ln", "Lg", "P"):
