@@ -115,29 +115,16 @@ def rank_workload(cfg, rank, world, frames_per_rank):
     return I.make_workload(cfg, frames=[g % n_cfg for g in gids])
 
 
-def algorithmic_counts(nsl, w, vols, layout):
-    """Canonical march-sample counts from the debug counters (equal to the oracle's by parity),
-    plus the samples the kernel actually gathers (the C9 front-light shortcut skips the front march)."""
+def algorithmic_counts(nsl, w, vols, outputs):
+    """Work of one step from the instrumented launch of the same fast path
+    (nsl_guiding_map_batch_counted): canonical march samples (the metric's unit,
+    equal to the oracle's counters by parity) and trilinear gathers the kernel
+    actually executed (empty occupancy blocks and the C9 front march skip them)."""
     import torch
-    from dataclasses import replace
-    rgbt, depth, dbg = nsl.run_workload(w, layout=layout, debug=True, vols=vols)
+    c = nsl.guiding_map_batch_counted(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                                      w.frame_ids, outputs[0], outputs[1])
     torch.cuda.synchronize()
-    d = dbg.cpu().numpy().reshape(-1, 6).astype(np.int64)
-    prim = np.where(d[:, 0] > 0, d[:, 3] - d[:, 0] + 1, 0).sum()
-    light = d[:, 5].sum()
-    canonical = int(prim + light)
-    executed = canonical
-    if w.light_mode == 1 and w.cameras[0].projection == 0:
-        # front-light march lengths alone (n_lights = 1 guide = front only): skipped by C9 where n_lo >= 2
-        w1 = replace(w, lights=[row[:1] for row in w.lights], _cache=w._cache)
-        _, _, dbg1 = nsl.run_workload(w1, layout=layout, debug=True, vols=vols)
-        torch.cuda.synchronize()
-        d1 = dbg1.cpu().numpy().reshape(-1, 6).astype(np.int64)
-        executed = int(canonical - d1[d1[:, 0] >= 2, 5].sum())
-    occ = int(d[:, 4].sum())
-    return {"canonical_samples": canonical, "primary_samples": int(prim), "light_samples": int(light),
-            "executed_samples": executed, "occupied_samples": occ,
-            "pixels_in_support": int((d[:, 0] > 0).sum())}
+    return c
 
 
 def load_peaks():
@@ -249,7 +236,7 @@ def main():
 
     vols = step()
     torch.cuda.synchronize()
-    counts = algorithmic_counts(nsl, w, vols, layout)
+    counts = algorithmic_counts(nsl, w, vols, outputs)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -292,14 +279,14 @@ def main():
     peaks = load_peaks()
     bytes_per_sample = 16 if layout == 2 else 32
     march_s = statistics.mean(march_ms) / 1e3
-    achieved = counts["executed_samples"] * bytes_per_sample / march_s / 1e9
+    achieved = counts["gathers"] * bytes_per_sample / march_s / 1e9
     sm_mhz = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
     l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e9          # GB/s: 148 SMs x 128 B/clk L1 x max SM clock
     roof = {"bound": "l1tex", "achieved": achieved, "peak": l1_peak, "unit": "GB/s", "frac": achieved / l1_peak,
             "traffic": None,
             "peak_source": "derived: 148 SMs x 128 B/clk (B300_MICROARCH L1 line/cycle) x sm_max_mhz",
             "kernel": "march_kernel", "kernel_ms": march_s * 1e3,
-            "algorithmic_bytes_per_launch": counts["executed_samples"] * bytes_per_sample,
+            "algorithmic_bytes_per_launch": counts["gathers"] * bytes_per_sample,
             "hbm_peak_gbs": peaks.get("hbm_gbs")}
 
     line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": K, "warmup": args.warmup,

@@ -169,6 +169,22 @@ nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, 
                                  float* out_rgbt, float* out_depth, uint32_t* out_debug,
                                  nsl_stream stream);
 
+/* The same launch as nsl_guiding_map_batch (identical results, the timed
+ * fast path), instrumented: it also accumulates into `counters` (device,
+ * 4 x u64, zeroed by the call on `stream`):
+ *   [0] primary samples processed  = sum over pixels of (n_term - n_lo + 1)
+ *   [1] light samples (canonical)  = sum over pixels of light_samples (C12)
+ *   [2] trilinear gathers executed (samples in non-empty occupancy blocks that
+ *       the kernel actually loaded; the C9 front march is not executed)
+ *   [3] occupied primary samples   = sum of n_occ
+ * [0]+[1] is the canonical march-sample count of DESIGN.md §7. */
+nsl_status nsl_guiding_map_batch_counted(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                                         const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
+                                         int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                                         const uint32_t* frame_ids, int32_t F,
+                                         float* out_rgbt, float* out_depth, uint64_t* counters,
+                                         nsl_stream stream);
+
 /* End-to-end convenience call with HOST buffers: uploads the host density
  * grid, lays it out, marches the F frames and copies the results back into
  * host out_rgbt (F*H*W*4 floats) / out_depth (F*H*W floats); synchronises

@@ -78,8 +78,8 @@ class FrameConstantsS(ctypes.Structure):
 
 
 EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_upload", "nsl_volume_check",
-           "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_host",
-           "nsl_debug_frame_constants", "nsl_debug_jitter"]
+           "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_batch_counted",
+           "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter"]
 
 _lib = None
 
@@ -107,6 +107,8 @@ def lib():
                                   vp, vp, vp, vp]
     L.nsl_guiding_map_batch.argtypes = [P(vp), i32, P(i32), P(CameraS), P(LightS), i32, i32, P(MediumS),
                                         P(MarchS), P(u32), i32, vp, vp, vp, vp]
+    L.nsl_guiding_map_batch_counted.argtypes = [P(vp), i32, P(i32), P(CameraS), P(LightS), i32, i32, P(MediumS),
+                                                P(MarchS), P(u32), i32, vp, vp, vp, vp]
     L.nsl_guiding_map_host.argtypes = [P(GridDesc), vp, i32, P(CameraS), P(LightS), i32, i32, P(MediumS),
                                        P(MarchS), P(u32), i32, vp, vp, vp]
     L.nsl_debug_frame_constants.argtypes = [P(GridDesc), P(CameraS), P(LightS), i32, i32, P(MediumS),
@@ -245,6 +247,26 @@ def guiding_map_batch(vols: Sequence[Volume], frame_vol: Sequence[int], cams, li
                                        ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)), fid, F,
                                        _ptr(out_rgbt), _ptr(out_depth), _ptr(out_debug), _stream_handle(stream)),
            "nsl_guiding_map_batch")
+
+
+def guiding_map_batch_counted(vols, frame_vol, cams, lights, light_mode, medium, march, frame_ids, out_rgbt,
+                              out_depth, stream=None) -> dict:
+    """The timed fast path plus work counters: returns canonical primary/light
+    sample counts, trilinear gathers actually executed and occupied samples."""
+    import torch
+    F = len(cams)
+    counters = torch.zeros(4, dtype=torch.int64, device="cuda")
+    hv = (ctypes.c_void_p * len(vols))(*[v.handle.value for v in vols])
+    fv = (ctypes.c_int32 * F)(*frame_vol)
+    cs = (CameraS * F)(*[camera_s(c) for c in cams])
+    fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+    _check(lib().nsl_guiding_map_batch_counted(hv, len(vols), fv, cs, lights_s(lights), len(lights[0]), light_mode,
+                                               ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)), fid, F,
+                                               _ptr(out_rgbt), _ptr(out_depth), counters.data_ptr(),
+                                               _stream_handle(stream)), "nsl_guiding_map_batch_counted")
+    c = counters.cpu().tolist()
+    return {"primary_samples": c[0], "light_samples": c[1], "gathers": c[2], "occupied_samples": c[3],
+            "canonical_samples": c[0] + c[1]}
 
 
 def guiding_map_host(grid, host_density, layout, cams, lights, light_mode, medium, march, frame_ids,

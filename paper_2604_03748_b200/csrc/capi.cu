@@ -15,8 +15,10 @@ using namespace nsl;
 struct nsl_volume {
     nsl_grid_desc g;
     int32_t layout;
-    void* data;                       // caller-owned storage
+    void* data;                       // caller-owned storage: layout body | occupancy mask | tail
     unsigned long long* invalid;      // counter in the storage tail
+    uint32_t* occ;                    // occupancy bitmask inside the storage
+    nsl::OccGeom og;
 };
 
 namespace {
@@ -53,6 +55,14 @@ constexpr size_t kTail = 256;  // counter area after the layout (keeps 16-B alig
 
 size_t body_bytes(const nsl_grid_desc* g, int layout) {
     return layout_elems(layout, g->nx, g->ny, g->nz) * layout_elem_bytes(layout);
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// storage = [layout body | occupancy mask | tail counter], each 256-B aligned
+size_t mask_offset(const nsl_grid_desc* g, int layout) { return align_up(body_bytes(g, layout), 256); }
+size_t tail_offset(const nsl_grid_desc* g, int layout) {
+    return mask_offset(g, layout) + align_up((size_t)occ_geom(g->nx, g->ny, g->nz).words * 4, 256);
 }
 
 nsl_status check_grid(const nsl_grid_desc* g) {
@@ -166,6 +176,8 @@ VolDesc desc_of(const nsl_volume* v) {
     d.origin[1] = v->g.origin[1];
     d.origin[2] = v->g.origin[2];
     d.dx = v->g.voxel_width;
+    d.occ = v->occ;
+    d.og = v->og;
     return d;
 }
 
@@ -191,8 +203,6 @@ struct Workspace {
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
 };
-
-size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
                         const MarchConst& mc, cudaStream_t s, Workspace& ws) {
@@ -222,7 +232,7 @@ const char* nsl_version(void) { return "nsl-b200 0.1 (sm_100a)"; }
 
 size_t nsl_volume_bytes(const nsl_grid_desc* g, int32_t layout) {
     if (check_grid(g) != NSL_OK || check_layout(layout) != NSL_OK) return 0;
-    return align_up(body_bytes(g, layout), 256) + kTail;
+    return tail_offset(g, layout) + kTail;
 }
 
 nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32_t density_on_device, int32_t layout,
@@ -245,7 +255,9 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     v->g = *g;
     v->layout = layout;
     v->data = device_storage;
-    v->invalid = reinterpret_cast<unsigned long long*>(static_cast<char*>(device_storage) + align_up(body_bytes(g, layout), 256));
+    v->invalid = reinterpret_cast<unsigned long long*>(static_cast<char*>(device_storage) + tail_offset(g, layout));
+    v->occ = reinterpret_cast<uint32_t*>(static_cast<char*>(device_storage) + mask_offset(g, layout));
+    v->og = occ_geom(g->nx, g->ny, g->nz);
     auto bail = [&](nsl_status st) { delete v; return st; };
     cudaError_t e = cudaMemsetAsync(v->invalid, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemsetAsync"));
@@ -261,6 +273,8 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     }
     e = launch_layout(raw, desc_of(v), device_storage, v->invalid, s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "layout kernel launch"));
+    e = launch_occupancy(raw, desc_of(v), v->occ, s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "occupancy kernel launch"));
     if (staging) {
         e = cudaFreeAsync(staging, s);
         if (e != cudaSuccess) return bail(cuda_fail(e, "cudaFreeAsync(staging)"));
@@ -285,10 +299,11 @@ nsl_status nsl_volume_release(nsl_volume* v) {
     return NSL_OK;
 }
 
-nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
-                                 const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
-                                 const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
-                                 float* out_rgbt, float* out_depth, uint32_t* out_debug, nsl_stream stream) {
+static nsl_status batch_impl(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                             const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                             const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                             float* out_rgbt, float* out_depth, uint32_t* out_debug, unsigned long long* counters,
+                             nsl_stream stream) {
     g_err.clear();
     if (F < 1 || F > 65535) return fail(NSL_ERR_INVALID_ARG, "F must be in [1, 65535]");
     if (!vols || n_vols < 1 || !frame_vol || !cams || !frame_ids)
@@ -299,8 +314,11 @@ nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, 
     for (int i = 0; i < n_vols; ++i)
         if (!vols[i]) return fail(NSL_ERR_INVALID_ARG, "vols[%d] is NULL", i);
     const int layout = vols[0]->layout;
-    for (int i = 1; i < n_vols; ++i)
+    int max_words = 0;
+    for (int i = 0; i < n_vols; ++i) {
         if (vols[i]->layout != layout) return fail(NSL_ERR_UNSUPPORTED, "all volumes of a batch must share a layout");
+        max_words = vols[i]->og.words > max_words ? vols[i]->og.words : max_words;
+    }
     const int W = cams[0].width, H = cams[0].height, proj = cams[0].projection;
     std::vector<FrameIn> frames((size_t)F);
     for (int f = 0; f < F; ++f) {
@@ -319,12 +337,35 @@ nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, 
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
     if (nsl_status st = build_frames(frames, lights, n_lights, mc, s, ws)) return st;
-    cudaError_t e = launch_march(ws.params, mc, F, W, H, proj, layout, reinterpret_cast<float4*>(out_rgbt), out_depth,
-                                 out_debug, s);
+    cudaError_t e = launch_march(ws.params, mc, F, W, H, proj, layout, max_words, reinterpret_cast<float4*>(out_rgbt),
+                                 out_depth, out_debug, counters, s);
     cudaError_t e2 = cudaFreeAsync(ws.base, s);
     if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
     if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(frame tables)");
     return NSL_OK;
+}
+
+nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                                 const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                                 const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                                 float* out_rgbt, float* out_depth, uint32_t* out_debug, nsl_stream stream) {
+    return batch_impl(vols, n_vols, frame_vol, cams, lights, n_lights, light_mode, med, m, frame_ids, F, out_rgbt,
+                      out_depth, out_debug, nullptr, stream);
+}
+
+nsl_status nsl_guiding_map_batch_counted(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                                         const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
+                                         int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                                         const uint32_t* frame_ids, int32_t F, float* out_rgbt, float* out_depth,
+                                         uint64_t* counters, nsl_stream stream) {
+    if (!counters) {
+        g_err = "counters is NULL";
+        return NSL_ERR_INVALID_ARG;
+    }
+    NSL_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint64_t), reinterpret_cast<cudaStream_t>(stream)),
+             "cudaMemsetAsync(counters)");
+    return batch_impl(vols, n_vols, frame_vol, cams, lights, n_lights, light_mode, med, m, frame_ids, F, out_rgbt,
+                      out_depth, nullptr, reinterpret_cast<unsigned long long*>(counters), stream);
 }
 
 nsl_status nsl_guiding_map(const nsl_volume* vol, const nsl_camera* cam, const nsl_light* lights, int32_t n_lights,

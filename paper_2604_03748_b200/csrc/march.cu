@@ -2,12 +2,19 @@
 // L394-407; C3-C12) for sm_100a.
 //
 // One thread per pixel; a warp marches a coherent 8x4 pixel tile, a CTA a
-// 16x8 tile; blockIdx.y is the frame of the batch (row a9).  Sample
-// positions use only explicitly rounded fp32 operations (__fmaf_rn,
+// 16x16 tile (8 warps); blockIdx.y is the frame of the batch (row a9).
+// Sample positions use only explicitly rounded fp32 operations (__fmaf_rn,
 // __fmul_rn) so that every index decision is bit-identical to the oracle
 // (C14); values are fp32 with FMA lerps.  The step range is
 // clipped exactly (C5) and each light march's length is computed exactly
 // (C8) so the inner loops carry no bounds tests.
+//
+// The path is bound by L1 data-pipe wavefronts of the trilinear gathers
+// (profiles/).  Before gathering, every sample tests the
+// volume's occupancy bitmask, staged per CTA in shared memory: a sample
+// whose cell lies in an all-zero block is exactly 0 (C1), so skipping its
+// loads changes no bit of the result while removing most of the wavefronts
+// (empty space outside the smoke).
 #include <cuda_fp16.h>
 
 #include "nsl_internal.cuh"
@@ -15,11 +22,14 @@
 namespace nsl {
 namespace {
 
-constexpr int kTileW = 16, kTileH = 8, kThreads = 128;
+constexpr int kTileW = 16, kTileH = 16, kThreads = 256;
+constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
     const void* __restrict__ data;
+    const uint32_t* mask;  // shared memory
     int sy, sz;
+    int shift, nbx, nby;
     float sx1, sy1, sz1;   // support upper bounds n+1
 };
 
@@ -30,12 +40,16 @@ __device__ __forceinline__ bool inside(const Vol& v, float x, float y, float z) 
 }
 
 // C1 trilinear at an in-support padded-index position (corners always exist
-// thanks to the apron).  floor and fraction are exact in fp32.
-template <int LAYOUT>
-__device__ __forceinline__ float sample(const Vol& v, float x, float y, float z) {
+// thanks to the apron).  floor and fraction are exact in fp32.  Samples in an
+// empty occupancy block return 0 without touching global memory.
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
     const float fx0 = floorf(x), fy0 = floorf(y), fz0 = floorf(z);
-    const float fx = __fsub_rn(x, fx0), fy = __fsub_rn(y, fy0), fz = __fsub_rn(z, fz0);
     const int ix = (int)fx0, iy = (int)fy0, iz = (int)fz0;
+    const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
+    if (!((v.mask[b >> 5] >> (b & 31)) & 1u)) return 0.0f;
+    if (COUNT) ++gathers;
+    const float fx = __fsub_rn(x, fx0), fy = __fsub_rn(y, fy0), fz = __fsub_rn(z, fz0);
     const int e = ix + iy * v.sy + iz * v.sz;
     if (LAYOUT == kLinearF32) {
         const float* p = static_cast<const float*>(v.data) + e;
@@ -55,10 +69,10 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z)
     } else {
         const uint4 u = __ldg(static_cast<const uint4*>(v.data) + e);
         const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
-        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+        const float2 bb = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
         const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
         const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
-        const float x00 = lerpf(a.x, a.y, fx), x10 = lerpf(b.x, b.y, fx);
+        const float x00 = lerpf(a.x, a.y, fx), x10 = lerpf(bb.x, bb.y, fx);
         const float x01 = lerpf(c.x, c.y, fx), x11 = lerpf(d.x, d.y, fx);
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
     }
@@ -100,6 +114,22 @@ struct Ray {
     }
 };
 
+__device__ __forceinline__ void slab(float o, float d, float s, float eps, float& t0, float& t1, bool& miss) {
+    if (d != 0.0f) {
+        const float inv = 1.0f / d;
+        float ta = (-eps - o) * inv, tb = (s + eps - o) * inv;
+        if (ta > tb) {
+            const float tt = ta;
+            ta = tb;
+            tb = tt;
+        }
+        t0 = fmaxf(t0, ta);
+        t1 = fminf(t1, tb);
+    } else if (!(o > -eps && o < s + eps)) {
+        miss = true;
+    }
+}
+
 // C5: exact first/last in-support step in [1, Ncap] (0,-1 if none).  A float
 // slab test on the box expanded by 1e-3 index units brackets the range to
 // within one step; exact per-sample tests then shrink it (the in-support set
@@ -109,24 +139,11 @@ __device__ __forceinline__ void clip_ray(const Ray& r, const Vol& v, int Ncap, i
     n1 = -1;
     const float eps = 1e-3f;
     float t0 = -3.0e38f, t1 = 3.0e38f;
-    const float o[3] = {r.ox, r.oy, r.oz}, d[3] = {r.dx, r.dy, r.dz}, s[3] = {v.sx1, v.sy1, v.sz1};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (d[a] != 0.0f) {
-            const float inv = 1.0f / d[a];
-            float ta = (-eps - o[a]) * inv, tb = (s[a] + eps - o[a]) * inv;
-            if (ta > tb) {
-                const float tt = ta;
-                ta = tb;
-                tb = tt;
-            }
-            t0 = fmaxf(t0, ta);
-            t1 = fminf(t1, tb);
-        } else if (!(o[a] > -eps && o[a] < s[a] + eps)) {
-            return;
-        }
-    }
-    if (!(t0 <= t1)) return;
+    bool miss = false;
+    slab(r.ox, r.dx, v.sx1, eps, t0, t1, miss);
+    slab(r.oy, r.dy, v.sy1, eps, t0, t1, miss);
+    slab(r.oz, r.dz, v.sz1, eps, t0, t1, miss);
+    if (miss || !(t0 <= t1)) return;
     float a = floorf((t0 - r.delta) / r.h), b = ceilf((t1 - r.delta) / r.h);
     a = fmaxf(a, 1.0f);
     b = fminf(b, (float)Ncap);
@@ -161,20 +178,21 @@ __device__ __forceinline__ int light_count(const Vol& v, float ux, float uy, flo
     return M;
 }
 
-// sum of rho over j = 1..M along the light (all in support)
-template <int LAYOUT>
+// sum of rho over j = 1..M along the light (all in support); two independent
+// accumulators give the scheduler two gathers in flight per thread.
+template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ float light_sum(const Vol& v, float ux, float uy, float uz, float lx, float ly, float lz,
-                                           float hl, int M) {
+                                           float hl, int M, uint32_t& gathers) {
     float acc0 = 0.0f, acc1 = 0.0f;
     int j = 1;
     for (; j + 1 <= M; j += 2) {
         const float s0 = __fmul_rn((float)j, hl), s1 = __fmul_rn((float)(j + 1), hl);
-        acc0 += sample<LAYOUT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz));
-        acc1 += sample<LAYOUT>(v, __fmaf_rn(s1, lx, ux), __fmaf_rn(s1, ly, uy), __fmaf_rn(s1, lz, uz));
+        acc0 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
+        acc1 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s1, lx, ux), __fmaf_rn(s1, ly, uy), __fmaf_rn(s1, lz, uz), gathers);
     }
     if (j <= M) {
         const float s0 = __fmul_rn((float)j, hl);
-        acc0 += sample<LAYOUT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz));
+        acc0 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
     }
     return acc0 + acc1;
 }
@@ -184,140 +202,176 @@ __device__ __forceinline__ float hg32(float g, float c) {
     return (1.0f - g * g) / (12.566370614359172f * d * sqrtf(d));
 }
 
-template <int LAYOUT, int PROJ, bool DEBUG>
+template <int LAYOUT, int PROJ, int MODE>
 __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
-                                                         uint32_t* __restrict__ out_debug, int W, int H,
+                                                         uint32_t* __restrict__ out_debug,
+                                                         unsigned long long* __restrict__ counters, int W, int H,
                                                          int tiles_x) {
-    __shared__ __align__(16) FrameParams sp;
+    constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
+    extern __shared__ __align__(16) uint4 smem[];
+    FrameParams& sp = *reinterpret_cast<FrameParams*>(smem);
+    uint4* smask4 = smem + sizeof(FrameParams) / 16;
     const int f = blockIdx.y;
     {
-        const int4* src = reinterpret_cast<const int4*>(fps + f);
-        int4* dst = reinterpret_cast<int4*>(&sp);
-        for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 16); i += blockDim.x) dst[i] = src[i];
+        const uint4* src = reinterpret_cast<const uint4*>(fps + f);
+        for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 16); i += blockDim.x) smem[i] = src[i];
+    }
+    __syncthreads();
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(sp.occ);
+        const int n4 = sp.occ_words >> 2;
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) smask4[i] = __ldg(src + i);
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
     const int px = tx * kTileW + (warp & 1) * 8 + (lane & 7);
     const int py = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);
-    if (px >= W || py >= H) return;
+    const bool valid = px < W && py < H;
+    if (!COUNT && !valid) return;
 
     Vol v;
     v.data = sp.data;
+    v.mask = reinterpret_cast<const uint32_t*>(smask4);
     v.sy = sp.sy;
     v.sz = sp.sz;
+    v.shift = sp.occ_shift;
+    v.nbx = sp.occ_nbx;
+    v.nby = sp.occ_nby;
     v.sx1 = sp.supp[0];
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
 
-    // ---- a2: ray (C3), jitter (C4)
-    Ray r;
-    float P[4];
-    const float fpx = (float)px, fpy = (float)py;
-    if (PROJ == 0) {
-        r.ox = __fmaf_rn(fpy, sp.Ey[0], __fmaf_rn(fpx, sp.Ex[0], sp.B[0]));
-        r.oy = __fmaf_rn(fpy, sp.Ey[1], __fmaf_rn(fpx, sp.Ex[1], sp.B[1]));
-        r.oz = __fmaf_rn(fpy, sp.Ey[2], __fmaf_rn(fpx, sp.Ex[2], sp.B[2]));
-        r.dx = sp.Dg[0];
-        r.dy = sp.Dg[1];
-        r.dz = sp.Dg[2];
+    uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0;
+    if (valid) {
+        // ---- a2: ray (C3), jitter (C4)
+        Ray r;
+        float P[4];
+        const float fpx = (float)px, fpy = (float)py;
+        if (PROJ == 0) {
+            r.ox = __fmaf_rn(fpy, sp.Ey[0], __fmaf_rn(fpx, sp.Ex[0], sp.B[0]));
+            r.oy = __fmaf_rn(fpy, sp.Ey[1], __fmaf_rn(fpx, sp.Ex[1], sp.B[1]));
+            r.oz = __fmaf_rn(fpy, sp.Ey[2], __fmaf_rn(fpx, sp.Ex[2], sp.B[2]));
+            r.dx = sp.Dg[0];
+            r.dy = sp.Dg[1];
+            r.dz = sp.Dg[2];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) P[l] = sp.P[l];
-    } else {
-        const float d0 = __fmaf_rn(fpy, sp.Ey[0], __fmaf_rn(fpx, sp.Ex[0], sp.F0[0]));
-        const float d1 = __fmaf_rn(fpy, sp.Ey[1], __fmaf_rn(fpx, sp.Ex[1], sp.F0[1]));
-        const float d2 = __fmaf_rn(fpy, sp.Ey[2], __fmaf_rn(fpx, sp.Ex[2], sp.F0[2]));
-        const float q = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
-        const float inv = __fdiv_rn(1.0f, __fsqrt_rn(q));
-        const float dir0 = __fmul_rn(d0, inv), dir1 = __fmul_rn(d1, inv), dir2 = __fmul_rn(d2, inv);
-        r.dx = __fmul_rn(dir0, sp.inv_dx);
-        r.dy = __fmul_rn(dir1, sp.inv_dx);
-        r.dz = __fmul_rn(dir2, sp.inv_dx);
-        r.ox = sp.Oe[0];
-        r.oy = sp.Oe[1];
-        r.oz = sp.Oe[2];
+            for (int l = 0; l < 4; ++l) P[l] = sp.P[l];
+        } else {
+            const float d0 = __fmaf_rn(fpy, sp.Ey[0], __fmaf_rn(fpx, sp.Ex[0], sp.F0[0]));
+            const float d1 = __fmaf_rn(fpy, sp.Ey[1], __fmaf_rn(fpx, sp.Ex[1], sp.F0[1]));
+            const float d2 = __fmaf_rn(fpy, sp.Ey[2], __fmaf_rn(fpx, sp.Ex[2], sp.F0[2]));
+            const float q = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+            const float inv = __fdiv_rn(1.0f, __fsqrt_rn(q));
+            const float dir0 = __fmul_rn(d0, inv), dir1 = __fmul_rn(d1, inv), dir2 = __fmul_rn(d2, inv);
+            r.dx = __fmul_rn(dir0, sp.inv_dx);
+            r.dy = __fmul_rn(dir1, sp.inv_dx);
+            r.dz = __fmul_rn(dir2, sp.inv_dx);
+            r.ox = sp.Oe[0];
+            r.oy = sp.Oe[1];
+            r.oz = sp.Oe[2];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) P[l] = hg32(mc.g, sp.Ln[l][0] * dir0 + sp.Ln[l][1] * dir1 + sp.Ln[l][2] * dir2);
-    }
-    r.h = mc.h;
-    const uint32_t pix = (uint32_t)py * (uint32_t)W + (uint32_t)px;
-    r.delta = mc.jitter ? jitter_delta(jitter_hash(mc.seed_lo, mc.seed_hi, sp.frame_id, pix), mc.h) : 0.0f;
+            for (int l = 0; l < 4; ++l)
+                P[l] = hg32(mc.g, sp.Ln[l][0] * dir0 + sp.Ln[l][1] * dir1 + sp.Ln[l][2] * dir2);
+        }
+        r.h = mc.h;
+        const uint32_t pix = (uint32_t)py * (uint32_t)W + (uint32_t)px;
+        r.delta = mc.jitter ? jitter_delta(jitter_hash(mc.seed_lo, mc.seed_hi, sp.frame_id, pix), mc.h) : 0.0f;
 
-    // ---- C5 clip
-    int n_lo, n_hi;
-    clip_ray(r, v, mc.Ncap, n_lo, n_hi);
+        // ---- C5 clip
+        int n_lo, n_hi;
+        clip_ray(r, v, mc.Ncap, n_lo, n_hi);
 
-    // ---- a4-a7 march
-    float tau = 0.0f, T = 1.0f, Dout = 0.0f;
-    float S[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    int n_hit = 0, n_term = n_hi > 0 ? n_hi : 0;
-    uint32_t n_occ = 0, lsamp = 0;
-    const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && n_lo >= 2;
-    for (int n = n_lo; n <= n_hi; ++n) {
-        float t, x, y, z;
-        r.at(n, t, x, y, z);
-        const float rho = sample<LAYOUT>(v, x, y, z);
-        if (rho > 0.0f) {
-            ++n_occ;
-            const float sig_t = mc.kappa * rho;
-            const float sig_s = mc.alpha * sig_t;
-            if (n_hit == 0 && sig_s > mc.tau_d) {   // C6
-                n_hit = n;
-                Dout = t;
-            }
-            const float s = sig_t * mc.h;            // C7
-            const float Tp = T;
-            tau += s;
-            T = __expf(-tau);
-            float A;
-            if (mc.form == NSL_OPACITY_EXP) A = mc.alpha * (Tp - T);
-            else if (mc.form == NSL_OPACITY_RIEMANN) A = mc.alpha * Tp * s;
-            else A = Tp * sig_s;
+        // ---- a4-a7 march
+        float tau = 0.0f, T = 1.0f, Dout = 0.0f;
+        float S[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        int n_hit = 0, n_term = n_hi > 0 ? n_hi : 0;
+        uint32_t n_occ = 0, lsamp = 0;
+        const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && n_lo >= 2;
+        for (int n = n_lo; n <= n_hi; ++n) {
+            float t, x, y, z;
+            r.at(n, t, x, y, z);
+            const float rho = sample<LAYOUT, COUNT>(v, x, y, z, c_gath);
+            if (rho > 0.0f) {
+                ++n_occ;
+                const float sig_t = mc.kappa * rho;
+                const float sig_s = mc.alpha * sig_t;
+                if (n_hit == 0 && sig_s > mc.tau_d) {   // C6
+                    n_hit = n;
+                    Dout = t;
+                }
+                const float s = sig_t * mc.h;            // C7
+                const float Tp = T;
+                tau += s;
+                T = __expf(-tau);
+                float A;
+                if (mc.form == NSL_OPACITY_EXP) A = mc.alpha * (Tp - T);
+                else if (mc.form == NSL_OPACITY_RIEMANN) A = mc.alpha * Tp * s;
+                else A = Tp * sig_s;
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {             // C8 + C10
-                if (l < mc.n_lights) {
-                    float Tl;
-                    if (l == 0 && front_fast) {
-                        Tl = Tp;                      // C9: T^front_n = T_{n-1}
-                    } else {
+                for (int l = 0; l < 4; ++l) {             // C8 + C10
+                    if (l < mc.n_lights) {
+                        float Tl;
                         const float lx = sp.Lg[l][0], ly = sp.Lg[l][1], lz = sp.Lg[l][2];
-                        const int M = light_count(v, x, y, z, lx, ly, lz, mc.hl);
-                        const float sum = light_sum<LAYOUT>(v, x, y, z, lx, ly, lz, mc.hl, M);
-                        Tl = __expf(-(mc.hl * mc.kappa) * sum);
-                        lsamp += (uint32_t)M;
+                        if (l == 0 && front_fast) {
+                            Tl = Tp;                      // C9: T^front_n = T_{n-1}
+                            if (COUNT) lsamp += (uint32_t)light_count(v, x, y, z, lx, ly, lz, mc.hl);
+                        } else {
+                            const int M = light_count(v, x, y, z, lx, ly, lz, mc.hl);
+                            const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, M, c_gath);
+                            Tl = __expf(-(mc.hl * mc.kappa) * sum);
+                            lsamp += (uint32_t)M;
+                        }
+                        S[l] = __fmaf_rn(A, Tl, S[l]);
                     }
-                    S[l] = __fmaf_rn(A, Tl, S[l]);
+                }
+                if (T < mc.t_min) {                       // C11
+                    n_term = n;
+                    break;
                 }
             }
-            if (T < mc.t_min) {                       // C11
-                n_term = n;
-                break;
+        }
+        // ---- a6/a8: L_c = sum_l rgb_lc P_l S_l; vectorised stores
+        float L0 = 0.0f, L1 = 0.0f, L2 = 0.0f;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            if (l < mc.n_lights) {
+                const float w = P[l] * S[l];
+                L0 += sp.rgb[l][0] * w;
+                L1 += sp.rgb[l][1] * w;
+                L2 += sp.rgb[l][2] * w;
             }
         }
-    }
-    // ---- a6/a8: L_c = sum_l rgb_lc P_l S_l; vectorised stores
-    float L0 = 0.0f, L1 = 0.0f, L2 = 0.0f;
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-        if (l < mc.n_lights) {
-            const float w = P[l] * S[l];
-            L0 += sp.rgb[l][0] * w;
-            L1 += sp.rgb[l][1] * w;
-            L2 += sp.rgb[l][2] * w;
+        const size_t o = (size_t)f * (size_t)W * (size_t)H + pix;
+        out_rgbt[o] = make_float4(L0, L1, L2, T);
+        out_depth[o] = Dout;
+        const bool hit_support = n_lo > 0 && n_hi >= n_lo;
+        if (DEBUG) {
+            uint32_t* dbg = out_debug + o * 6;
+            dbg[0] = hit_support ? (uint32_t)n_lo : 0u;
+            dbg[1] = hit_support ? (uint32_t)n_hi : 0u;
+            dbg[2] = (uint32_t)n_hit;
+            dbg[3] = (uint32_t)n_term;
+            dbg[4] = n_occ;
+            dbg[5] = lsamp;
+        }
+        if (COUNT) {
+            c_prim = hit_support ? (uint32_t)(n_term - n_lo + 1) : 0u;
+            c_light = lsamp;
+            c_occ = n_occ;
         }
     }
-    const size_t o = (size_t)f * (size_t)W * (size_t)H + pix;
-    out_rgbt[o] = make_float4(L0, L1, L2, T);
-    out_depth[o] = Dout;
-    if (DEBUG) {
-        uint32_t* dbg = out_debug + o * 6;
-        dbg[0] = n_hi >= n_lo && n_lo > 0 ? (uint32_t)n_lo : 0u;
-        dbg[1] = n_hi >= n_lo && n_lo > 0 ? (uint32_t)n_hi : 0u;
-        dbg[2] = (uint32_t)n_hit;
-        dbg[3] = (uint32_t)n_term;
-        dbg[4] = n_occ;
-        dbg[5] = lsamp;
+    if (COUNT) {
+        __shared__ unsigned int red[4];
+        if (threadIdx.x < 4) red[threadIdx.x] = 0;
+        __syncthreads();
+        atomicAdd(&red[0], c_prim);
+        atomicAdd(&red[1], c_light);
+        atomicAdd(&red[2], c_gath);
+        atomicAdd(&red[3], c_occ);
+        __syncthreads();
+        if (threadIdx.x < 4) atomicAdd(counters + threadIdx.x, (unsigned long long)red[threadIdx.x]);
     }
 }
 
@@ -329,33 +383,45 @@ __global__ void jitter_debug_kernel(MarchConst mc, uint32_t frame, int n, uint32
     delta[p] = mc.jitter ? jitter_delta(h, mc.h) : 0.0f;
 }
 
-template <int LAYOUT, int PROJ>
-cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
-                      uint32_t* debug, cudaStream_t s) {
+template <int LAYOUT, int PROJ, int MODE>
+cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, size_t smem, float4* rgbt,
+                       float* depth, uint32_t* debug, unsigned long long* counters, cudaStream_t s) {
     const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
     dim3 grid((unsigned)(tiles_x * tiles_y), (unsigned)F);
-    if (debug)
-        march_kernel<LAYOUT, PROJ, true><<<grid, kThreads, 0, s>>>(fp, mc, rgbt, depth, debug, W, H, tiles_x);
-    else
-        march_kernel<LAYOUT, PROJ, false><<<grid, kThreads, 0, s>>>(fp, mc, rgbt, depth, debug, W, H, tiles_x);
+    auto k = march_kernel<LAYOUT, PROJ, MODE>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<grid, kThreads, smem, s>>>(fp, mc, rgbt, depth, debug, counters, W, H, tiles_x);
     return cudaGetLastError();
 }
 
+template <int LAYOUT, int PROJ>
+cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, size_t smem, float4* rgbt,
+                      float* depth, uint32_t* debug, unsigned long long* counters, cudaStream_t s) {
+    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
+    if (counters) return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
+    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
+}
+
 template <int LAYOUT>
-cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, float4* rgbt,
-                     float* depth, uint32_t* debug, cudaStream_t s) {
-    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, rgbt, depth, debug, s)
-                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, rgbt, depth, debug, s);
+cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, size_t smem,
+                     float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters, cudaStream_t s) {
+    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s)
+                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
 }
 
 }  // namespace
 
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection, int layout,
-                         float4* rgbt, float* depth, uint32_t* debug, cudaStream_t s) {
+                         int max_occ_words, float4* rgbt, float* depth, uint32_t* debug,
+                         unsigned long long* counters, cudaStream_t s) {
+    const size_t smem = sizeof(FrameParams) + (size_t)max_occ_words * 4;
     switch (layout) {
-        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, s);
-        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, s);
-        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, s);
+        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, s);
+        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, s);
+        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -9,12 +9,24 @@
 
 namespace nsl {
 
+// Occupancy bitmask geometry (DESIGN.md §6 "empty-space skip"): one bit per
+// block of (2^shift)^3 padded cells; cell c = floor(U) in [0, n] per axis.
+// A clear bit means every corner of every cell of the block is 0, so any
+// trilinear sample whose cell lies in the block is exactly 0 (C1).
+struct OccGeom {
+    int32_t shift, nbx, nby, nbz;
+    int32_t words;             // ceil(nbx*nby*nbz / 32), padded to a multiple of 4
+};
+OccGeom occ_geom(int nx, int ny, int nz);
+
 // Per-volume description handed to the frame-setup kernel.
 struct VolDesc {
     const void* data;
     int32_t nx, ny, nz, layout;
     float origin[3];
     float dx;
+    const uint32_t* occ;
+    OccGeom og;
 };
 
 // Raw per-frame input (host -> device, one memcpy per call).
@@ -39,7 +51,8 @@ struct FrameParams {
     float Ln[4][3], Lg[4][3], P[4], rgb[4][3];
     uint32_t frame_id;
     int32_t front_ok;          // C9 preconditions hold for this frame
-    int32_t pad[2];
+    const uint32_t* occ;       // occupancy bitmask (global), staged to shared memory per CTA
+    int32_t occ_shift, occ_nbx, occ_nby, occ_words;
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 
@@ -62,10 +75,13 @@ constexpr int kCornerF16 = NSL_LAYOUT_CORNER_F16;
 // Launch helpers implemented in the .cu files.
 cudaError_t launch_layout(const float* raw, const VolDesc& v, void* storage, unsigned long long* invalid,
                           cudaStream_t s);
+cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, cudaStream_t s);
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s);
+// mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection,
-                         int layout, float4* rgbt, float* depth, uint32_t* debug, cudaStream_t s);
+                         int layout, int max_occ_words, float4* rgbt, float* depth, uint32_t* debug,
+                         unsigned long long* counters, cudaStream_t s);
 cudaError_t launch_jitter_debug(const MarchConst& mc, uint32_t frame_id, int n, uint32_t* hash, float* delta,
                                 cudaStream_t s);
 

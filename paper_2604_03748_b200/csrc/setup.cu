@@ -63,7 +63,11 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
     p.W = cam.width;
     p.H = cam.height;
     p.frame_id = fr.frame_id;
-    p.pad[0] = p.pad[1] = 0;
+    p.occ = fr.vol.occ;
+    p.occ_shift = fr.vol.og.shift;
+    p.occ_nbx = fr.vol.og.nbx;
+    p.occ_nby = fr.vol.og.nby;
+    p.occ_words = fr.vol.og.words;
 
     // ---- camera basis (C3)
     const double dx = (double)fr.vol.dx;

@@ -5,6 +5,8 @@
 // never bounds-checks a corner.  One thread per output element: the writes
 // are fully coalesced, the gathers from the x-fastest raw grid are
 // sector-coalesced along x.  HBM-bound: bytes = raw read + layout write.
+#include <cstdlib>
+
 #include <cuda_fp16.h>
 
 #include "nsl_internal.cuh"
@@ -94,7 +96,60 @@ __global__ void layout_corner_f16_kernel(Raw r, uint4* __restrict__ out, unsigne
     }
 }
 
+// One thread per occupancy block: the block is non-empty iff some padded
+// voxel in [b*B, b*B + B]^3 (the corners of its cells) is nonzero.
+__global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g) {
+    const int B = 1 << g.shift;
+    const int total = g.nbx * g.nby * g.nbz;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < total; b += gridDim.x * blockDim.x) {
+        const int bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        const int x0 = max(bx * B, 1), x1 = min(bx * B + B, r.nx);
+        const int y0 = max(by * B, 1), y1 = min(by * B + B, r.ny);
+        const int z0 = max(bz * B, 1), z1 = min(bz * B + B, r.nz);
+        bool any = false;
+        for (int k = z0; k <= z1 && !any; ++k)
+            for (int j = y0; j <= y1 && !any; ++j)
+                for (int i = x0; i <= x1; ++i)
+                    if (r.at(i, j, k) != 0.0f) {
+                        any = true;
+                        break;
+                    }
+        if (any) atomicOr(mask + (b >> 5), 1u << (b & 31));
+    }
+}
+
 }  // namespace
+
+// Occupancy block size: the smallest 2^shift (shift >= 1) whose bitmask fits
+// the per-CTA shared-memory budget (default 40 KB; NSL_OCC_BUDGET / NSL_OCC_SHIFT
+// override for experiments).
+OccGeom occ_geom(int nx, int ny, int nz) {
+    long budget = 40 * 1024;
+    if (const char* e = getenv("NSL_OCC_BUDGET")) budget = atol(e);
+    int forced = 0;
+    if (const char* e = getenv("NSL_OCC_SHIFT")) forced = atoi(e);
+    OccGeom g{};
+    for (int s = forced > 0 ? forced : 1; s <= 10; ++s) {
+        const int B = 1 << s;
+        g.shift = s;
+        g.nbx = (nx + 1 + B - 1) / B;
+        g.nby = (ny + 1 + B - 1) / B;
+        g.nbz = (nz + 1 + B - 1) / B;
+        const long bits = (long)g.nbx * g.nby * g.nbz;
+        g.words = (int)(((bits + 31) / 32 + 3) / 4 * 4);
+        if (forced > 0 || (long)g.words * 4 <= budget) break;
+    }
+    return g;
+}
+
+cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, cudaStream_t s) {
+    Raw r{raw, v.nx, v.ny, v.nz};
+    cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)v.og.words * 4, s);
+    if (e != cudaSuccess) return e;
+    const int total = v.og.nbx * v.og.nby * v.og.nbz;
+    occupancy_kernel<<<(total + 127) / 128, 128, 0, s>>>(r, mask, v.og);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_layout(const float* raw, const VolDesc& v, void* storage, unsigned long long* invalid,
                           cudaStream_t s) {

@@ -60,7 +60,8 @@ def test_volume_bytes(nsl):
     lin = nsl.volume_bytes(g, nsl.LAYOUT_LINEAR_F32)
     quad = nsl.volume_bytes(g, nsl.LAYOUT_QUAD_F32)
     f16 = nsl.volume_bytes(g, nsl.LAYOUT_CORNER_F16)
-    tail = 256
+    # body | occupancy mask (2x2x2-cell blocks: 3*3*4 bits -> 4 words -> one 256-B slot) | 256-B tail
+    tail = 256 + 256
     up = lambda x: (x + 255) // 256 * 256
     assert lin == up(6 * 7 * 8 * 4) + tail
     assert quad == up(5 * 6 * 8 * 16) + tail
