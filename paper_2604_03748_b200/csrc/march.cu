@@ -2,7 +2,7 @@
 // L394-407; C3-C12) for sm_100a.
 //
 // One thread per pixel; a warp marches a coherent 8x4 pixel tile, a CTA a
-// 16x16 tile (8 warps); blockIdx.y is the frame of the batch (row a9).
+// 16x16 tile (8 warps); blockIdx.z is the frame of the batch (row a9).
 // Sample positions use only explicitly rounded fp32 operations (__fmaf_rn,
 // __fmul_rn) so that every index decision is bit-identical to the oracle
 // (C14); values are fp32 with FMA lerps.  The step range is
@@ -114,9 +114,10 @@ struct Ray {
     }
 };
 
-__device__ __forceinline__ void slab(float o, float d, float s, float eps, float& t0, float& t1, bool& miss) {
+// inv: 1/d (per-frame constant for orthographic cameras, computed per ray otherwise)
+__device__ __forceinline__ void slab(float o, float d, float inv, float s, float eps, float& t0, float& t1,
+                                     bool& miss) {
     if (d != 0.0f) {
-        const float inv = 1.0f / d;
         float ta = (-eps - o) * inv, tb = (s + eps - o) * inv;
         if (ta > tb) {
             const float tt = ta;
@@ -134,17 +135,18 @@ __device__ __forceinline__ void slab(float o, float d, float s, float eps, float
 // slab test on the box expanded by 1e-3 index units brackets the range to
 // within one step; exact per-sample tests then shrink it (the in-support set
 // is contiguous because every coordinate is monotone in n).
-__device__ __forceinline__ void clip_ray(const Ray& r, const Vol& v, int Ncap, int& n0, int& n1) {
+__device__ __forceinline__ void clip_ray(const Ray& r, const Vol& v, const float inv[3], float inv_h, int Ncap,
+                                         int& n0, int& n1) {
     n0 = 0;
     n1 = -1;
     const float eps = 1e-3f;
     float t0 = -3.0e38f, t1 = 3.0e38f;
     bool miss = false;
-    slab(r.ox, r.dx, v.sx1, eps, t0, t1, miss);
-    slab(r.oy, r.dy, v.sy1, eps, t0, t1, miss);
-    slab(r.oz, r.dz, v.sz1, eps, t0, t1, miss);
+    slab(r.ox, r.dx, inv[0], v.sx1, eps, t0, t1, miss);
+    slab(r.oy, r.dy, inv[1], v.sy1, eps, t0, t1, miss);
+    slab(r.oz, r.dz, inv[2], v.sz1, eps, t0, t1, miss);
     if (miss || !(t0 <= t1)) return;
-    float a = floorf((t0 - r.delta) / r.h), b = ceilf((t1 - r.delta) / r.h);
+    float a = floorf((t0 - r.delta) * inv_h) - 1.0f, b = ceilf((t1 - r.delta) * inv_h) + 1.0f;
     a = fmaxf(a, 1.0f);
     b = fminf(b, (float)Ncap);
     if (!(a <= b)) return;
@@ -157,17 +159,11 @@ __device__ __forceinline__ void clip_ray(const Ray& r, const Vol& v, int Ncap, i
 }
 
 // C8: M = number of leading in-support light samples Y_j = fma(j*h_l, L, U).
+// lim/ilh: per-frame exit plane and 1/(L*h_l) per axis (FrameParams) -> estimate, then exact fix-up.
 __device__ __forceinline__ int light_count(const Vol& v, float ux, float uy, float uz, float lx, float ly, float lz,
-                                           float hl) {
-    float smax = 3.0e38f;
-    if (lx > 0.0f) smax = fminf(smax, __fdividef(v.sx1 - ux, lx));
-    else if (lx < 0.0f) smax = fminf(smax, __fdividef(-ux, lx));
-    if (ly > 0.0f) smax = fminf(smax, __fdividef(v.sy1 - uy, ly));
-    else if (ly < 0.0f) smax = fminf(smax, __fdividef(-uy, ly));
-    if (lz > 0.0f) smax = fminf(smax, __fdividef(v.sz1 - uz, lz));
-    else if (lz < 0.0f) smax = fminf(smax, __fdividef(-uz, lz));
-    float mf = floorf(__fdividef(smax, hl));
-    mf = fminf(fmaxf(mf, 0.0f), 16777216.0f);
+                                           float hl, const float lim[3], const float ilh[3]) {
+    const float m = fminf(fminf((lim[0] - ux) * ilh[0], (lim[1] - uy) * ilh[1]), (lim[2] - uz) * ilh[2]);
+    const float mf = fminf(fmaxf(floorf(m), 0.0f), 16777216.0f);
     int M = (int)mf;
     auto in_j = [&](int j) {
         const float s = __fmul_rn((float)j, hl);
@@ -197,6 +193,26 @@ __device__ __forceinline__ float light_sum(const Vol& v, float ux, float uy, flo
     return acc0 + acc1;
 }
 
+// The guide set's top and bottom lights are exact opposites (L_g,2 = -L_g,1 bit
+// for bit): both marches walk the same line through U in opposite directions.
+// One loop serves both: s_j is shared and fma(-s, L, U) == fma(s, -L, U) exactly,
+// so the positions are the canonical ones of C8 for each light.
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy, float uz, float lx, float ly,
+                                               float lz, float hl, int Ma, int Mb, float& sa, float& sb,
+                                               uint32_t& gathers) {
+    float a = 0.0f, b = 0.0f;
+    const int M = max(Ma, Mb);
+    for (int j = 1; j <= M; ++j) {
+        const float s = __fmul_rn((float)j, hl);
+        if (j <= Ma) a += sample<LAYOUT, COUNT>(v, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), __fmaf_rn(s, lz, uz), gathers);
+        if (j <= Mb)
+            b += sample<LAYOUT, COUNT>(v, __fmaf_rn(-s, lx, ux), __fmaf_rn(-s, ly, uy), __fmaf_rn(-s, lz, uz), gathers);
+    }
+    sa = a;
+    sb = b;
+}
+
 __device__ __forceinline__ float hg32(float g, float c) {
     const float d = (1.0f + g * g) - 2.0f * g * c;
     return (1.0f - g * g) / (12.566370614359172f * d * sqrtf(d));
@@ -206,30 +222,22 @@ template <int LAYOUT, int PROJ, int MODE>
 __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
-                                                         unsigned long long* __restrict__ counters, int W, int H,
-                                                         int tiles_x) {
+                                                         unsigned long long* __restrict__ counters, int W, int H) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
     extern __shared__ __align__(16) uint4 smem[];
     FrameParams& sp = *reinterpret_cast<FrameParams*>(smem);
     uint4* smask4 = smem + sizeof(FrameParams) / 16;
-    const int f = blockIdx.y;
+    const int f = blockIdx.z;
     {
         const uint4* src = reinterpret_cast<const uint4*>(fps + f);
         for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 16); i += blockDim.x) smem[i] = src[i];
     }
     __syncthreads();
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(sp.occ);
-        const int n4 = sp.occ_words >> 2;
-        for (int i = threadIdx.x; i < n4; i += blockDim.x) smask4[i] = __ldg(src + i);
-    }
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
-    const int px = tx * kTileW + (warp & 1) * 8 + (lane & 7);
-    const int py = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);
+    const int px = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
+    const int py = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
     const bool valid = px < W && py < H;
-    if (!COUNT && !valid) return;
+    const size_t o = (size_t)f * (size_t)W * (size_t)H + (size_t)py * W + px;
 
     Vol v;
     v.data = sp.data;
@@ -243,11 +251,48 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
 
+    if (PROJ == 0) {
+        // Tile culling (exact): every ray of the tile is parallel to D_g with its origin
+        // within tile_r of the centre ray; if the centre ray misses the support box
+        // expanded by tile_r, no sample of the tile is in support (C5) and the
+        // output is the empty map (L = 0, T = 1, D = 0, counters 0).
+        const float cx = (float)(blockIdx.x * kTileW) + 7.5f, cy = (float)(blockIdx.y * kTileH) + 7.5f;
+        Ray c;
+        c.ox = fmaf(cy, sp.Ey[0], fmaf(cx, sp.Ex[0], sp.B[0]));
+        c.oy = fmaf(cy, sp.Ey[1], fmaf(cx, sp.Ex[1], sp.B[1]));
+        c.oz = fmaf(cy, sp.Ey[2], fmaf(cx, sp.Ex[2], sp.B[2]));
+        float t0 = -3.0e38f, t1 = 3.0e38f;
+        bool miss = false;
+        const float rr = sp.tile_r;
+        slab(c.ox + rr, sp.Dg[0], sp.invD[0], v.sx1 + 2.0f * rr, 0.0f, t0, t1, miss);
+        slab(c.oy + rr, sp.Dg[1], sp.invD[1], v.sy1 + 2.0f * rr, 0.0f, t0, t1, miss);
+        slab(c.oz + rr, sp.Dg[2], sp.invD[2], v.sz1 + 2.0f * rr, 0.0f, t0, t1, miss);
+        if (miss || !(t0 <= t1) || t1 < 0.0f) {
+            if (valid) {
+                out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
+                out_depth[o] = 0.0f;
+                if (DEBUG) {
+                    uint32_t* dbg = out_debug + o * 6;
+                    dbg[0] = dbg[1] = dbg[2] = dbg[3] = dbg[4] = dbg[5] = 0u;
+                }
+            }
+            return;   // uniform over the CTA
+        }
+    }
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(sp.occ);
+        const int n4 = sp.occ_words >> 2;
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) smask4[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    if (!COUNT && !valid) return;
+
     uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0;
     if (valid) {
         // ---- a2: ray (C3), jitter (C4)
         Ray r;
         float P[4];
+        float inv[3];
         const float fpx = (float)px, fpy = (float)py;
         if (PROJ == 0) {
             r.ox = __fmaf_rn(fpy, sp.Ey[0], __fmaf_rn(fpx, sp.Ex[0], sp.B[0]));
@@ -256,6 +301,9 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
             r.dx = sp.Dg[0];
             r.dy = sp.Dg[1];
             r.dz = sp.Dg[2];
+            inv[0] = sp.invD[0];
+            inv[1] = sp.invD[1];
+            inv[2] = sp.invD[2];
 #pragma unroll
             for (int l = 0; l < 4; ++l) P[l] = sp.P[l];
         } else {
@@ -263,14 +311,17 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
             const float d1 = __fmaf_rn(fpy, sp.Ey[1], __fmaf_rn(fpx, sp.Ex[1], sp.F0[1]));
             const float d2 = __fmaf_rn(fpy, sp.Ey[2], __fmaf_rn(fpx, sp.Ex[2], sp.F0[2]));
             const float q = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
-            const float inv = __fdiv_rn(1.0f, __fsqrt_rn(q));
-            const float dir0 = __fmul_rn(d0, inv), dir1 = __fmul_rn(d1, inv), dir2 = __fmul_rn(d2, inv);
+            const float iq = __fdiv_rn(1.0f, __fsqrt_rn(q));
+            const float dir0 = __fmul_rn(d0, iq), dir1 = __fmul_rn(d1, iq), dir2 = __fmul_rn(d2, iq);
             r.dx = __fmul_rn(dir0, sp.inv_dx);
             r.dy = __fmul_rn(dir1, sp.inv_dx);
             r.dz = __fmul_rn(dir2, sp.inv_dx);
             r.ox = sp.Oe[0];
             r.oy = sp.Oe[1];
             r.oz = sp.Oe[2];
+            inv[0] = r.dx != 0.0f ? 1.0f / r.dx : 0.0f;
+            inv[1] = r.dy != 0.0f ? 1.0f / r.dy : 0.0f;
+            inv[2] = r.dz != 0.0f ? 1.0f / r.dz : 0.0f;
 #pragma unroll
             for (int l = 0; l < 4; ++l)
                 P[l] = hg32(mc.g, sp.Ln[l][0] * dir0 + sp.Ln[l][1] * dir1 + sp.Ln[l][2] * dir2);
@@ -281,7 +332,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
 
         // ---- C5 clip
         int n_lo, n_hi;
-        clip_ray(r, v, mc.Ncap, n_lo, n_hi);
+        clip_ray(r, v, inv, 1.0f / mc.h, mc.Ncap, n_lo, n_hi);
 
         // ---- a4-a7 march
         float tau = 0.0f, T = 1.0f, Dout = 0.0f;
@@ -289,6 +340,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
         int n_hit = 0, n_term = n_hi > 0 ? n_hi : 0;
         uint32_t n_occ = 0, lsamp = 0;
         const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && n_lo >= 2;
+        const bool paired = sp.pair12 != 0;
         for (int n = n_lo; n <= n_hi; ++n) {
             float t, x, y, z;
             r.at(n, t, x, y, z);
@@ -309,18 +361,29 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
                 if (mc.form == NSL_OPACITY_EXP) A = mc.alpha * (Tp - T);
                 else if (mc.form == NSL_OPACITY_RIEMANN) A = mc.alpha * Tp * s;
                 else A = Tp * sig_s;
+                const float kl = mc.hl * mc.kappa;
+                if (paired) {                              // C8: top/bottom in one loop
+                    const int Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
+                    const int Mb = light_count(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2]);
+                    float sa, sb;
+                    light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, Ma, Mb, sa,
+                                                  sb, c_gath);
+                    S[1] = __fmaf_rn(A, __expf(-kl * sa), S[1]);
+                    S[2] = __fmaf_rn(A, __expf(-kl * sb), S[2]);
+                    lsamp += (uint32_t)(Ma + Mb);
+                }
 #pragma unroll
                 for (int l = 0; l < 4; ++l) {             // C8 + C10
-                    if (l < mc.n_lights) {
+                    if (l < mc.n_lights && !(paired && (l == 1 || l == 2))) {
                         float Tl;
                         const float lx = sp.Lg[l][0], ly = sp.Lg[l][1], lz = sp.Lg[l][2];
                         if (l == 0 && front_fast) {
                             Tl = Tp;                      // C9: T^front_n = T_{n-1}
-                            if (COUNT) lsamp += (uint32_t)light_count(v, x, y, z, lx, ly, lz, mc.hl);
+                            if (COUNT) lsamp += (uint32_t)light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
                         } else {
-                            const int M = light_count(v, x, y, z, lx, ly, lz, mc.hl);
+                            const int M = light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
                             const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, M, c_gath);
-                            Tl = __expf(-(mc.hl * mc.kappa) * sum);
+                            Tl = __expf(-kl * sum);
                             lsamp += (uint32_t)M;
                         }
                         S[l] = __fmaf_rn(A, Tl, S[l]);
@@ -343,7 +406,6 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
                 L2 += sp.rgb[l][2] * w;
             }
         }
-        const size_t o = (size_t)f * (size_t)W * (size_t)H + pix;
         out_rgbt[o] = make_float4(L0, L1, L2, T);
         out_depth[o] = Dout;
         const bool hit_support = n_lo > 0 && n_hi >= n_lo;
@@ -387,13 +449,13 @@ template <int LAYOUT, int PROJ, int MODE>
 cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, size_t smem, float4* rgbt,
                        float* depth, uint32_t* debug, unsigned long long* counters, cudaStream_t s) {
     const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
-    dim3 grid((unsigned)(tiles_x * tiles_y), (unsigned)F);
+    dim3 grid((unsigned)tiles_x, (unsigned)tiles_y, (unsigned)F);
     auto k = march_kernel<LAYOUT, PROJ, MODE>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k<<<grid, kThreads, smem, s>>>(fp, mc, rgbt, depth, debug, counters, W, H, tiles_x);
+    k<<<grid, kThreads, smem, s>>>(fp, mc, rgbt, depth, debug, counters, W, H);
     return cudaGetLastError();
 }
 

@@ -53,6 +53,13 @@ struct FrameParams {
     int32_t front_ok;          // C9 preconditions hold for this frame
     const uint32_t* occ;       // occupancy bitmask (global), staged to shared memory per CTA
     int32_t occ_shift, occ_nbx, occ_nby, occ_words;
+    // per-frame helpers for the conservative (estimate-only) computations:
+    float invD[3];             // ortho: 1/D_g per axis (0 where D_g = 0)
+    float lim[4][3];           // light march exit plane per axis (n+1, 0, or 3e38 if L = 0)
+    float ilh[4][3];           // 1 / (L_g * h_l) per axis (1 if L = 0)
+    float tile_r;              // ortho: half-diagonal of a 16x16 pixel tile in index units
+    int32_t pair12;            // guide set: light 2 == -light 1 bit-exactly (paired side march)
+    int32_t pad2[3];
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 

@@ -149,6 +149,28 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
     bool ok = mc.front_identity && mc.light_mode == NSL_LIGHTS_GUIDE && cam.projection == 0 && mc.hl == mc.h;
     for (int q = 0; q < 3; ++q) ok = ok && (p.Lg[0][q] == -p.Dg[q]);
     p.front_ok = ok ? 1 : 0;
+    // ---- estimate helpers (never decide an index on their own: every use is
+    //      followed by exact prescribed-op checks in march.cu)
+    for (int q = 0; q < 3; ++q) p.invD[q] = p.Dg[q] != 0.0f ? 1.0f / p.Dg[q] : 0.0f;
+    for (int l = 0; l < 4; ++l)
+        for (int q = 0; q < 3; ++q) {
+            const float L = p.Lg[l][q];
+            p.lim[l][q] = L > 0.0f ? p.supp[q] : (L < 0.0f ? 0.0f : 3.0e38f);
+            p.ilh[l][q] = L != 0.0f ? 1.0f / (L * mc.hl) : 1.0f;
+        }
+    {
+        // 16x16 tile: half extents 8|Ex| + 8|Ey| (index units), plus one pixel of slack
+        double rr = 0.0;
+        for (int q = 0; q < 3; ++q) {
+            const double e = 9.0 * (fabs((double)p.Ex[q]) + fabs((double)p.Ey[q]));
+            rr += e * e;
+        }
+        p.tile_r = (float)sqrt(rr) + 1.0f;
+    }
+    bool pair = mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3;
+    for (int q = 0; q < 3; ++q) pair = pair && (p.Lg[2][q] == -p.Lg[1][q]);
+    p.pair12 = pair ? 1 : 0;
+    p.pad2[0] = p.pad2[1] = p.pad2[2] = 0;
     out[fi] = p;
 }
 
