@@ -17,7 +17,7 @@ from typing import List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-LIB_PATH = os.path.join(_HERE, "lib", "libnsl.so")
+LIB_PATH = os.environ.get("NSL_LIB") or os.path.join(_HERE, "lib", "libnsl.so")   # NSL_LIB: build variants
 CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu")]
 HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_ROOT, "include", "nsl.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

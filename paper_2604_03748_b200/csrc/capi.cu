@@ -19,6 +19,7 @@ struct nsl_volume {
     unsigned long long* invalid;      // counter in the storage tail
     uint32_t* occ;                    // occupancy bitmask inside the storage
     nsl::OccGeom og;
+    int32_t* aabb;                    // occupied block bounds in the storage tail
 };
 
 namespace {
@@ -178,6 +179,7 @@ VolDesc desc_of(const nsl_volume* v) {
     d.dx = v->g.voxel_width;
     d.occ = v->occ;
     d.og = v->og;
+    d.aabb = v->aabb;
     return d;
 }
 
@@ -258,6 +260,7 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     v->invalid = reinterpret_cast<unsigned long long*>(static_cast<char*>(device_storage) + tail_offset(g, layout));
     v->occ = reinterpret_cast<uint32_t*>(static_cast<char*>(device_storage) + mask_offset(g, layout));
     v->og = occ_geom(g->nx, g->ny, g->nz);
+    v->aabb = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(v->invalid) + 16);
     auto bail = [&](nsl_status st) { delete v; return st; };
     cudaError_t e = cudaMemsetAsync(v->invalid, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemsetAsync"));
@@ -273,7 +276,7 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     }
     e = launch_layout(raw, desc_of(v), device_storage, v->invalid, s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "layout kernel launch"));
-    e = launch_occupancy(raw, desc_of(v), v->occ, s);
+    e = launch_occupancy(raw, desc_of(v), v->occ, v->aabb, s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "occupancy kernel launch"));
     if (staging) {
         e = cudaFreeAsync(staging, s);

@@ -23,6 +23,9 @@ namespace nsl {
 namespace {
 
 constexpr int kTileW = 16, kTileH = 16, kThreads = 256;
+#ifndef NSL_MINB
+#define NSL_MINB 1   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB))
+#endif
 constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
@@ -213,13 +216,20 @@ __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy,
     sb = b;
 }
 
+// Conservative count of leading light samples inside the occupied box (one
+// extra for rounding): samples beyond it are exactly 0 and need not be taken.
+__device__ __forceinline__ int box_count(float ux, float uy, float uz, const float alim[3], const float ilh[3]) {
+    const float m = fminf(fminf((alim[0] - ux) * ilh[0], (alim[1] - uy) * ilh[1]), (alim[2] - uz) * ilh[2]);
+    return (int)fminf(fmaxf(floorf(m), -1.0f), 16777215.0f) + 1;
+}
+
 __device__ __forceinline__ float hg32(float g, float c) {
     const float d = (1.0f + g * g) - 2.0f * g * c;
     return (1.0f - g * g) / (12.566370614359172f * d * sqrtf(d));
 }
 
 template <int LAYOUT, int PROJ, int MODE>
-__global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
+__global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H) {
@@ -330,9 +340,26 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
         const uint32_t pix = (uint32_t)py * (uint32_t)W + (uint32_t)px;
         r.delta = mc.jitter ? jitter_delta(jitter_hash(mc.seed_lo, mc.seed_hi, sp.frame_id, pix), mc.h) : 0.0f;
 
-        // ---- C5 clip
+        // ---- C5 clip (exact, for the bookkeeping), then the occupied-box sub-range
+        //      actually marched: outside the box every sample is exactly 0
         int n_lo, n_hi;
-        clip_ray(r, v, inv, 1.0f / mc.h, mc.Ncap, n_lo, n_hi);
+        const float inv_h = 1.0f / mc.h;
+        clip_ray(r, v, inv, inv_h, mc.Ncap, n_lo, n_hi);
+        int m_lo = n_lo, m_hi = n_hi;
+        {
+            float u0 = -3.0e38f, u1 = 3.0e38f;
+            bool miss = false;
+            slab(r.ox - sp.alo[0], r.dx, inv[0], sp.ahi[0] - sp.alo[0], 1e-3f, u0, u1, miss);
+            slab(r.oy - sp.alo[1], r.dy, inv[1], sp.ahi[1] - sp.alo[1], 1e-3f, u0, u1, miss);
+            slab(r.oz - sp.alo[2], r.dz, inv[2], sp.ahi[2] - sp.alo[2], 1e-3f, u0, u1, miss);
+            if (miss || !(u0 <= u1)) {
+                m_hi = m_lo - 1;
+            } else {
+                const float a = floorf((u0 - r.delta) * inv_h) - 1.0f, b = ceilf((u1 - r.delta) * inv_h) + 1.0f;
+                if (a > (float)m_lo) m_lo = a < (float)m_hi ? (int)a : m_hi + 1;
+                if (b < (float)m_hi) m_hi = b > (float)m_lo ? (int)b : m_lo - 1;
+            }
+        }
 
         // ---- a4-a7 march
         float tau = 0.0f, T = 1.0f, Dout = 0.0f;
@@ -341,7 +368,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
         uint32_t n_occ = 0, lsamp = 0;
         const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && n_lo >= 2;
         const bool paired = sp.pair12 != 0;
-        for (int n = n_lo; n <= n_hi; ++n) {
+        for (int n = m_lo; n <= m_hi; ++n) {
             float t, x, y, z;
             r.at(n, t, x, y, z);
             const float rho = sample<LAYOUT, COUNT>(v, x, y, z, c_gath);
@@ -366,7 +393,9 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
                     const int Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
                     const int Mb = light_count(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2]);
                     float sa, sb;
-                    light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, Ma, Mb, sa,
+                    const int ma = min(Ma, box_count(x, y, z, sp.alim[1], sp.ilh[1]));
+                    const int mb = min(Mb, box_count(x, y, z, sp.alim[2], sp.ilh[2]));
+                    light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, ma, mb, sa,
                                                   sb, c_gath);
                     S[1] = __fmaf_rn(A, __expf(-kl * sa), S[1]);
                     S[2] = __fmaf_rn(A, __expf(-kl * sb), S[2]);
@@ -382,7 +411,8 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const FrameParams* __re
                             if (COUNT) lsamp += (uint32_t)light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
                         } else {
                             const int M = light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
-                            const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, M, c_gath);
+                            const int mm = min(M, box_count(x, y, z, sp.alim[l], sp.ilh[l]));
+                            const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, mm, c_gath);
                             Tl = __expf(-kl * sum);
                             lsamp += (uint32_t)M;
                         }

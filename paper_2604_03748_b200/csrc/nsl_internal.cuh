@@ -27,6 +27,7 @@ struct VolDesc {
     float dx;
     const uint32_t* occ;
     OccGeom og;
+    const int32_t* aabb;       // occupied block bounds: bmin xyz, bmax xyz (bmin > bmax: empty volume)
 };
 
 // Raw per-frame input (host -> device, one memcpy per call).
@@ -59,7 +60,10 @@ struct FrameParams {
     float ilh[4][3];           // 1 / (L_g * h_l) per axis (1 if L = 0)
     float tile_r;              // ortho: half-diagonal of a 16x16 pixel tile in index units
     int32_t pair12;            // guide set: light 2 == -light 1 bit-exactly (paired side march)
-    int32_t pad2[3];
+    // occupied box [alo, ahi) in padded-index positions: every sample outside it is exactly 0
+    float alo[3], ahi[3];
+    float alim[4][3];          // light march exit plane of the occupied box per axis
+    int32_t pad2[1];
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 
@@ -82,7 +86,7 @@ constexpr int kCornerF16 = NSL_LAYOUT_CORNER_F16;
 // Launch helpers implemented in the .cu files.
 cudaError_t launch_layout(const float* raw, const VolDesc& v, void* storage, unsigned long long* invalid,
                           cudaStream_t s);
-cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, cudaStream_t s);
+cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, int32_t* aabb, cudaStream_t s);
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s);
 // mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path

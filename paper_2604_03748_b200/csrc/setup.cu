@@ -170,7 +170,31 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
     bool pair = mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3;
     for (int q = 0; q < 3; ++q) pair = pair && (p.Lg[2][q] == -p.Lg[1][q]);
     p.pair12 = pair ? 1 : 0;
-    p.pad2[0] = p.pad2[1] = p.pad2[2] = 0;
+    // occupied box in padded-index positions: cells [bmin*B, (bmax+1)*B) -> U in [lo, hi), clipped to the support
+    if (fr.vol.aabb) {
+        const int B = 1 << fr.vol.og.shift;
+        for (int q = 0; q < 3; ++q) {
+            const int bmin = fr.vol.aabb[q], bmax = fr.vol.aabb[3 + q];
+            if (bmin > bmax) {                      // empty volume: a point box
+                p.alo[q] = 0.0f;
+                p.ahi[q] = 0.0f;
+            } else {
+                p.alo[q] = (float)(bmin * B);
+                p.ahi[q] = fminf((float)((bmax + 1) * B), p.supp[q]);
+            }
+        }
+    } else {
+        for (int q = 0; q < 3; ++q) {
+            p.alo[q] = 0.0f;
+            p.ahi[q] = p.supp[q];
+        }
+    }
+    for (int l = 0; l < 4; ++l)
+        for (int q = 0; q < 3; ++q) {
+            const float L = p.Lg[l][q];
+            p.alim[l][q] = L > 0.0f ? p.ahi[q] : (L < 0.0f ? p.alo[q] : 3.0e38f);
+        }
+    p.pad2[0] = 0;
     out[fi] = p;
 }
 

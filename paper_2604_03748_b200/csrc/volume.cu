@@ -98,7 +98,7 @@ __global__ void layout_corner_f16_kernel(Raw r, uint4* __restrict__ out, unsigne
 
 // One thread per occupancy block: the block is non-empty iff some padded
 // voxel in [b*B, b*B + B]^3 (the corners of its cells) is nonzero.
-__global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g) {
+__global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g, int32_t* __restrict__ aabb) {
     const int B = 1 << g.shift;
     const int total = g.nbx * g.nby * g.nbz;
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < total; b += gridDim.x * blockDim.x) {
@@ -114,7 +114,15 @@ __global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g) 
                         any = true;
                         break;
                     }
-        if (any) atomicOr(mask + (b >> 5), 1u << (b & 31));
+        if (any) {
+            atomicOr(mask + (b >> 5), 1u << (b & 31));
+            atomicMin(aabb + 0, bx);
+            atomicMin(aabb + 1, by);
+            atomicMin(aabb + 2, bz);
+            atomicMax(aabb + 3, bx);
+            atomicMax(aabb + 4, by);
+            atomicMax(aabb + 5, bz);
+        }
     }
 }
 
@@ -142,12 +150,14 @@ OccGeom occ_geom(int nx, int ny, int nz) {
     return g;
 }
 
-cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, cudaStream_t s) {
+cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, int32_t* aabb, cudaStream_t s) {
     Raw r{raw, v.nx, v.ny, v.nz};
     cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)v.og.words * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(aabb, 0x7f, 3 * sizeof(int32_t), s);      // bmin = 0x7f7f7f7f
+    if (e == cudaSuccess) e = cudaMemsetAsync(aabb + 3, 0xff, 3 * sizeof(int32_t), s);  // bmax = -1
     if (e != cudaSuccess) return e;
     const int total = v.og.nbx * v.og.nby * v.og.nbz;
-    occupancy_kernel<<<(total + 127) / 128, 128, 0, s>>>(r, mask, v.og);
+    occupancy_kernel<<<(total + 127) / 128, 128, 0, s>>>(r, mask, v.og, aabb);
     return cudaGetLastError();
 }
 
