@@ -45,14 +45,27 @@ __device__ __forceinline__ bool inside(const Vol& v, float x, float y, float z) 
 // C1 trilinear at an in-support padded-index position (corners always exist
 // thanks to the apron).  floor and fraction are exact in fp32.  Samples in an
 // empty occupancy block return 0 without touching global memory.
+// floor on the FMA pipe: for 0 <= x < 2^22, x + 1.5*2^23 rounded toward -inf is
+// exactly floor(x) + 1.5*2^23 (unit spacing there), so the integer sits in the
+// low mantissa bits and r - 1.5*2^23 is floor(x) exactly.  No F2I/FRND (the
+// quarter-rate XU pipe) per sample.  Positions in support satisfy 0 < x < n+1.
+constexpr float kFloorBias = 12582912.0f;   // 1.5 * 2^23, bit pattern 0x4B400000
+__device__ __forceinline__ void cellof(float x, int& i, float& frac) {
+    const float r = __fadd_rd(x, kFloorBias);
+    i = __float_as_int(r) - 0x4B400000;
+    frac = __fsub_rn(x, __fsub_rn(r, kFloorBias));
+}
+
 template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
-    const float fx0 = floorf(x), fy0 = floorf(y), fz0 = floorf(z);
-    const int ix = (int)fx0, iy = (int)fy0, iz = (int)fz0;
+    int ix, iy, iz;
+    float fx, fy, fz;
+    cellof(x, ix, fx);
+    cellof(y, iy, fy);
+    cellof(z, iz, fz);
     const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
     if (!((v.mask[b >> 5] >> (b & 31)) & 1u)) return 0.0f;
     if (COUNT) ++gathers;
-    const float fx = __fsub_rn(x, fx0), fy = __fsub_rn(y, fy0), fz = __fsub_rn(z, fz0);
     const int e = ix + iy * v.sy + iz * v.sz;
     if (LAYOUT == kLinearF32) {
         const float* p = static_cast<const float*>(v.data) + e;
@@ -105,7 +118,10 @@ __device__ __forceinline__ float jitter_delta(uint32_t h32, float h) {
 struct Ray {
     float ox, oy, oz, dx, dy, dz, delta, h;
     __device__ __forceinline__ void at(int n, float& t, float& x, float& y, float& z) const {
-        t = __fmaf_rn((float)n, h, delta);
+        atf((float)n, t, x, y, z);
+    }
+    __device__ __forceinline__ void atf(float nf, float& t, float& x, float& y, float& z) const {
+        t = __fmaf_rn(nf, h, delta);
         x = __fmaf_rn(t, dx, ox);
         y = __fmaf_rn(t, dy, oy);
         z = __fmaf_rn(t, dz, oz);
@@ -184,13 +200,14 @@ __device__ __forceinline__ float light_sum(const Vol& v, float ux, float uy, flo
                                            float hl, int M, uint32_t& gathers) {
     float acc0 = 0.0f, acc1 = 0.0f;
     int j = 1;
-    for (; j + 1 <= M; j += 2) {
-        const float s0 = __fmul_rn((float)j, hl), s1 = __fmul_rn((float)(j + 1), hl);
+    float jf = 1.0f;   // exact float copy of j (j < 2^24): no I2F in the loop
+    for (; j + 1 <= M; j += 2, jf += 2.0f) {
+        const float s0 = __fmul_rn(jf, hl), s1 = __fmul_rn(jf + 1.0f, hl);
         acc0 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
         acc1 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s1, lx, ux), __fmaf_rn(s1, ly, uy), __fmaf_rn(s1, lz, uz), gathers);
     }
     if (j <= M) {
-        const float s0 = __fmul_rn((float)j, hl);
+        const float s0 = __fmul_rn(jf, hl);
         acc0 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
     }
     return acc0 + acc1;
@@ -206,14 +223,34 @@ __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy,
                                                uint32_t& gathers) {
     float a = 0.0f, b = 0.0f;
     const int M = max(Ma, Mb);
-    for (int j = 1; j <= M; ++j) {
-        const float s = __fmul_rn((float)j, hl);
+    float jf = 1.0f;
+    for (int j = 1; j <= M; ++j, jf += 1.0f) {
+        const float s = __fmul_rn(jf, hl);
         if (j <= Ma) a += sample<LAYOUT, COUNT>(v, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), __fmaf_rn(s, lz, uz), gathers);
         if (j <= Mb)
             b += sample<LAYOUT, COUNT>(v, __fmaf_rn(-s, lx, ux), __fmaf_rn(-s, ly, uy), __fmaf_rn(-s, lz, uz), gathers);
     }
     sa = a;
     sb = b;
+}
+
+// Fast-path bound on the light samples that can be nonzero: the estimate of the
+// support count plus one (>= the exact count), capped by the occupied-box
+// count, then shrunk with exact prescribed-op tests until the last sample is in
+// support (so every index is valid).  Every in-support sample inside the
+// occupied box is covered, hence the sum equals the canonical one (C8).
+__device__ __forceinline__ int light_bound(const Vol& v, float ux, float uy, float uz, float lx, float ly, float lz,
+                                           float hl, const float lim[3], const float ilh[3], const float alim[3]) {
+    const float ms = fminf(fminf((lim[0] - ux) * ilh[0], (lim[1] - uy) * ilh[1]), (lim[2] - uz) * ilh[2]);
+    const float mb = fminf(fminf((alim[0] - ux) * ilh[0], (alim[1] - uy) * ilh[1]), (alim[2] - uz) * ilh[2]);
+    float m = fminf(floorf(ms), floorf(mb)) + 1.0f;
+    m = fminf(fmaxf(m, 0.0f), 16777216.0f);
+    while (m > 0.0f) {
+        const float s = __fmul_rn(m, hl);
+        if (inside(v, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), __fmaf_rn(s, lz, uz))) break;
+        m -= 1.0f;
+    }
+    return (int)m;
 }
 
 // Conservative count of leading light samples inside the occupied box (one
@@ -368,9 +405,10 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
         uint32_t n_occ = 0, lsamp = 0;
         const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && n_lo >= 2;
         const bool paired = sp.pair12 != 0;
-        for (int n = m_lo; n <= m_hi; ++n) {
+        float nf = (float)m_lo;
+        for (int n = m_lo; n <= m_hi; ++n, nf += 1.0f) {
             float t, x, y, z;
-            r.at(n, t, x, y, z);
+            r.atf(nf, t, x, y, z);
             const float rho = sample<LAYOUT, COUNT>(v, x, y, z, c_gath);
             if (rho > 0.0f) {
                 ++n_occ;
@@ -390,11 +428,20 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
                 else A = Tp * sig_s;
                 const float kl = mc.hl * mc.kappa;
                 if (paired) {                              // C8: top/bottom in one loop
-                    const int Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
-                    const int Mb = light_count(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2]);
+                    int Ma, Mb, ma, mb;
+                    if (DEBUG || COUNT) {
+                        Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
+                        Mb = light_count(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2]);
+                        ma = min(Ma, box_count(x, y, z, sp.alim[1], sp.ilh[1]));
+                        mb = min(Mb, box_count(x, y, z, sp.alim[2], sp.ilh[2]));
+                    } else {
+                        Ma = Mb = 0;
+                        ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1],
+                                         sp.alim[1]);
+                        mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2],
+                                         sp.alim[2]);
+                    }
                     float sa, sb;
-                    const int ma = min(Ma, box_count(x, y, z, sp.alim[1], sp.ilh[1]));
-                    const int mb = min(Mb, box_count(x, y, z, sp.alim[2], sp.ilh[2]));
                     light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, ma, mb, sa,
                                                   sb, c_gath);
                     S[1] = __fmaf_rn(A, __expf(-kl * sa), S[1]);
@@ -410,8 +457,14 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
                             Tl = Tp;                      // C9: T^front_n = T_{n-1}
                             if (COUNT) lsamp += (uint32_t)light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
                         } else {
-                            const int M = light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
-                            const int mm = min(M, box_count(x, y, z, sp.alim[l], sp.ilh[l]));
+                            int M, mm;
+                            if (DEBUG || COUNT) {
+                                M = light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
+                                mm = min(M, box_count(x, y, z, sp.alim[l], sp.ilh[l]));
+                            } else {
+                                M = 0;
+                                mm = light_bound(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l], sp.alim[l]);
+                            }
                             const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, mm, c_gath);
                             Tl = __expf(-kl * sum);
                             lsamp += (uint32_t)M;
