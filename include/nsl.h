@@ -171,12 +171,15 @@ nsl_status nsl_guiding_map_batch(const nsl_volume* const* vols, int32_t n_vols, 
 
 /* The same launch as nsl_guiding_map_batch (identical results, the timed
  * fast path), instrumented: it also accumulates into `counters` (device,
- * 4 x u64, zeroed by the call on `stream`):
+ * 8 x u64, zeroed by the call on `stream`):
  *   [0] primary samples processed  = sum over pixels of (n_term - n_lo + 1)
  *   [1] light samples (canonical)  = sum over pixels of light_samples (C12)
  *   [2] trilinear gathers executed (samples in non-empty occupancy blocks that
  *       the kernel actually loaded; the C9 front march is not executed)
  *   [3] occupied primary samples   = sum of n_occ
+ *   [4] primary samples tested (occupied-box sub-range actually walked)
+ *   [5] light samples tested (occupied-box-clipped marches actually walked)
+ *   [6], [7] reserved (0)
  * [0]+[1] is the canonical march-sample count of DESIGN.md §7. */
 nsl_status nsl_guiding_map_batch_counted(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
                                          const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,

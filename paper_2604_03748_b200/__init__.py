@@ -255,7 +255,7 @@ def guiding_map_batch_counted(vols, frame_vol, cams, lights, light_mode, medium,
     sample counts, trilinear gathers actually executed and occupied samples."""
     import torch
     F = len(cams)
-    counters = torch.zeros(4, dtype=torch.int64, device="cuda")
+    counters = torch.zeros(8, dtype=torch.int64, device="cuda")
     hv = (ctypes.c_void_p * len(vols))(*[v.handle.value for v in vols])
     fv = (ctypes.c_int32 * F)(*frame_vol)
     cs = (CameraS * F)(*[camera_s(c) for c in cams])
@@ -266,7 +266,7 @@ def guiding_map_batch_counted(vols, frame_vol, cams, lights, light_mode, medium,
                                                _stream_handle(stream)), "nsl_guiding_map_batch_counted")
     c = counters.cpu().tolist()
     return {"primary_samples": c[0], "light_samples": c[1], "gathers": c[2], "occupied_samples": c[3],
-            "canonical_samples": c[0] + c[1]}
+            "tested_primary": c[4], "tested_light": c[5], "canonical_samples": c[0] + c[1]}
 
 
 def guiding_map_host(grid, host_density, layout, cams, lights, light_mode, medium, march, frame_ids,

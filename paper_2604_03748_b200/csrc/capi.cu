@@ -365,7 +365,7 @@ nsl_status nsl_guiding_map_batch_counted(const nsl_volume* const* vols, int32_t 
         g_err = "counters is NULL";
         return NSL_ERR_INVALID_ARG;
     }
-    NSL_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint64_t), reinterpret_cast<cudaStream_t>(stream)),
+    NSL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint64_t), reinterpret_cast<cudaStream_t>(stream)),
              "cudaMemsetAsync(counters)");
     return batch_impl(vols, n_vols, frame_vol, cams, lights, n_lights, light_mode, med, m, frame_ids, F, out_rgbt,
                       out_depth, nullptr, reinterpret_cast<unsigned long long*>(counters), stream);

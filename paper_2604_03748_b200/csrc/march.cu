@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
     __syncthreads();
     if (!COUNT && !valid) return;
 
-    uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0;
+    uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0, c_tp = 0, c_tl = 0;
     if (valid) {
         // ---- a2: ray (C3), jitter (C4)
         Ray r;
@@ -409,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
         for (int n = m_lo; n <= m_hi; ++n, nf += 1.0f) {
             float t, x, y, z;
             r.atf(nf, t, x, y, z);
+            if (COUNT) ++c_tp;
             const float rho = sample<LAYOUT, COUNT>(v, x, y, z, c_gath);
             if (rho > 0.0f) {
                 ++n_occ;
@@ -441,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
                         mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2],
                                          sp.alim[2]);
                     }
+                    if (COUNT) c_tl += (uint32_t)(ma + mb);
                     float sa, sb;
                     light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, ma, mb, sa,
                                                   sb, c_gath);
@@ -465,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
                                 M = 0;
                                 mm = light_bound(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l], sp.alim[l]);
                             }
+                            if (COUNT) c_tl += (uint32_t)mm;
                             const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, mm, c_gath);
                             Tl = __expf(-kl * sum);
                             lsamp += (uint32_t)M;
@@ -508,15 +511,17 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
         }
     }
     if (COUNT) {
-        __shared__ unsigned int red[4];
-        if (threadIdx.x < 4) red[threadIdx.x] = 0;
+        __shared__ unsigned int red[6];
+        if (threadIdx.x < 6) red[threadIdx.x] = 0;
         __syncthreads();
         atomicAdd(&red[0], c_prim);
         atomicAdd(&red[1], c_light);
         atomicAdd(&red[2], c_gath);
         atomicAdd(&red[3], c_occ);
+        atomicAdd(&red[4], c_tp);
+        atomicAdd(&red[5], c_tl);
         __syncthreads();
-        if (threadIdx.x < 4) atomicAdd(counters + threadIdx.x, (unsigned long long)red[threadIdx.x]);
+        if (threadIdx.x < 6) atomicAdd(counters + threadIdx.x, (unsigned long long)red[threadIdx.x]);
     }
 }
 
