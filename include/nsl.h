@@ -188,6 +188,28 @@ nsl_status nsl_guiding_map_batch_counted(const nsl_volume* const* vols, int32_t 
                                          float* out_rgbt, float* out_depth, uint64_t* counters,
                                          nsl_stream stream);
 
+/* Plans: the same batch, prepared once.  nsl_plan_create validates and
+ * marshals the per-frame inputs (cameras, lights, frame ids, volume
+ * references) exactly as nsl_guiding_map_batch does and uploads them into
+ * plan-owned device memory (cudaMalloc; the upload is enqueued on `stream`).
+ * nsl_plan_execute then enqueues only device work — the per-frame setup
+ * kernel (rows a2/a3) and the march kernel (rows a4-a8) — with no host
+ * marshalling and no host<->device copy, so it is cheap to call every frame
+ * and capturable in a CUDA graph.  Results are identical to the batch call.
+ * The referenced volumes' device storage must stay valid (re-uploading a
+ * volume into the same storage between executions is allowed: the plan keeps
+ * the storage pointers, not the host handles).  out_debug / counters as in
+ * nsl_guiding_map_batch / _counted (at most one of them non-NULL).
+ * nsl_plan_destroy frees the plan's device memory (synchronising the device). */
+typedef struct nsl_plan nsl_plan;
+nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                           const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
+                           int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                           const uint32_t* frame_ids, int32_t F, nsl_stream stream, nsl_plan** out);
+nsl_status nsl_plan_execute(const nsl_plan* plan, float* out_rgbt, float* out_depth, uint32_t* out_debug,
+                            uint64_t* counters, nsl_stream stream);
+nsl_status nsl_plan_destroy(nsl_plan* plan);
+
 /* End-to-end convenience call with HOST buffers: uploads the host density
  * grid, lays it out, marches the F frames and copies the results back into
  * host out_rgbt (F*H*W*4 floats) / out_depth (F*H*W floats); synchronises

@@ -79,6 +79,7 @@ class FrameConstantsS(ctypes.Structure):
 
 EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_upload", "nsl_volume_check",
            "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_batch_counted",
+           "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter"]
 
 _lib = None
@@ -109,6 +110,10 @@ def lib():
                                         P(MarchS), P(u32), i32, vp, vp, vp, vp]
     L.nsl_guiding_map_batch_counted.argtypes = [P(vp), i32, P(i32), P(CameraS), P(LightS), i32, i32, P(MediumS),
                                                 P(MarchS), P(u32), i32, vp, vp, vp, vp]
+    L.nsl_plan_create.argtypes = [P(vp), i32, P(i32), P(CameraS), P(LightS), i32, i32, P(MediumS), P(MarchS),
+                                  P(u32), i32, vp, P(vp)]
+    L.nsl_plan_execute.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.nsl_plan_destroy.argtypes = [vp]
     L.nsl_guiding_map_host.argtypes = [P(GridDesc), vp, i32, P(CameraS), P(LightS), i32, i32, P(MediumS),
                                        P(MarchS), P(u32), i32, vp, vp, vp]
     L.nsl_debug_frame_constants.argtypes = [P(GridDesc), P(CameraS), P(LightS), i32, i32, P(MediumS),
@@ -267,6 +272,52 @@ def guiding_map_batch_counted(vols, frame_vol, cams, lights, light_mode, medium,
     c = counters.cpu().tolist()
     return {"primary_samples": c[0], "light_samples": c[1], "gathers": c[2], "occupied_samples": c[3],
             "tested_primary": c[4], "tested_light": c[5], "canonical_samples": c[0] + c[1]}
+
+
+class Plan:
+    """A prepared batch (nsl_plan_*): per-frame inputs marshalled and uploaded once;
+    execute() enqueues only the setup and march kernels (no host work per call)."""
+
+    def __init__(self, vols, frame_vol, cams, lights, light_mode, medium, march, frame_ids, stream=None):
+        F = len(cams)
+        self.F, self.H, self.W = F, cams[0].height, cams[0].width
+        hv = (ctypes.c_void_p * len(vols))(*[v.handle.value for v in vols])
+        fv = (ctypes.c_int32 * F)(*frame_vol)
+        cs = (CameraS * F)(*[camera_s(c) for c in cams])
+        fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+        h = ctypes.c_void_p()
+        _check(lib().nsl_plan_create(hv, len(vols), fv, cs, lights_s(lights), len(lights[0]), light_mode,
+                                     ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)), fid, F,
+                                     _stream_handle(stream), ctypes.byref(h)), "nsl_plan_create")
+        self.handle = h
+
+    def execute(self, out_rgbt, out_depth, out_debug=None, counters=None, stream=None):
+        _check(lib().nsl_plan_execute(self.handle, _ptr(out_rgbt), _ptr(out_depth), _ptr(out_debug), _ptr(counters),
+                                      _stream_handle(stream)), "nsl_plan_execute")
+
+    def execute_counted(self, out_rgbt, out_depth, stream=None) -> dict:
+        import torch
+        c = torch.zeros(8, dtype=torch.int64, device="cuda")
+        self.execute(out_rgbt, out_depth, None, c, stream)
+        c = c.cpu().tolist()
+        return {"primary_samples": c[0], "light_samples": c[1], "gathers": c[2], "occupied_samples": c[3],
+                "tested_primary": c[4], "tested_light": c[5], "canonical_samples": c[0] + c[1]}
+
+    def destroy(self):
+        if getattr(self, "handle", None) is not None and _lib is not None:
+            _lib.nsl_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def make_plan(w, vols, march=None, stream=None) -> Plan:
+    return Plan(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, march or w.march, w.frame_ids,
+                stream=stream)
 
 
 def guiding_map_host(grid, host_density, layout, cams, lights, light_mode, medium, march, frame_ids,

@@ -302,46 +302,73 @@ nsl_status nsl_volume_release(nsl_volume* v) {
     return NSL_OK;
 }
 
+// Validated, marshalled form of a batch call (host side only).
+struct Prepared {
+    std::vector<FrameIn> frames;
+    MarchConst mc;
+    int F = 0, W = 0, H = 0, proj = 0, layout = 0, max_words = 0, n_lights = 0;
+};
+
+static nsl_status prepare(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                          const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                          const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                          Prepared& P) {
+    if (F < 1 || F > 65535) return fail(NSL_ERR_INVALID_ARG, "F must be in [1, 65535]");
+    if (!vols || n_vols < 1 || !frame_vol || !cams || !frame_ids)
+        return fail(NSL_ERR_INVALID_ARG, "NULL vols/frame_vol/cams/frame_ids");
+    if (nsl_status st = check_common(lights, n_lights, light_mode, med, m)) return st;
+    for (int i = 0; i < n_vols; ++i)
+        if (!vols[i]) return fail(NSL_ERR_INVALID_ARG, "vols[%d] is NULL", i);
+    P.layout = vols[0]->layout;
+    P.max_words = 0;
+    for (int i = 0; i < n_vols; ++i) {
+        if (vols[i]->layout != P.layout) return fail(NSL_ERR_UNSUPPORTED, "all volumes of a batch must share a layout");
+        P.max_words = vols[i]->og.words > P.max_words ? vols[i]->og.words : P.max_words;
+    }
+    P.W = cams[0].width;
+    P.H = cams[0].height;
+    P.proj = cams[0].projection;
+    P.F = F;
+    P.n_lights = n_lights;
+    P.frames.assign((size_t)F, FrameIn{});
+    for (int f = 0; f < F; ++f) {
+        if (nsl_status st = check_camera(&cams[f], f)) return st;
+        if (cams[f].width != P.W || cams[f].height != P.H)
+            return fail(NSL_ERR_INVALID_ARG, "camera[%d]: size differs", f);
+        if (cams[f].projection != P.proj) return fail(NSL_ERR_UNSUPPORTED, "camera[%d]: mixed projections", f);
+        if (frame_vol[f] < 0 || frame_vol[f] >= n_vols) return fail(NSL_ERR_INVALID_ARG, "frame_vol[%d] out of range", f);
+        if (nsl_status st = check_lights(lights + (size_t)f * n_lights, n_lights, light_mode, f)) return st;
+        FrameIn& fi = P.frames[f];
+        memset(&fi, 0, sizeof fi);
+        fi.cam = cams[f];
+        fi.vol = desc_of(vols[frame_vol[f]]);
+        fi.frame_id = frame_ids[f];
+    }
+    P.mc = make_const(n_lights, light_mode, med, m);
+    return NSL_OK;
+}
+
+static nsl_status check_outputs(const float* out_rgbt, const float* out_depth) {
+    if (!out_rgbt || !out_depth) return fail(NSL_ERR_INVALID_ARG, "NULL output");
+    if (reinterpret_cast<uintptr_t>(out_rgbt) % 16) return fail(NSL_ERR_INVALID_ARG, "out_rgbt must be 16-B aligned");
+    return NSL_OK;
+}
+
 static nsl_status batch_impl(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
                              const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
                              const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
                              float* out_rgbt, float* out_depth, uint32_t* out_debug, unsigned long long* counters,
                              nsl_stream stream) {
     g_err.clear();
-    if (F < 1 || F > 65535) return fail(NSL_ERR_INVALID_ARG, "F must be in [1, 65535]");
-    if (!vols || n_vols < 1 || !frame_vol || !cams || !frame_ids)
-        return fail(NSL_ERR_INVALID_ARG, "NULL vols/frame_vol/cams/frame_ids");
-    if (!out_rgbt || !out_depth) return fail(NSL_ERR_INVALID_ARG, "NULL output");
-    if (reinterpret_cast<uintptr_t>(out_rgbt) % 16) return fail(NSL_ERR_INVALID_ARG, "out_rgbt must be 16-B aligned");
-    if (nsl_status st = check_common(lights, n_lights, light_mode, med, m)) return st;
-    for (int i = 0; i < n_vols; ++i)
-        if (!vols[i]) return fail(NSL_ERR_INVALID_ARG, "vols[%d] is NULL", i);
-    const int layout = vols[0]->layout;
-    int max_words = 0;
-    for (int i = 0; i < n_vols; ++i) {
-        if (vols[i]->layout != layout) return fail(NSL_ERR_UNSUPPORTED, "all volumes of a batch must share a layout");
-        max_words = vols[i]->og.words > max_words ? vols[i]->og.words : max_words;
-    }
-    const int W = cams[0].width, H = cams[0].height, proj = cams[0].projection;
-    std::vector<FrameIn> frames((size_t)F);
-    for (int f = 0; f < F; ++f) {
-        if (nsl_status st = check_camera(&cams[f], f)) return st;
-        if (cams[f].width != W || cams[f].height != H) return fail(NSL_ERR_INVALID_ARG, "camera[%d]: size differs", f);
-        if (cams[f].projection != proj) return fail(NSL_ERR_UNSUPPORTED, "camera[%d]: mixed projections", f);
-        if (frame_vol[f] < 0 || frame_vol[f] >= n_vols) return fail(NSL_ERR_INVALID_ARG, "frame_vol[%d] out of range", f);
-        if (nsl_status st = check_lights(lights + (size_t)f * n_lights, n_lights, light_mode, f)) return st;
-        FrameIn& fi = frames[f];
-        memset(&fi, 0, sizeof fi);
-        fi.cam = cams[f];
-        fi.vol = desc_of(vols[frame_vol[f]]);
-        fi.frame_id = frame_ids[f];
-    }
-    const MarchConst mc = make_const(n_lights, light_mode, med, m);
+    if (nsl_status st = check_outputs(out_rgbt, out_depth)) return st;
+    Prepared P;
+    if (nsl_status st = prepare(vols, n_vols, frame_vol, cams, lights, n_lights, light_mode, med, m, frame_ids, F, P))
+        return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
-    if (nsl_status st = build_frames(frames, lights, n_lights, mc, s, ws)) return st;
-    cudaError_t e = launch_march(ws.params, mc, F, W, H, proj, layout, max_words, reinterpret_cast<float4*>(out_rgbt),
-                                 out_depth, out_debug, counters, s);
+    if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, s, ws)) return st;
+    cudaError_t e = launch_march(ws.params, P.mc, P.F, P.W, P.H, P.proj, P.layout, P.max_words,
+                                 reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug, counters, s);
     cudaError_t e2 = cudaFreeAsync(ws.base, s);
     if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
     if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(frame tables)");
@@ -424,6 +451,74 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     if (st != NSL_OK) return st;
     NSL_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return NSL_OK;
+}
+
+struct nsl_plan {
+    Prepared P;                 // frames vector cleared after upload
+    void* dev = nullptr;        // FrameIn[F] | lights[F*nl] | FrameParams[F]
+    FrameIn* in = nullptr;
+    nsl_light* lights = nullptr;
+    FrameParams* params = nullptr;
+};
+
+nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                           const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                           const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                           nsl_stream stream, nsl_plan** out) {
+    g_err.clear();
+    if (!out) return fail(NSL_ERR_INVALID_ARG, "NULL out");
+    nsl_plan* p = new nsl_plan;
+    if (nsl_status st = prepare(vols, n_vols, frame_vol, cams, lights, n_lights, light_mode, med, m, frame_ids, F, p->P)) {
+        delete p;
+        return st;
+    }
+    const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
+    const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
+    const size_t b_p = sizeof(FrameParams) * F;
+    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_p);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "cudaMalloc(plan)");
+    }
+    p->in = reinterpret_cast<FrameIn*>(p->dev);
+    p->lights = reinterpret_cast<nsl_light*>(static_cast<char*>(p->dev) + b_in);
+    p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l);
+    std::vector<char> host(b_in + b_l);
+    memcpy(host.data(), p->P.frames.data(), sizeof(FrameIn) * F);
+    memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
+    e = cudaMemcpyAsync(p->dev, host.data(), host.size(), cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+        cudaFree(p->dev);
+        delete p;
+        return cuda_fail(e, "plan upload");
+    }
+    p->P.frames.clear();
+    p->P.frames.shrink_to_fit();
+    *out = p;
+    return NSL_OK;
+}
+
+nsl_status nsl_plan_execute(const nsl_plan* p, float* out_rgbt, float* out_depth, uint32_t* out_debug,
+                            uint64_t* counters, nsl_stream stream) {
+    g_err.clear();
+    if (!p) return fail(NSL_ERR_INVALID_ARG, "NULL plan");
+    if (nsl_status st = check_outputs(out_rgbt, out_depth)) return st;
+    if (out_debug && counters) return fail(NSL_ERR_INVALID_ARG, "debug and counters are exclusive");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (counters) NSL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint64_t), s), "cudaMemsetAsync(counters)");
+    NSL_CUDA(launch_frame_setup(p->in, p->lights, p->P.F, p->P.mc, p->params, s), "frame_setup_kernel launch");
+    NSL_CUDA(launch_march(p->params, p->P.mc, p->P.F, p->P.W, p->P.H, p->P.proj, p->P.layout, p->P.max_words,
+                          reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug,
+                          reinterpret_cast<unsigned long long*>(counters), s),
+             "march_kernel launch");
+    return NSL_OK;
+}
+
+nsl_status nsl_plan_destroy(nsl_plan* p) {
+    if (!p) return NSL_OK;
+    cudaError_t e = cudaFree(p->dev);
+    delete p;
+    return e == cudaSuccess ? NSL_OK : cuda_fail(e, "cudaFree(plan)");
 }
 
 nsl_status nsl_debug_frame_constants(const nsl_grid_desc* g, const nsl_camera* cam, const nsl_light* lights,

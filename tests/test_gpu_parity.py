@@ -293,3 +293,28 @@ def test_random_tiny_cases(nsl):
         w = _case(grid, vals, cam, lights, mode, med, m, frame_id=int(rng.integers(0, 1000)))
         g, gd, gdbg = run(nsl, w)
         compare_frame(w, 0, g[0], gd[0], gdbg[0])
+
+
+def test_plan_equals_batch_and_counts(nsl):
+    import torch
+    w = I.make_workload("C2", frames=[0, 9, 33])
+    ref = run(nsl, w, debug=False)
+    vols = nsl.upload_workload_volumes(w)
+    plan = nsl.make_plan(w, vols)
+    outs = nsl.alloc_outputs(w.n_frames, w.height, w.width, debug=True)
+    for _ in range(2):
+        plan.execute(outs[0], outs[1])
+        torch.cuda.synchronize()
+        assert np.array_equal(outs[0].cpu().numpy(), ref[0])
+        assert np.array_equal(outs[1].cpu().numpy(), ref[1])
+    # counters: canonical counts equal the debug counters' sums (= the oracle's, by parity)
+    c = plan.execute_counted(outs[0], outs[1])
+    assert np.array_equal(outs[0].cpu().numpy(), ref[0])
+    plan.execute(outs[0], outs[1], outs[2])
+    torch.cuda.synchronize()
+    d = outs[2].cpu().numpy().reshape(-1, 6).astype(np.int64)
+    prim = np.where(d[:, 0] > 0, d[:, 3] - d[:, 0] + 1, 0).sum()
+    assert c["primary_samples"] == prim
+    assert c["light_samples"] == d[:, 5].sum()
+    assert c["occupied_samples"] == d[:, 4].sum()
+    assert 0 < c["gathers"] <= c["tested_primary"] + c["tested_light"] <= c["canonical_samples"]
