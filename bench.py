@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
     p.add_argument("--layout", default="quad_f32", choices=["linear_f32", "quad_f32", "corner_f16"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--gather", action="store_true",
+                   help="N>1: after the timed loop, time the NCCL gather of all guiding maps to rank 0")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     return p.parse_args()
@@ -266,18 +268,40 @@ def main():
     value = total_rays / t_loop
     ms_step = 1e3 * t_loop / K
 
-    # roofline of the dominant kernel (march_kernel): executed trilinear gathers x 32 B (fp32) or 16 B (fp16)
+    # roofline of the dominant kernel (march_kernel).  ncu shows it issue/ALU-bound
+    # (no memory unit near its peak), so bound = "alu": algorithmic work = SURVEY §8(d)'s 25
+    # FP32/INT ops per canonical march sample x the canonical samples of one launch; peak =
+    # 148 SMs x 128 FP32/INT32 lanes x max SM clock.  The L1 view (32 B per canonical sample
+    # through L1/TEX vs 148 x 128 B/clk) and the gathers actually executed are reported beside it.
     peaks = load_peaks()
-    bytes_per_sample = 16 if layout == 2 else 32
     march_s = statistics.mean(march_ms) / 1e3
-    achieved = counts["gathers"] * bytes_per_sample / march_s / 1e9
     sm_mhz = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
-    l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e9          # GB/s: 148 SMs x 128 B/clk L1 x max SM clock
-    roof = {"bound": "l1tex", "achieved": achieved, "peak": l1_peak, "unit": "GB/s", "frac": achieved / l1_peak,
-            "traffic": None,
-            "peak_source": "derived: 148 SMs x 128 B/clk (B300_MICROARCH L1 line/cycle) x sm_max_mhz",
-            "kernel": "march_kernel", "kernel_ms": march_s * 1e3,
-            "algorithmic_bytes_per_launch": counts["gathers"] * bytes_per_sample,
+    ops = 25 * counts["canonical_samples"]
+    achieved = ops / march_s / 1e9
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9          # Gop/s
+    bytes_per_sample = 16 if layout == 2 else 32
+    l1_achieved = counts["canonical_samples"] * 32 / march_s / 1e9
+    l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e9           # GB/s
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_march_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("config") == cfg and tj.get("layout") == args.layout and tj.get("frames") == F:
+                traffic = tj["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak,
+            "traffic": traffic,
+            "peak_source": "derived: 148 SMs x 128 FP32/INT32 lanes x sm_max_mhz (B200_PROFILING.md unit counts)",
+            "per_unit": "25 ops per canonical march sample (SURVEY 8(d))",
+            "kernel": "march_kernel (+ frame_setup_kernel, same launch sequence)", "kernel_ms": march_s * 1e3,
+            "algorithmic_ops_per_launch": ops,
+            "l1tex_view": {"achieved_gbs": l1_achieved, "peak_gbs": l1_peak, "frac": l1_achieved / l1_peak,
+                           "per_unit": "32 B (8 fp32 corners) per canonical sample"},
+            "executed_gathers_per_launch": counts["gathers"],
+            "executed_gather_gbs": counts["gathers"] * bytes_per_sample / march_s / 1e9,
+            "algorithmic_output_bytes_per_launch": 20 * W * H * F,
             "hbm_peak_gbs": peaks.get("hbm_gbs")}
 
     line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -291,6 +315,22 @@ def main():
             "ms_per_frame": ms_step / F, "frames_per_s": F * world * K / t_loop,
             "march_ms_per_step": statistics.mean(march_ms), "layout_ms_per_step": statistics.mean(layout_ms),
             "counts_per_rank_step": counts, "gpu_launches": 4 * K, "clocks": clk, "roofline": roof}
+
+    # optional result gather to rank 0 (the only collective of the design; not in the timed step)
+    if world > 1 and args.gather:
+        from paper_2604_03748_b200 import sharding
+        rgbt_local = outputs[0]
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        full = sharding.gather_frames(rgbt_local, F * world)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        tg = torch.tensor([g0.elapsed_time(g1)], device="cuda")
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        line["gather"] = {"ms": float(tg.item()), "bytes_to_rank0": int(rgbt_local.numel() * 4 * (world - 1)),
+                          "what": "rgbt float4 maps of all ranks -> rank 0 (torch.distributed.gather, NCCL)"}
+        del full
 
     # end-to-end through the public host API: pinned host density in, pinned host guiding maps out
     if not args.no_e2e:

@@ -24,7 +24,8 @@ namespace {
 
 constexpr int kTileW = 16, kTileH = 16, kThreads = 256;
 #ifndef NSL_MINB
-#define NSL_MINB 1   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB))
+#define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
+                     // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)
 #endif
 constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 

@@ -129,10 +129,10 @@ __global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g, 
 }  // namespace
 
 // Occupancy block size: the smallest 2^shift (shift >= 1) whose bitmask fits
-// the per-CTA shared-memory budget (default 40 KB; NSL_OCC_BUDGET / NSL_OCC_SHIFT
+// the per-CTA shared-memory budget (default 16 KB; NSL_OCC_BUDGET / NSL_OCC_SHIFT
 // override for experiments).
 OccGeom occ_geom(int nx, int ny, int nz) {
-    long budget = 40 * 1024;
+    long budget = 16 * 1024;   // ~33 blocks per axis; measured best on C2 (profiles/r1_sweep.txt)
     if (const char* e = getenv("NSL_OCC_BUDGET")) budget = atol(e);
     int forced = 0;
     if (const char* e = getenv("NSL_OCC_SHIFT")) forced = atoi(e);
