@@ -4,7 +4,9 @@
 One *step* = one pass of the whole hot path over one batch: the volume
 layout (row a1, from the device-resident raw grid) plus the batched march of
 all frames of BASELINE.json configs[1] (C2: chimney plume 128^3, 60 frames of
-512x512, rotating camera, guide lights), rows a2-a9, in 3 kernel launches.
+512x512, rotating camera, guide lights), rows a2-a9: 4 kernel launches per
+step (layout, occupancy, frame setup, march) from device-resident inputs via a
+prepared plan (nsl_plan_execute).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
 
@@ -125,9 +127,10 @@ def load_peaks():
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def time_oracle(cfg, seconds, max_frames=None):
-    """The oracle, as it stands (single-threaded C), on whole frames of the workload until
-    ~`seconds` of CPU work; returns rays/s, samples/s and the sample description."""
+def time_oracle(cfg, seconds, max_frames=None, stride=1):
+    """The oracle, as it stands (single-threaded C), on frames of the workload (every
+    `stride`-th pixel) until ~`seconds` of CPU work or `max_frames` frames; returns
+    rays/s, samples/s and the sample description."""
     import oracle
     import nsl_inputs as I
     w = I.make_workload(cfg, frames=[0])
@@ -139,10 +142,8 @@ def time_oracle(cfg, seconds, max_frames=None):
     f = 0
     while (len(frames) < max_frames) if max_frames is not None else (t_total < seconds or not frames):
         wf = I.make_workload(cfg, frames=[f % n_cfg])
-        if cfg in ("C4", "C5"):
-            pix = np.arange(0, wf.width * wf.height, 16 if cfg == "C4" else 64)
-        else:
-            pix = None
+        sub = stride * (16 if cfg == "C4" else 64 if cfg == "C5" else 1)
+        pix = np.arange(0, wf.width * wf.height, sub) if sub > 1 else None
         wf.volume(0)                        # generation is not oracle work
         t0 = time.perf_counter()
         r = oracle.run_workload_frame(wf, 0, pixels=pix)
@@ -154,7 +155,7 @@ def time_oracle(cfg, seconds, max_frames=None):
         frames.append(f % n_cfg)
         f += stride
     desc = (f"oracle (plain C, fp64, 1 thread) on {len(frames)} frame(s) {frames[:6]}{'...' if len(frames) > 6 else ''}"
-            f" of {cfg}" + (" (pixel subsample)" if cfg in ("C4", "C5") else " (all pixels)"))
+            f" of {cfg}" + (f" (every {sub}th pixel)" if sub > 1 else " (all pixels)"))
     return {"rays_per_s": rays / t_total, "samples_per_s": samples / t_total, "seconds": t_total,
             "sample": desc, "rays": rays}
 
@@ -174,9 +175,12 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = args.config
+    # each step = one frame of the workload, pixel-subsampled so that the whole
+    # (K + W)-step run stays within ~90 s of single-core oracle work
+    stride = max(1, math.ceil((args.steps + args.warmup) * 0.25 / 90.0))
     for _ in range(args.warmup):
-        time_oracle(cfg, 0.0, max_frames=1)
-    res = time_oracle(cfg, 0.0, max_frames=max(1, args.steps))
+        time_oracle(cfg, 0.0, max_frames=1, stride=stride)
+    res = time_oracle(cfg, 0.0, max_frames=max(1, args.steps), stride=stride)
     v = res["rays_per_s"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "rays/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * res["seconds"] / max(1, args.steps),

@@ -21,7 +21,8 @@ w = I.make_workload(a.config, frames=list(range(a.frames)) if a.frames else None
 layout = nsl.LAYOUTS[a.layout]
 vols = nsl.upload_workload_volumes(w, layout)
 outs = nsl.alloc_outputs(w.n_frames, w.height, w.width)
+plan = nsl.make_plan(w, vols)
 for _ in range(2 + a.launches):
-    nsl.run_workload(w, layout=layout, vols=vols, outputs=outs)
+    plan.execute(outs[0], outs[1])
 torch.cuda.synchronize()
 print("ok", w.name, w.n_frames, a.layout)
