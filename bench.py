@@ -138,7 +138,7 @@ def time_oracle(cfg, seconds, max_frames=None, stride=1):
     rays = samples = 0
     t_total = 0.0
     frames = []
-    stride = 4
+    fstride = 4                             # frames 0, 4, 8, ... of the camera path
     f = 0
     while (len(frames) < max_frames) if max_frames is not None else (t_total < seconds or not frames):
         wf = I.make_workload(cfg, frames=[f % n_cfg])
@@ -153,7 +153,7 @@ def time_oracle(cfg, seconds, max_frames=None, stride=1):
         rays += len(r["pixels"])
         t_total += dt
         frames.append(f % n_cfg)
-        f += stride
+        f += fstride
     desc = (f"oracle (plain C, fp64, 1 thread) on {len(frames)} frame(s) {frames[:6]}{'...' if len(frames) > 6 else ''}"
             f" of {cfg}" + (f" (every {sub}th pixel)" if sub > 1 else " (all pixels)"))
     return {"rays_per_s": rays / t_total, "samples_per_s": samples / t_total, "seconds": t_total,
