@@ -31,11 +31,16 @@ constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
     const void* __restrict__ data;
-    const uint32_t* mask;  // shared memory
     int sy, sz;
-    int shift, nbx, nby;
-    float sx1, sy1, sz1;   // support upper bounds n+1
+    float inv_b, nbx_f, nbxy_f;   // 2^-shift, blocks per x row, blocks per z slab (exact in fp32)
+    float sx1, sy1, sz1;          // support upper bounds n+1
 };
+
+// Dynamic shared memory of march_kernel: [FrameParams | occupancy mask words].
+// Indexed through this file-scope array so the mask test is one LDS with an
+// immediate offset (no generic->shared address conversion in the loops).
+extern __shared__ __align__(16) uint32_t nsl_smem[];
+constexpr int kMaskWord0 = (int)(sizeof(FrameParams) / 4);
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return __fmaf_rn(t, b - a, a); }
 
@@ -59,14 +64,20 @@ __device__ __forceinline__ void cellof(float x, int& i, float& frac) {
 
 template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
+    // occupancy block index in exact fp32: floor(x / B) via fma rounded toward -inf
+    // onto the 1.5*2^23 grid (x * 2^-s is exact), then the linear index with two
+    // exact FMAs (every term is an integer < 2^24); the bias stays in the x term.
+    const float bx = __fmaf_rd(x, v.inv_b, kFloorBias);
+    const float by = __fsub_rn(__fmaf_rd(y, v.inv_b, kFloorBias), kFloorBias);
+    const float bz = __fsub_rn(__fmaf_rd(z, v.inv_b, kFloorBias), kFloorBias);
+    const int b = __float_as_int(__fmaf_rn(bz, v.nbxy_f, __fmaf_rn(by, v.nbx_f, bx))) - 0x4B400000;
+    if (!((nsl_smem[kMaskWord0 + (b >> 5)] >> (b & 31)) & 1u)) return 0.0f;
+    if (COUNT) ++gathers;
     int ix, iy, iz;
     float fx, fy, fz;
     cellof(x, ix, fx);
     cellof(y, iy, fy);
     cellof(z, iz, fz);
-    const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
-    if (!((v.mask[b >> 5] >> (b & 31)) & 1u)) return 0.0f;
-    if (COUNT) ++gathers;
     const int e = ix + iy * v.sy + iz * v.sz;
     if (LAYOUT == kLinearF32) {
         const float* p = static_cast<const float*>(v.data) + e;
@@ -272,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
-    extern __shared__ __align__(16) uint4 smem[];
+    uint4* smem = reinterpret_cast<uint4*>(nsl_smem);
     FrameParams& sp = *reinterpret_cast<FrameParams*>(smem);
     uint4* smask4 = smem + sizeof(FrameParams) / 16;
     const int f = blockIdx.z;
@@ -289,12 +300,11 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
 
     Vol v;
     v.data = sp.data;
-    v.mask = reinterpret_cast<const uint32_t*>(smask4);
     v.sy = sp.sy;
     v.sz = sp.sz;
-    v.shift = sp.occ_shift;
-    v.nbx = sp.occ_nbx;
-    v.nby = sp.occ_nby;
+    v.inv_b = __int_as_float((127 - sp.occ_shift) << 23);   // 2^-shift exactly
+    v.nbx_f = (float)sp.occ_nbx;
+    v.nbxy_f = (float)(sp.occ_nbx * sp.occ_nby);
     v.sx1 = sp.supp[0];
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];

@@ -134,6 +134,7 @@ __global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g, 
 OccGeom occ_geom(int nx, int ny, int nz) {
     long budget = 16 * 1024;   // ~33 blocks per axis; measured best on C2 (profiles/r1_sweep.txt)
     if (const char* e = getenv("NSL_OCC_BUDGET")) budget = atol(e);
+    if (budget > 16 * 1024) budget = 16 * 1024;   // <= 2^17 blocks: the march's fp32 block index stays exact
     int forced = 0;
     if (const char* e = getenv("NSL_OCC_SHIFT")) forced = atoi(e);
     OccGeom g{};
@@ -145,7 +146,9 @@ OccGeom occ_geom(int nx, int ny, int nz) {
         g.nbz = (nz + 1 + B - 1) / B;
         const long bits = (long)g.nbx * g.nby * g.nbz;
         g.words = (int)(((bits + 31) / 32 + 3) / 4 * 4);
-        if (forced > 0 || (long)g.words * 4 <= budget) break;
+        if ((forced > 0 && s >= forced) || (long)g.words * 4 <= budget) {
+            if ((long)g.words * 4 <= 16 * 1024) break;
+        }
     }
     return g;
 }
