@@ -319,12 +319,22 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
         c.ox = fmaf(cy, sp.Ey[0], fmaf(cx, sp.Ex[0], sp.B[0]));
         c.oy = fmaf(cy, sp.Ey[1], fmaf(cx, sp.Ex[1], sp.B[1]));
         c.oz = fmaf(cy, sp.Ey[2], fmaf(cx, sp.Ex[2], sp.B[2]));
+        // FAST mode culls against the occupied box (every sample outside it is 0, and
+        // FAST writes no counters); DEBUG/COUNTED need the support box for n_lo/n_hi.
         float t0 = -3.0e38f, t1 = 3.0e38f;
         bool miss = false;
         const float rr = sp.tile_r;
-        slab(c.ox + rr, sp.Dg[0], sp.invD[0], v.sx1 + 2.0f * rr, 0.0f, t0, t1, miss);
-        slab(c.oy + rr, sp.Dg[1], sp.invD[1], v.sy1 + 2.0f * rr, 0.0f, t0, t1, miss);
-        slab(c.oz + rr, sp.Dg[2], sp.invD[2], v.sz1 + 2.0f * rr, 0.0f, t0, t1, miss);
+        float lo[3] = {0.0f, 0.0f, 0.0f}, hi[3] = {v.sx1, v.sy1, v.sz1};
+        if (!DEBUG && !COUNT) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                lo[q] = sp.alo[q];
+                hi[q] = sp.ahi[q];
+            }
+        }
+        slab(c.ox - lo[0] + rr, sp.Dg[0], sp.invD[0], hi[0] - lo[0] + 2.0f * rr, 0.0f, t0, t1, miss);
+        slab(c.oy - lo[1] + rr, sp.Dg[1], sp.invD[1], hi[1] - lo[1] + 2.0f * rr, 0.0f, t0, t1, miss);
+        slab(c.oz - lo[2] + rr, sp.Dg[2], sp.invD[2], hi[2] - lo[2] + 2.0f * rr, 0.0f, t0, t1, miss);
         if (miss || !(t0 <= t1) || t1 < 0.0f) {
             if (valid) {
                 out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
@@ -388,12 +398,16 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
         const uint32_t pix = (uint32_t)py * (uint32_t)W + (uint32_t)px;
         r.delta = mc.jitter ? jitter_delta(jitter_hash(mc.seed_lo, mc.seed_hi, sp.frame_id, pix), mc.h) : 0.0f;
 
-        // ---- C5 clip (exact, for the bookkeeping), then the occupied-box sub-range
-        //      actually marched: outside the box every sample is exactly 0
-        int n_lo, n_hi;
+        // ---- C5: the steps actually marched are the in-support steps of [1, N] whose
+        //      positions lie in the occupied box (every other sample is exactly 0).
+        //      FAST: bracket the box's step range (float slab test, +-1 step) and make
+        //      its two ends exact with prescribed-op support tests (the in-support set
+        //      is contiguous, so the whole range is then in support).  DEBUG/COUNTED
+        //      also need the exact support range n_lo..n_hi for the bookkeeping.
+        int n_lo = 0, n_hi = -1;
         const float inv_h = 1.0f / mc.h;
-        clip_ray(r, v, inv, inv_h, mc.Ncap, n_lo, n_hi);
-        int m_lo = n_lo, m_hi = n_hi;
+        if (DEBUG || COUNT) clip_ray(r, v, inv, inv_h, mc.Ncap, n_lo, n_hi);
+        int m_lo, m_hi;
         {
             float u0 = -3.0e38f, u1 = 3.0e38f;
             bool miss = false;
@@ -401,11 +415,26 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
             slab(r.oy - sp.alo[1], r.dy, inv[1], sp.ahi[1] - sp.alo[1], 1e-3f, u0, u1, miss);
             slab(r.oz - sp.alo[2], r.dz, inv[2], sp.ahi[2] - sp.alo[2], 1e-3f, u0, u1, miss);
             if (miss || !(u0 <= u1)) {
-                m_hi = m_lo - 1;
-            } else {
+                m_lo = 1;
+                m_hi = 0;
+            } else if (DEBUG || COUNT) {
+                m_lo = n_lo;
+                m_hi = n_hi;
                 const float a = floorf((u0 - r.delta) * inv_h) - 1.0f, b = ceilf((u1 - r.delta) * inv_h) + 1.0f;
                 if (a > (float)m_lo) m_lo = a < (float)m_hi ? (int)a : m_hi + 1;
                 if (b < (float)m_hi) m_hi = b > (float)m_lo ? (int)b : m_lo - 1;
+            } else {
+                const float a = fmaxf(floorf((u0 - r.delta) * inv_h) - 1.0f, 1.0f);
+                const float b = fminf(ceilf((u1 - r.delta) * inv_h) + 1.0f, (float)mc.Ncap);
+                if (a <= b) {
+                    m_lo = (int)a;
+                    m_hi = (int)b;
+                    while (m_lo <= m_hi && !r.in(v, m_lo)) ++m_lo;
+                    while (m_hi >= m_lo && !r.in(v, m_hi)) --m_hi;
+                } else {
+                    m_lo = 1;
+                    m_hi = 0;
+                }
             }
         }
 
@@ -414,7 +443,8 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
         float S[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         int n_hit = 0, n_term = n_hi > 0 ? n_hi : 0;
         uint32_t n_occ = 0, lsamp = 0;
-        const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && n_lo >= 2;
+        // C9 precondition per ray: step 1 lies outside the support (i.e. n_lo >= 2)
+        const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && m_lo <= m_hi && !r.in(v, 1);
         const bool paired = sp.pair12 != 0;
         float nf = (float)m_lo;
         for (int n = m_lo; n <= m_hi; ++n, nf += 1.0f) {
