@@ -31,6 +31,7 @@ constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
     const void* __restrict__ data;
+    uint32_t mask_sa;             // shared-space byte address of the occupancy mask
     int sy, sz;
     float inv_b, nbx_f, nbxy_f;   // 2^-shift, blocks per x row, blocks per z slab (exact in fp32)
     float sx1, sy1, sz1;          // support upper bounds n+1
@@ -71,7 +72,9 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
     const float by = __fsub_rn(__fmaf_rd(y, v.inv_b, kFloorBias), kFloorBias);
     const float bz = __fsub_rn(__fmaf_rd(z, v.inv_b, kFloorBias), kFloorBias);
     const int b = __float_as_int(__fmaf_rn(bz, v.nbxy_f, __fmaf_rn(by, v.nbx_f, bx))) - 0x4B400000;
-    if (!((nsl_smem[kMaskWord0 + (b >> 5)] >> (b & 31)) & 1u)) return 0.0f;
+    uint32_t word;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(v.mask_sa + ((uint32_t)b >> 5) * 4u));
+    if (!((word >> (b & 31)) & 1u)) return 0.0f;
     if (COUNT) ++gathers;
     int ix, iy, iz;
     float fx, fy, fz;
@@ -90,9 +93,9 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
     } else if (LAYOUT == kQuadF32) {
         const float4* p = static_cast<const float4*>(v.data) + e;
-        const float4 q0 = __ldg(p), q1 = __ldg(p + v.sz);
-        const float x00 = lerpf(q0.x, q0.y, fx), x10 = lerpf(q0.z, q0.w, fx);
-        const float x01 = lerpf(q1.x, q1.y, fx), x11 = lerpf(q1.z, q1.w, fx);
+        const float4 q0 = __ldg(p), q1 = __ldg(p + v.sz);     // (c0, c1 - c0, c2, c3 - c2)
+        const float x00 = __fmaf_rn(fx, q0.y, q0.x), x10 = __fmaf_rn(fx, q0.w, q0.z);
+        const float x01 = __fmaf_rn(fx, q1.y, q1.x), x11 = __fmaf_rn(fx, q1.w, q1.z);
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
     } else {
         const uint4 u = __ldg(static_cast<const uint4*>(v.data) + e);
@@ -302,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
     v.data = sp.data;
     v.sy = sp.sy;
     v.sz = sp.sz;
+    v.mask_sa = (uint32_t)__cvta_generic_to_shared(smask4);
     v.inv_b = __int_as_float((127 - sp.occ_shift) << 23);   // 2^-shift exactly
     v.nbx_f = (float)sp.occ_nbx;
     v.nbxy_f = (float)(sp.occ_nbx * sp.occ_nby);

@@ -65,13 +65,13 @@ __global__ void layout_quad_kernel(Raw r, float4* __restrict__ out, unsigned lon
         int i = (int)(e % qx);
         size_t rest = e / qx;
         int j = (int)(rest % qy), k = (int)(rest / qy);
-        float4 q;
-        q.x = r.at(i, j, k);
-        q.y = r.at(i + 1, j, k);
-        q.z = r.at(i, j + 1, k);
-        q.w = r.at(i + 1, j + 1, k);
-        if (i >= 1 && j >= 1 && k >= 1 && k <= r.nz) check(q.x, invalid);
-        out[e] = q;
+        // (c000, c100 - c000, c010, c110 - c010): the x-lerps of the march become one
+        // FMA each, fma(fx, c100 - c000, c000), with the difference rounded exactly as
+        // the kernel's own lerp would round it (bit-identical to the LINEAR layout)
+        const float c000 = r.at(i, j, k), c100 = r.at(i + 1, j, k);
+        const float c010 = r.at(i, j + 1, k), c110 = r.at(i + 1, j + 1, k);
+        if (i >= 1 && j >= 1 && k >= 1 && k <= r.nz) check(c000, invalid);
+        out[e] = make_float4(c000, __fsub_rn(c100, c000), c010, __fsub_rn(c110, c010));
     }
 }
 
