@@ -23,6 +23,12 @@ namespace nsl {
 namespace {
 
 constexpr int kTileW = 16, kTileH = 16, kThreads = 256;
+#ifndef NSL_BLOCKIDX
+#define NSL_BLOCKIDX 1   // occupancy block index: 1 exact fp32 FMAs, 0 integer shifts of the cell floor
+#endif
+#ifndef NSL_MASKREAD
+#define NSL_MASKREAD 1   // mask word read: 1 ld.shared via a 32-bit address, 0 extern shared array
+#endif
 #ifndef NSL_MINB
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
                      // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)
@@ -34,6 +40,7 @@ struct Vol {
     uint32_t mask_sa;             // shared-space byte address of the occupancy mask
     int sy, sz;
     float inv_b, nbx_f, nbxy_f;   // 2^-shift, blocks per x row, blocks per z slab (exact in fp32)
+    int shift, nbx, nby;
     float sx1, sy1, sz1;          // support upper bounds n+1
 };
 
@@ -65,6 +72,7 @@ __device__ __forceinline__ void cellof(float x, int& i, float& frac) {
 
 template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
+#if NSL_BLOCKIDX == 1
     // occupancy block index in exact fp32: floor(x / B) via fma rounded toward -inf
     // onto the 1.5*2^23 grid (x * 2^-s is exact), then the linear index with two
     // exact FMAs (every term is an integer < 2^24); the bias stays in the x term.
@@ -72,15 +80,31 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
     const float by = __fsub_rn(__fmaf_rd(y, v.inv_b, kFloorBias), kFloorBias);
     const float bz = __fsub_rn(__fmaf_rd(z, v.inv_b, kFloorBias), kFloorBias);
     const int b = __float_as_int(__fmaf_rn(bz, v.nbxy_f, __fmaf_rn(by, v.nbx_f, bx))) - 0x4B400000;
+#else
+    // cell floors (shared with the gather below), block = cell >> shift
+    const float rx = __fadd_rd(x, kFloorBias), ry = __fadd_rd(y, kFloorBias), rz = __fadd_rd(z, kFloorBias);
+    const int ix = __float_as_int(rx) - 0x4B400000, iy = __float_as_int(ry) - 0x4B400000,
+              iz = __float_as_int(rz) - 0x4B400000;
+    const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
+#endif
+#if NSL_MASKREAD == 1
     uint32_t word;
     asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(v.mask_sa + ((uint32_t)b >> 5) * 4u));
+#else
+    const uint32_t word = nsl_smem[kMaskWord0 + (b >> 5)];
+#endif
     if (!((word >> (b & 31)) & 1u)) return 0.0f;
     if (COUNT) ++gathers;
+#if NSL_BLOCKIDX == 1
     int ix, iy, iz;
     float fx, fy, fz;
     cellof(x, ix, fx);
     cellof(y, iy, fy);
     cellof(z, iz, fz);
+#else
+    const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias)),
+                fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
+#endif
     const int e = ix + iy * v.sy + iz * v.sz;
     if (LAYOUT == kLinearF32) {
         const float* p = static_cast<const float*>(v.data) + e;
@@ -309,6 +333,9 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
     v.inv_b = __int_as_float((127 - sp.occ_shift) << 23);   // 2^-shift exactly
     v.nbx_f = (float)sp.occ_nbx;
     v.nbxy_f = (float)(sp.occ_nbx * sp.occ_nby);
+    v.shift = sp.occ_shift;
+    v.nbx = sp.occ_nbx;
+    v.nby = sp.occ_nby;
     v.sx1 = sp.supp[0];
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];

@@ -1,8 +1,9 @@
 # compile-time variants of libnsl for the perf sweep (NSL_LIB selects one at run time)
 set -e
 cd "$(dirname "$0")/.."
-for mb in 1 4 5 6; do
+for mb in ${MBS:-5}; do for bi in 0 1; do for mr in 0 1; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -cudart static \
-       -DNSL_MINB=$mb -o /tmp/libnsl_mb$mb.so paper_2604_03748_b200/csrc/*.cu &
-done
+       -DNSL_MINB=$mb -DNSL_BLOCKIDX=$bi -DNSL_MASKREAD=$mr -o /tmp/libnsl_mb${mb}_b${bi}_m${mr}.so \
+       paper_2604_03748_b200/csrc/*.cu 2>/dev/null &
+done; done; done
 wait
