@@ -24,10 +24,10 @@ namespace {
 
 constexpr int kTileW = 16, kTileH = 16, kThreads = 256;
 #ifndef NSL_BLOCKIDX
-#define NSL_BLOCKIDX 1   // occupancy block index: 1 exact fp32 FMAs, 0 integer shifts of the cell floor
+#define NSL_BLOCKIDX 0   // occupancy block index: 1 exact fp32 FMAs, 0 integer shifts of the cell floor (measured equal, profiles/r1_sweep.txt)
 #endif
 #ifndef NSL_MASKREAD
-#define NSL_MASKREAD 1   // mask word read: 1 ld.shared via a 32-bit address, 0 extern shared array
+#define NSL_MASKREAD 0   // mask word read: 1 ld.shared via a 32-bit address, 0 extern shared array
 #endif
 #ifndef NSL_MINB
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
