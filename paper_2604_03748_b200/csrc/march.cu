@@ -64,11 +64,13 @@ __device__ __forceinline__ bool inside(const Vol& v, float x, float y, float z) 
 // low mantissa bits and r - 1.5*2^23 is floor(x) exactly.  No F2I/FRND (the
 // quarter-rate XU pipe) per sample.  Positions in support satisfy 0 < x < n+1.
 constexpr float kFloorBias = 12582912.0f;   // 1.5 * 2^23, bit pattern 0x4B400000
+#if NSL_BLOCKIDX == 1
 __device__ __forceinline__ void cellof(float x, int& i, float& frac) {
     const float r = __fadd_rd(x, kFloorBias);
     i = __float_as_int(r) - 0x4B400000;
     frac = __fsub_rn(x, __fsub_rn(r, kFloorBias));
 }
+#endif
 
 template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
