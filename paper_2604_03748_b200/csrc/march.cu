@@ -29,6 +29,9 @@ constexpr int kTileW = 16, kTileH = 16, kThreads = 256;
 #ifndef NSL_MASKREAD
 #define NSL_MASKREAD 0   // mask word read: 1 ld.shared via a 32-bit address, 0 extern shared array
 #endif
+#ifndef NSL_PAIRWALK
+#define NSL_PAIRWALK 1   // paired top/bottom march: 1 combined chord walk, 0 lock-step both sides
+#endif
 #ifndef NSL_MINB
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
                      // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)
@@ -262,6 +265,31 @@ template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy, float uz, float lx, float ly,
                                                float lz, float hl, int Ma, int Mb, float& sa, float& sb,
                                                uint32_t& gathers) {
+#if NSL_PAIRWALK == 1
+    // Walk the combined chord k = 0 .. Ma+Mb-1 (j = k+1 on the +L side, then j = k-Ma+1
+    // on the -L side) two samples per iteration: no lane idles on the shorter side.
+    // jf carries the sign of the side, so s = jf*h_l = +-fl(j*h_l) exactly.
+    float a = 0.0f, b = 0.0f;
+    const int K = Ma + Mb;
+    const float maf = (float)Ma;
+    float kf = 0.0f;
+    int k = 0;
+    for (; k + 1 < K; k += 2, kf += 2.0f) {
+        const float j0 = kf < maf ? kf + 1.0f : maf - kf - 1.0f;
+        const float j1 = kf + 1.0f < maf ? kf + 2.0f : maf - kf - 2.0f;
+        const float s0 = __fmul_rn(j0, hl), s1 = __fmul_rn(j1, hl);
+        const float r0 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
+        const float r1 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s1, lx, ux), __fmaf_rn(s1, ly, uy), __fmaf_rn(s1, lz, uz), gathers);
+        if (j0 > 0.0f) a += r0; else b += r0;
+        if (j1 > 0.0f) a += r1; else b += r1;
+    }
+    if (k < K) {
+        const float j0 = kf < maf ? kf + 1.0f : maf - kf - 1.0f;
+        const float s0 = __fmul_rn(j0, hl);
+        const float r0 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
+        if (j0 > 0.0f) a += r0; else b += r0;
+    }
+#else
     float a = 0.0f, b = 0.0f;
     const int M = max(Ma, Mb);
     float jf = 1.0f;
@@ -271,6 +299,7 @@ __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy,
         if (j <= Mb)
             b += sample<LAYOUT, COUNT>(v, __fmaf_rn(-s, lx, ux), __fmaf_rn(-s, ly, uy), __fmaf_rn(-s, lz, uz), gathers);
     }
+#endif
     sa = a;
     sb = b;
 }
