@@ -63,7 +63,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // storage = [layout body | occupancy mask | tail counter], each 256-B aligned
 size_t mask_offset(const nsl_grid_desc* g, int layout) { return align_up(body_bytes(g, layout), 256); }
 size_t tail_offset(const nsl_grid_desc* g, int layout) {
-    return mask_offset(g, layout) + align_up((size_t)occ_geom(g->nx, g->ny, g->nz).words * 4, 256);
+    return mask_offset(g, layout) + align_up((size_t)occ_geom(g->nx, g->ny, g->nz).words_total * 4, 256);
 }
 
 nsl_status check_grid(const nsl_grid_desc* g) {
@@ -323,7 +323,7 @@ static nsl_status prepare(const nsl_volume* const* vols, int32_t n_vols, const i
     P.max_words = 0;
     for (int i = 0; i < n_vols; ++i) {
         if (vols[i]->layout != P.layout) return fail(NSL_ERR_UNSUPPORTED, "all volumes of a batch must share a layout");
-        P.max_words = vols[i]->og.words > P.max_words ? vols[i]->og.words : P.max_words;
+        P.max_words = vols[i]->og.words_total > P.max_words ? vols[i]->og.words_total : P.max_words;
     }
     P.W = cams[0].width;
     P.H = cams[0].height;

@@ -330,6 +330,31 @@ __device__ __forceinline__ int box_count(float ux, float uy, float uz, const flo
     return (int)fminf(fmaxf(floorf(m), -1.0f), 16777215.0f) + 1;
 }
 
+// Exit planes of the region that can hold nonzero samples of light l's march from
+// height uz: for a horizontal light (L_z == 0 exactly, so every Y_j,z == uz and the
+// march stays in the z block-slab of uz) the slab's 2-D box of non-empty blocks;
+// otherwise the occupied 3-D box.  Either way samples beyond it are exactly 0.
+__device__ __forceinline__ void march_region(const FrameParams& sp, const Vol& v, int l, float uz, float out[3]) {
+    if ((sp.lz0 >> l) & 1) {
+        const int iz = __float_as_int(__fadd_rd(uz, kFloorBias)) - 0x4B400000;
+        const int bz = iz >> v.shift;
+        const int* slab = reinterpret_cast<const int*>(nsl_smem) + kMaskWord0 + sp.slab_off;
+        const int2 mn = *reinterpret_cast<const int2*>(slab + 2 * bz);
+        const int2 mx = *reinterpret_cast<const int2*>(slab + 2 * sp.occ_nbz + 2 * bz);
+        const float B = (float)(1 << v.shift);
+        const float lox = (float)mn.x * B, hix = fminf((float)(mx.x + 1) * B, v.sx1);
+        const float loy = (float)mn.y * B, hiy = fminf((float)(mx.y + 1) * B, v.sy1);
+        const float Lx = sp.Lg[l][0], Ly = sp.Lg[l][1];
+        out[0] = Lx > 0.0f ? hix : (Lx < 0.0f ? lox : 3.0e38f);
+        out[1] = Ly > 0.0f ? hiy : (Ly < 0.0f ? loy : 3.0e38f);
+        out[2] = 3.0e38f;
+    } else {
+        out[0] = sp.alim[l][0];
+        out[1] = sp.alim[l][1];
+        out[2] = sp.alim[l][2];
+    }
+}
+
 __device__ __forceinline__ float hg32(float g, float c) {
     const float d = (1.0f + g * g) - 2.0f * g * c;
     return (1.0f - g * g) / (12.566370614359172f * d * sqrtf(d));
@@ -536,14 +561,18 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
                     if (DEBUG || COUNT) {
                         Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
                         Mb = light_count(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2]);
-                        ma = min(Ma, box_count(x, y, z, sp.alim[1], sp.ilh[1]));
-                        mb = min(Mb, box_count(x, y, z, sp.alim[2], sp.ilh[2]));
+                        float ra[3], rb[3];
+                        march_region(sp, v, 1, z, ra);
+                        march_region(sp, v, 2, z, rb);
+                        ma = min(Ma, box_count(x, y, z, ra, sp.ilh[1]));
+                        mb = min(Mb, box_count(x, y, z, rb, sp.ilh[2]));
                     } else {
                         Ma = Mb = 0;
-                        ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1],
-                                         sp.alim[1]);
-                        mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2],
-                                         sp.alim[2]);
+                        float ra[3], rb[3];
+                        march_region(sp, v, 1, z, ra);
+                        march_region(sp, v, 2, z, rb);
+                        ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1], ra);
+                        mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2], rb);
                     }
                     if (COUNT) c_tl += (uint32_t)(ma + mb);
                     float sa, sb;
@@ -565,10 +594,14 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
                             int M, mm;
                             if (DEBUG || COUNT) {
                                 M = light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
-                                mm = min(M, box_count(x, y, z, sp.alim[l], sp.ilh[l]));
+                                float rl[3];
+                                march_region(sp, v, l, z, rl);
+                                mm = min(M, box_count(x, y, z, rl, sp.ilh[l]));
                             } else {
                                 M = 0;
-                                mm = light_bound(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l], sp.alim[l]);
+                                float rl[3];
+                                march_region(sp, v, l, z, rl);
+                                mm = light_bound(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l], rl);
                             }
                             if (COUNT) c_tl += (uint32_t)mm;
                             const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, mm, c_gath);

@@ -16,7 +16,11 @@ namespace nsl {
 struct OccGeom {
     int32_t shift, nbx, nby, nbz;
     int32_t words;             // ceil(nbx*nby*nbz / 32), padded to a multiple of 4
+    int32_t words_total;       // mask + per-slab boxes: words + 4*nbz (a multiple of 4)
 };
+// Occupancy region (device, staged to shared memory by the march):
+//   [mask: words u32][slab_min: nbz x (bx, by) int32][slab_max: nbz x (bx, by) int32]
+// slab box of z-block slab bz = the x/y range of its non-empty blocks (min > max: empty).
 OccGeom occ_geom(int nx, int ny, int nz);
 
 // Per-volume description handed to the frame-setup kernel.
@@ -53,7 +57,8 @@ struct FrameParams {
     uint32_t frame_id;
     int32_t front_ok;          // C9 preconditions hold for this frame
     const uint32_t* occ;       // occupancy bitmask (global), staged to shared memory per CTA
-    int32_t occ_shift, occ_nbx, occ_nby, occ_words;
+    int32_t occ_shift, occ_nbx, occ_nby, occ_words;   // occ_words: mask + slab boxes (staged)
+    int32_t occ_nbz;
     // per-frame helpers for the conservative (estimate-only) computations:
     float invD[3];             // ortho: 1/D_g per axis (0 where D_g = 0)
     float lim[4][3];           // light march exit plane per axis (n+1, 0, or 3e38 if L = 0)
@@ -63,7 +68,9 @@ struct FrameParams {
     // occupied box [alo, ahi) in padded-index positions: every sample outside it is exactly 0
     float alo[3], ahi[3];
     float alim[4][3];          // light march exit plane of the occupied box per axis
-    int32_t pad2[1];
+    int32_t slab_off;          // word offset of the slab boxes in the staged occupancy region
+    int32_t lz0;               // bit l: L_g,l,z == 0 exactly (the march of light l stays in its z slab)
+    int32_t pad2[2];
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 

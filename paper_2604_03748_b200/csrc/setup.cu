@@ -67,7 +67,9 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
     p.occ_shift = fr.vol.og.shift;
     p.occ_nbx = fr.vol.og.nbx;
     p.occ_nby = fr.vol.og.nby;
-    p.occ_words = fr.vol.og.words;
+    p.occ_words = fr.vol.og.words_total;   // mask + slab boxes are staged together
+    p.slab_off = fr.vol.og.words;
+    p.occ_nbz = fr.vol.og.nbz;
 
     // ---- camera basis (C3)
     const double dx = (double)fr.vol.dx;
@@ -194,7 +196,9 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
             const float L = p.Lg[l][q];
             p.alim[l][q] = L > 0.0f ? p.ahi[q] : (L < 0.0f ? p.alo[q] : 3.0e38f);
         }
-    p.pad2[0] = 0;
+    p.lz0 = 0;
+    for (int l = 0; l < 4; ++l)
+        if (l < mc.n_lights && p.Lg[l][2] == 0.0f) p.lz0 |= 1 << l;   // horizontal light: marches stay in one z slab
     out[fi] = p;
 }
 

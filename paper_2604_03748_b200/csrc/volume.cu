@@ -116,6 +116,12 @@ __global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g, 
                     }
         if (any) {
             atomicOr(mask + (b >> 5), 1u << (b & 31));
+            int32_t* smin = reinterpret_cast<int32_t*>(mask + g.words);
+            int32_t* smax = smin + 2 * g.nbz;
+            atomicMin(smin + 2 * bz, bx);
+            atomicMin(smin + 2 * bz + 1, by);
+            atomicMax(smax + 2 * bz, bx);
+            atomicMax(smax + 2 * bz + 1, by);
             atomicMin(aabb + 0, bx);
             atomicMin(aabb + 1, by);
             atomicMin(aabb + 2, bz);
@@ -146,8 +152,9 @@ OccGeom occ_geom(int nx, int ny, int nz) {
         g.nbz = (nz + 1 + B - 1) / B;
         const long bits = (long)g.nbx * g.nby * g.nbz;
         g.words = (int)(((bits + 31) / 32 + 3) / 4 * 4);
+        g.words_total = g.words + 4 * g.nbz;
         if ((forced > 0 && s >= forced) || (long)g.words * 4 <= budget) {
-            if ((long)g.words * 4 <= 16 * 1024) break;
+            if ((long)g.words * 4 <= 16 * 1024 && g.nbz <= 1024) break;
         }
     }
     return g;
@@ -156,6 +163,8 @@ OccGeom occ_geom(int nx, int ny, int nz) {
 cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, int32_t* aabb, cudaStream_t s) {
     Raw r{raw, v.nx, v.ny, v.nz};
     cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)v.og.words * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(mask + v.og.words, 0x7f, (size_t)v.og.nbz * 8, s);                 // slab min
+    if (e == cudaSuccess) e = cudaMemsetAsync(mask + v.og.words + 2 * v.og.nbz, 0xff, (size_t)v.og.nbz * 8, s);  // slab max
     if (e == cudaSuccess) e = cudaMemsetAsync(aabb, 0x7f, 3 * sizeof(int32_t), s);      // bmin = 0x7f7f7f7f
     if (e == cudaSuccess) e = cudaMemsetAsync(aabb + 3, 0xff, 3 * sizeof(int32_t), s);  // bmax = -1
     if (e != cudaSuccess) return e;
