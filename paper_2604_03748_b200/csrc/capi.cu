@@ -4,8 +4,10 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "nsl_internal.cuh"
@@ -204,22 +206,45 @@ struct Workspace {
     FrameIn* in = nullptr;
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
+    uint32_t* order = nullptr;
 };
 
+// March tile order: centre-out by the distance of the tile centre from the image
+// centre (the smoke of a billboard is centred, so heavy tiles start first and the
+// end of the launch is made of cheap border tiles).  Packed (tx | ty << 16).
+std::vector<uint32_t> tile_order(int W, int H) {
+    const int tw = march_tile_w(), th = march_tile_h();
+    const int nx = (W + tw - 1) / tw, ny = (H + th - 1) / th;
+    std::vector<std::pair<double, uint32_t>> v;
+    v.reserve((size_t)nx * ny);
+    for (int ty = 0; ty < ny; ++ty)
+        for (int tx = 0; tx < nx; ++tx) {
+            const double dx = (tx + 0.5) * tw - 0.5 * W, dy = (ty + 0.5) * th - 0.5 * H;
+            v.push_back({dx * dx + dy * dy, (uint32_t)tx | ((uint32_t)ty << 16)});
+        }
+    std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<uint32_t> out(v.size());
+    for (size_t i = 0; i < v.size(); ++i) out[i] = v[i].second;
+    return out;
+}
+
 nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
-                        const MarchConst& mc, cudaStream_t s, Workspace& ws) {
+                        const MarchConst& mc, const std::vector<uint32_t>& order, cudaStream_t s, Workspace& ws) {
     const int F = (int)frames.size();
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
+    const size_t b_o = align_up(sizeof(uint32_t) * order.size(), 256);
     const size_t b_p = sizeof(FrameParams) * F;
     retain_pool_once();
-    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_p, s), "cudaMallocAsync(frame tables)");
+    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_o + b_p, s), "cudaMallocAsync(frame tables)");
     ws.in = reinterpret_cast<FrameIn*>(ws.base);
     ws.lights = reinterpret_cast<nsl_light*>(static_cast<char*>(ws.base) + b_in);
-    ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l);
-    std::vector<char> host(b_in + b_l);
+    ws.order = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.base) + b_in + b_l);
+    ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l + b_o);
+    std::vector<char> host(b_in + b_l + b_o);
     memcpy(host.data(), frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
+    if (!order.empty()) memcpy(host.data() + b_in + b_l, order.data(), sizeof(uint32_t) * order.size());
     NSL_CUDA(cudaMemcpyAsync(ws.base, host.data(), host.size(), cudaMemcpyHostToDevice, s), "frame table upload");
     NSL_CUDA(launch_frame_setup(ws.in, ws.lights, F, mc, ws.params, s), "frame_setup_kernel launch");
     return NSL_OK;
@@ -366,9 +391,9 @@ static nsl_status batch_impl(const nsl_volume* const* vols, int32_t n_vols, cons
         return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
-    if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, s, ws)) return st;
+    if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, tile_order(P.W, P.H), s, ws)) return st;
     cudaError_t e = launch_march(ws.params, P.mc, P.F, P.W, P.H, P.proj, P.layout, P.max_words,
-                                 reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug, counters, s);
+                                 reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug, counters, ws.order, s);
     cudaError_t e2 = cudaFreeAsync(ws.base, s);
     if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
     if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(frame tables)");
@@ -459,6 +484,7 @@ struct nsl_plan {
     FrameIn* in = nullptr;
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
+    uint32_t* order = nullptr;
 };
 
 nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
@@ -472,20 +498,24 @@ nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const 
         delete p;
         return st;
     }
+    const std::vector<uint32_t> order = tile_order(p->P.W, p->P.H);
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
+    const size_t b_o = align_up(sizeof(uint32_t) * order.size(), 256);
     const size_t b_p = sizeof(FrameParams) * F;
-    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_p);
+    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_o + b_p);
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaMalloc(plan)");
     }
     p->in = reinterpret_cast<FrameIn*>(p->dev);
     p->lights = reinterpret_cast<nsl_light*>(static_cast<char*>(p->dev) + b_in);
-    p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l);
-    std::vector<char> host(b_in + b_l);
+    p->order = reinterpret_cast<uint32_t*>(static_cast<char*>(p->dev) + b_in + b_l);
+    p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_o);
+    std::vector<char> host(b_in + b_l + b_o);
     memcpy(host.data(), p->P.frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
+    memcpy(host.data() + b_in + b_l, order.data(), sizeof(uint32_t) * order.size());
     e = cudaMemcpyAsync(p->dev, host.data(), host.size(), cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) {
         cudaFree(p->dev);
@@ -509,7 +539,7 @@ nsl_status nsl_plan_execute(const nsl_plan* p, float* out_rgbt, float* out_depth
     NSL_CUDA(launch_frame_setup(p->in, p->lights, p->P.F, p->P.mc, p->params, s), "frame_setup_kernel launch");
     NSL_CUDA(launch_march(p->params, p->P.mc, p->P.F, p->P.W, p->P.H, p->P.proj, p->P.layout, p->P.max_words,
                           reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug,
-                          reinterpret_cast<unsigned long long*>(counters), s),
+                          reinterpret_cast<unsigned long long*>(counters), p->order, s),
              "march_kernel launch");
     return NSL_OK;
 }
@@ -542,7 +572,7 @@ nsl_status nsl_debug_frame_constants(const nsl_grid_desc* g, const nsl_camera* c
     const MarchConst mc = make_const(n_lights, light_mode, med, m);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
-    if (nsl_status st = build_frames(frames, lights, n_lights, mc, s, ws)) return st;
+    if (nsl_status st = build_frames(frames, lights, n_lights, mc, std::vector<uint32_t>(), s, ws)) return st;
     FrameParams p;
     cudaError_t e = cudaMemcpyAsync(&p, ws.params, sizeof p, cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(ws.base, s);

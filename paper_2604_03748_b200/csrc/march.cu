@@ -22,7 +22,10 @@
 namespace nsl {
 namespace {
 
-constexpr int kTileW = 16, kTileH = 16, kThreads = 256;
+#ifndef NSL_TILEH
+#define NSL_TILEH 16     // CTA tile 16 x NSL_TILEH pixels (warps of 8x4): 16 -> 256 threads, 8 -> 128
+#endif
+constexpr int kTileW = 16, kTileH = NSL_TILEH, kThreads = 2 * NSL_TILEH * 8;
 #ifndef NSL_BLOCKIDX
 #define NSL_BLOCKIDX 0   // occupancy block index: 1 exact fp32 FMAs, 0 integer shifts of the cell floor (measured equal, profiles/r1_sweep.txt)
 #endif
@@ -361,23 +364,29 @@ __device__ __forceinline__ float hg32(float g, float c) {
 }
 
 template <int LAYOUT, int PROJ, int MODE>
-__global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
+__global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
-                                                         unsigned long long* __restrict__ counters, int W, int H) {
+                                                         unsigned long long* __restrict__ counters, int W, int H,
+                                                         const uint32_t* __restrict__ tile_order, int F) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
     uint4* smem = reinterpret_cast<uint4*>(nsl_smem);
     FrameParams& sp = *reinterpret_cast<FrameParams*>(smem);
     uint4* smask4 = smem + sizeof(FrameParams) / 16;
-    const int f = blockIdx.z;
+    // 1-D grid over (tile rank, frame), frame fastest; tiles in centre-out order
+    // (tile_order) so the heavy tiles of every frame start first and the tail of
+    // the launch is made of cheap border tiles.
+    const int f = (int)(blockIdx.x % (unsigned)F);
+    const uint32_t tile = __ldg(tile_order + blockIdx.x / (unsigned)F);
+    const int tx = (int)(tile & 0xffffu), ty = (int)(tile >> 16);
     {
         const uint4* src = reinterpret_cast<const uint4*>(fps + f);
         for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 16); i += blockDim.x) smem[i] = src[i];
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int px = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
-    const int py = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
+    const int px = tx * kTileW + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);
     const bool valid = px < W && py < H;
     const size_t o = (size_t)f * (size_t)W * (size_t)H + (size_t)py * W + px;
 
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB) march_kernel(const FramePa
         // within tile_r of the centre ray; if the centre ray misses the support box
         // expanded by tile_r, no sample of the tile is in support (C5) and the
         // output is the empty map (L = 0, T = 1, D = 0, counters 0).
-        const float cx = (float)(blockIdx.x * kTileW) + 7.5f, cy = (float)(blockIdx.y * kTileH) + 7.5f;
+        const float cx = (float)(tx * kTileW) + 0.5f * (kTileW - 1), cy = (float)(ty * kTileH) + 0.5f * (kTileH - 1);
         Ray c;
         c.ox = fmaf(cy, sp.Ey[0], fmaf(cx, sp.Ex[0], sp.B[0]));
         c.oy = fmaf(cy, sp.Ey[1], fmaf(cx, sp.Ex[1], sp.B[1]));
@@ -671,43 +680,51 @@ __global__ void jitter_debug_kernel(MarchConst mc, uint32_t frame, int n, uint32
 
 template <int LAYOUT, int PROJ, int MODE>
 cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, size_t smem, float4* rgbt,
-                       float* depth, uint32_t* debug, unsigned long long* counters, cudaStream_t s) {
+                       float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* tile_order,
+                       cudaStream_t s) {
     const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
-    dim3 grid((unsigned)tiles_x, (unsigned)tiles_y, (unsigned)F);
+    dim3 grid((unsigned)(tiles_x * tiles_y) * (unsigned)F);
     auto k = march_kernel<LAYOUT, PROJ, MODE>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k<<<grid, kThreads, smem, s>>>(fp, mc, rgbt, depth, debug, counters, W, H);
+    k<<<grid, kThreads, smem, s>>>(fp, mc, rgbt, depth, debug, counters, W, H, tile_order, F);
     return cudaGetLastError();
 }
 
 template <int LAYOUT, int PROJ>
 cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, size_t smem, float4* rgbt,
-                      float* depth, uint32_t* debug, unsigned long long* counters, cudaStream_t s) {
-    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
-    if (counters) return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
-    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
+                      float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* to, cudaStream_t s) {
+    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
+    if (counters) return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
+    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
 }
 
 template <int LAYOUT>
 cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, size_t smem,
-                     float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters, cudaStream_t s) {
-    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s)
-                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, s);
+                     float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* to,
+                     cudaStream_t s) {
+    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s)
+                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
 }
 
 }  // namespace
 
+int march_tile_w() { return kTileW; }
+int march_tile_h() { return kTileH; }
+
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection, int layout,
                          int max_occ_words, float4* rgbt, float* depth, uint32_t* debug,
-                         unsigned long long* counters, cudaStream_t s) {
+                         unsigned long long* counters, const uint32_t* tile_order, cudaStream_t s) {
     const size_t smem = sizeof(FrameParams) + (size_t)max_occ_words * 4;
     switch (layout) {
-        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, s);
-        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, s);
-        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, s);
+        case kLinearF32:
+            return launch_l<kLinearF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, tile_order, s);
+        case kQuadF32:
+            return launch_l<kQuadF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, tile_order, s);
+        case kCornerF16:
+            return launch_l<kCornerF16>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, tile_order, s);
     }
     return cudaErrorInvalidValue;
 }

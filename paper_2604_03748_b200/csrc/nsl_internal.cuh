@@ -99,7 +99,9 @@ cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F
 // mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection,
                          int layout, int max_occ_words, float4* rgbt, float* depth, uint32_t* debug,
-                         unsigned long long* counters, cudaStream_t s);
+                         unsigned long long* counters, const uint32_t* tile_order, cudaStream_t s);
+int march_tile_w();
+int march_tile_h();
 cudaError_t launch_jitter_debug(const MarchConst& mc, uint32_t frame_id, int n, uint32_t* hash, float* delta,
                                 cudaStream_t s);
 
