@@ -23,7 +23,7 @@ namespace nsl {
 namespace {
 
 #ifndef NSL_TILEH
-#define NSL_TILEH 16     // CTA tile 16 x NSL_TILEH pixels (warps of 8x4): 16 -> 256 threads, 8 -> 128
+#define NSL_TILEH 8      // CTA tile 16 x NSL_TILEH pixels (warps of 8x4): 8 -> 128 threads (measured best), 16 -> 256
 #endif
 constexpr int kTileW = 16, kTileH = NSL_TILEH, kThreads = 2 * NSL_TILEH * 8;
 #ifndef NSL_BLOCKIDX
