@@ -35,6 +35,10 @@ constexpr int kTileW = 16, kTileH = NSL_TILEH, kThreads = 2 * NSL_TILEH * 8;
 #ifndef NSL_PAIRWALK
 #define NSL_PAIRWALK 1   // paired top/bottom march: 1 combined chord walk, 0 lock-step both sides
 #endif
+#ifndef NSL_STAGE
+#define NSL_STAGE 1      // 1: stage FrameParams + occupancy region in shared memory per CTA; 0: read them
+                         //    through the read-only path from global memory (L1-resident)
+#endif
 #ifndef NSL_MINB
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
                      // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)
@@ -43,6 +47,7 @@ constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
     const void* __restrict__ data;
+    const uint32_t* __restrict__ occ;   // occupancy region in global memory (NSL_STAGE == 0)
     uint32_t mask_sa;             // shared-space byte address of the occupancy mask
     int sy, sz;
     float inv_b, nbx_f, nbxy_f;   // 2^-shift, blocks per x row, blocks per z slab (exact in fp32)
@@ -99,7 +104,11 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
     uint32_t word;
     asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(v.mask_sa + ((uint32_t)b >> 5) * 4u));
 #else
+#if NSL_STAGE
     const uint32_t word = nsl_smem[kMaskWord0 + (b >> 5)];
+#else
+    const uint32_t word = __ldg(v.occ + (b >> 5));
+#endif
 #endif
     if (!((word >> (b & 31)) & 1u)) return 0.0f;
     if (COUNT) ++gathers;
@@ -341,9 +350,15 @@ __device__ __forceinline__ void march_region(const FrameParams& sp, const Vol& v
     if ((sp.lz0 >> l) & 1) {
         const int iz = __float_as_int(__fadd_rd(uz, kFloorBias)) - 0x4B400000;
         const int bz = iz >> v.shift;
+#if NSL_STAGE
         const int* slab = reinterpret_cast<const int*>(nsl_smem) + kMaskWord0 + sp.slab_off;
         const int2 mn = *reinterpret_cast<const int2*>(slab + 2 * bz);
         const int2 mx = *reinterpret_cast<const int2*>(slab + 2 * sp.occ_nbz + 2 * bz);
+#else
+        const int* slab = reinterpret_cast<const int*>(v.occ) + sp.slab_off;
+        const int2 mn = __ldg(reinterpret_cast<const int2*>(slab + 2 * bz));
+        const int2 mx = __ldg(reinterpret_cast<const int2*>(slab + 2 * sp.occ_nbz + 2 * bz));
+#endif
         const float B = (float)(1 << v.shift);
         const float lox = (float)mn.x * B, hix = fminf((float)(mx.x + 1) * B, v.sx1);
         const float loy = (float)mn.y * B, hiy = fminf((float)(mx.y + 1) * B, v.sy1);
@@ -370,20 +385,26 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
                                                          unsigned long long* __restrict__ counters, int W, int H,
                                                          const uint32_t* __restrict__ tile_order, int F) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
+#if NSL_STAGE
     uint4* smem = reinterpret_cast<uint4*>(nsl_smem);
     FrameParams& sp = *reinterpret_cast<FrameParams*>(smem);
     uint4* smask4 = smem + sizeof(FrameParams) / 16;
+#endif
     // 1-D grid over (tile rank, frame), frame fastest; tiles in centre-out order
     // (tile_order) so the heavy tiles of every frame start first and the tail of
     // the launch is made of cheap border tiles.
     const int f = (int)(blockIdx.x % (unsigned)F);
     const uint32_t tile = __ldg(tile_order + blockIdx.x / (unsigned)F);
     const int tx = (int)(tile & 0xffffu), ty = (int)(tile >> 16);
+#if NSL_STAGE
     {
         const uint4* src = reinterpret_cast<const uint4*>(fps + f);
         for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 16); i += blockDim.x) smem[i] = src[i];
     }
     __syncthreads();
+#else
+    const FrameParams& sp = fps[f];
+#endif
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx * kTileW + (warp & 1) * 8 + (lane & 7);
     const int py = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);
@@ -394,7 +415,12 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
     v.data = sp.data;
     v.sy = sp.sy;
     v.sz = sp.sz;
+#if NSL_STAGE
     v.mask_sa = (uint32_t)__cvta_generic_to_shared(smask4);
+#else
+    v.mask_sa = 0;
+#endif
+    v.occ = sp.occ;
     v.inv_b = __int_as_float((127 - sp.occ_shift) << 23);   // 2^-shift exactly
     v.nbx_f = (float)sp.occ_nbx;
     v.nbxy_f = (float)(sp.occ_nbx * sp.occ_nby);
@@ -443,12 +469,14 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
             return;   // uniform over the CTA
         }
     }
+#if NSL_STAGE
     {
         const uint4* src = reinterpret_cast<const uint4*>(sp.occ);
         const int n4 = sp.occ_words >> 2;
         for (int i = threadIdx.x; i < n4; i += blockDim.x) smask4[i] = __ldg(src + i);
     }
     __syncthreads();
+#endif
     if (!COUNT && !valid) return;
 
     uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0, c_tp = 0, c_tl = 0;
@@ -717,7 +745,7 @@ int march_tile_h() { return kTileH; }
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection, int layout,
                          int max_occ_words, float4* rgbt, float* depth, uint32_t* debug,
                          unsigned long long* counters, const uint32_t* tile_order, cudaStream_t s) {
-    const size_t smem = sizeof(FrameParams) + (size_t)max_occ_words * 4;
+    const size_t smem = NSL_STAGE ? sizeof(FrameParams) + (size_t)max_occ_words * 4 : 0;
     switch (layout) {
         case kLinearF32:
             return launch_l<kLinearF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, tile_order, s);

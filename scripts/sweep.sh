@@ -12,6 +12,6 @@ except Exception as e:
 PY
 }
 bash scripts/build_variants.sh
-for mb in ${MBS:-5}; do for th in 8 16; do for sh in ${SHIFTS:-2}; do
-  run NSL_LIB=/tmp/libnsl_mb${mb}_t${th}_p0.so NSL_OCC_SHIFT=$sh
+for mb in ${MBS:-5}; do for st in 0 1; do for sh in ${SHIFTS:-2}; do
+  run NSL_LIB=/tmp/libnsl_mb${mb}_t8_s${st}.so NSL_OCC_SHIFT=$sh
 done; done; done
