@@ -36,8 +36,9 @@ constexpr int kTileW = 16, kTileH = NSL_TILEH, kThreads = 2 * NSL_TILEH * 8;
 #define NSL_PAIRWALK 1   // paired top/bottom march: 1 combined chord walk, 0 lock-step both sides
 #endif
 #ifndef NSL_STAGE
-#define NSL_STAGE 1      // 1: stage FrameParams + occupancy region in shared memory per CTA; 0: read them
-                         //    through the read-only path from global memory (L1-resident)
+#define NSL_STAGE 0      // 1: stage FrameParams + occupancy region in shared memory per CTA; 0: read them
+                         //    through the read-only path from global memory (L1-resident; measured equal or
+                         //    better, no __syncthreads, all of L1 for the volume)
 #endif
 #ifndef NSL_MINB
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
@@ -59,7 +60,9 @@ struct Vol {
 // Indexed through this file-scope array so the mask test is one LDS with an
 // immediate offset (no generic->shared address conversion in the loops).
 extern __shared__ __align__(16) uint32_t nsl_smem[];
+#if NSL_STAGE
 constexpr int kMaskWord0 = (int)(sizeof(FrameParams) / 4);
+#endif
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return __fmaf_rn(t, b - a, a); }
 
