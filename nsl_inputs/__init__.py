@@ -125,6 +125,22 @@ class March:
 
 
 @dataclass
+class Bake:
+    """Six-way bake parameters: spp, primary step h_b, light step h_bl (world)."""
+    spp: int = 16
+    step: float = 0.0
+    light_step: float = 0.0
+    max_steps: int = 0
+    t_min: float = 1e-4
+    seed: int = 0x6B616B65
+
+
+def default_bake(n: int, spp: int = 16, **kw) -> "Bake":
+    b = Bake(spp=spp, step=float(np.float32(1.0 / n)), light_step=float(np.float32(2.0 / n)))
+    return replace(b, **kw)
+
+
+@dataclass
 class Workload:
     name: str
     grid: Grid

@@ -219,3 +219,65 @@ def run_workload_frame(w, f: int, pixels=None, **kw) -> dict:
     """Oracle on frame f (local index) of an nsl_inputs.Workload."""
     return guiding_map(w.grid, w.volume(w.frame_vol[f]), w.cameras[f], w.lights[f], w.light_mode,
                        w.medium, w.march, frame_id=w.frame_ids[f], pixels=pixels, **kw)
+
+
+# ------------------------------------------------------------------ NEXT-1 six-way bake (DESIGN.md §10)
+class OrcBake(ctypes.Structure):
+    _fields_ = [("spp", ctypes.c_int32), ("step", ctypes.c_float), ("light_step", ctypes.c_float),
+                ("max_steps", ctypes.c_int32), ("t_min", ctypes.c_float), ("seed", ctypes.c_uint64)]
+
+
+def _bake_s(b) -> OrcBake:
+    return OrcBake(b.spp, b.step, b.light_step, b.max_steps, b.t_min, b.seed & 0xFFFFFFFFFFFFFFFF)
+
+
+def _load_bake():
+    L = _load()
+    if not getattr(L, "_bake_ready", False):
+        P = ctypes.POINTER
+        L.orc_bake_random.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                      P(ctypes.c_float)]
+        L.orc_bake_light_constants.argtypes = [P(OrcGrid), P(OrcCamera), ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_sixway_bake.argtypes = [P(OrcGrid), ctypes.c_void_p, DENSITY_FN, ctypes.c_void_p, P(OrcCamera),
+                                      P(OrcMedium), P(OrcBake), ctypes.c_uint32, ctypes.c_int64, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_sixway_bake.restype = ctypes.c_int
+        L._bake_ready = True
+    return L
+
+
+def bake_random(seed: int, frame: int, pixel: int, sample: int):
+    out = (ctypes.c_float * 4)()
+    _load_bake().orc_bake_random(seed & 0xFFFFFFFFFFFFFFFF, frame, pixel, sample, out)
+    return np.array(list(out), np.float32)
+
+
+def bake_light_constants(grid, cam):
+    Lg = np.zeros((6, 3), np.float32)
+    Ln = np.zeros((6, 3), np.float32)
+    _load_bake().orc_bake_light_constants(ctypes.byref(_grid(grid)), ctypes.byref(_camera(cam)), Lg.ctypes.data,
+                                          Ln.ctypes.data)
+    return Lg, Ln
+
+
+def sixway_bake(grid, vals, cam, medium, bake, frame_id: int = 0, pixels=None, density_fn=None) -> dict:
+    """Oracle of the six-way bake (B1-B6).  Returns out (n, 8) f64 in the Fig. 2 packing
+    (right, top, back, T, left, bottom, front, E), steps (n,) u32, pixels."""
+    L = _load_bake()
+    W, H = cam.width, cam.height
+    if pixels is None:
+        pix, n = None, W * H
+    else:
+        pix = np.ascontiguousarray(np.asarray(pixels, dtype=np.int64))
+        n = int(pix.size)
+    out = np.zeros((n, 8), np.float64)
+    steps = np.zeros((n,), np.uint32)
+    v = None if vals is None else np.ascontiguousarray(vals, dtype=np.float32)
+    cb = DENSITY_FN(density_fn) if density_fn is not None else DENSITY_FN()
+    rc = L.orc_sixway_bake(ctypes.byref(_grid(grid)), None if v is None else v.ctypes.data, cb, None,
+                           ctypes.byref(_camera(cam)), ctypes.byref(_medium(medium)), ctypes.byref(_bake_s(bake)),
+                           frame_id, n, None if pix is None else pix.ctypes.data, out.ctypes.data,
+                           steps.ctypes.data)
+    if rc:
+        raise ValueError("orc_sixway_bake rejected its arguments")
+    return {"out": out, "steps": steps, "pixels": np.arange(n, dtype=np.int64) if pix is None else pix}

@@ -367,3 +367,158 @@ int orc_guiding_map(const orc_grid* g, const float* vals,
     }
     return 0;
 }
+
+/* ================================================================ NEXT-1: six-way bake
+ * DESIGN.md §10 (B1-B6): deterministic single-scatter estimator of the six-way
+ * lightmaps ("{L_x^+, L_x^-, L_y^+, L_y^-, L_z^+, L_z^-}", L477
+ * "single bounce ... g = 0 ... samples per pixel"), transparency (L255) and an
+ * emissive carrier; jittered fixed-step quadrature with counter-based RNG. */
+
+static void camera_axes(const orc_camera* cam, double f[3], double r[3], double u[3]) {
+    double F[3] = {cam->forward[0], cam->forward[1], cam->forward[2]};
+    double Up[3] = {cam->up[0], cam->up[1], cam->up[2]};
+    double nf = norm3(F);
+    for (int a = 0; a < 3; ++a) f[a] = F[a] / nf;
+    double c[3];
+    cross3(f, Up, c);
+    double nc = norm3(c);
+    for (int a = 0; a < 3; ++a) r[a] = c[a] / nc;
+    cross3(r, f, u);
+}
+
+/* B2: counter-based stream keyed by (seed, frame, pixel, sample) */
+void orc_bake_random(uint64_t seed, uint32_t frame, uint32_t pixel, uint32_t sample, float u_out[4]) {
+    uint32_t h = orc_fmix32((uint32_t)(seed & 0xffffffffu) ^ 0x85EBCA6Bu);
+    h = orc_fmix32(h ^ (uint32_t)(seed >> 32));
+    h = orc_fmix32(h ^ frame);
+    h = orc_fmix32(h ^ pixel);
+    h = orc_fmix32(h ^ sample);
+    for (int i = 0; i < 4; ++i) {
+        u_out[i] = (float)(h >> 8) * (1.0f / 16777216.0f);
+        h = orc_fmix32(h + 0x9E3779B9u);
+    }
+}
+
+/* B1: billboard-axis light directions n_l (fp64) in the packing order of B6:
+ * right +r, top +u, back f, left -r, bottom -u, front -f. */
+static void bake_lights(const orc_camera* cam, double n[6][3]) {
+    double f[3], r[3], u[3];
+    camera_axes(cam, f, r, u);
+    for (int a = 0; a < 3; ++a) {
+        n[0][a] = r[a];
+        n[1][a] = u[a];
+        n[2][a] = f[a];
+        n[3][a] = -r[a];
+        n[4][a] = -u[a];
+        n[5][a] = -f[a];
+    }
+}
+
+int orc_bake_light_constants(const orc_grid* g, const orc_camera* cam, float Lg[6][3], float Ln[6][3]) {
+    if (!g || !cam) return 1;
+    double n[6][3];
+    bake_lights(cam, n);
+    for (int l = 0; l < 6; ++l)
+        for (int a = 0; a < 3; ++a) {
+            Ln[l][a] = (float)n[l][a];
+            Lg[l][a] = (float)(n[l][a] / (double)g->voxel_width);
+        }
+    return 0;
+}
+
+int orc_sixway_bake(const orc_grid* g, const float* vals, orc_density_fn density_fn, void* density_ctx,
+                    const orc_camera* cam, const orc_medium* med, const orc_bake* b, uint32_t frame_id,
+                    int64_t n_pix, const int64_t* pix, double* out8, uint32_t* out_steps) {
+    if (!g || (!vals && !density_fn) || !cam || !med || !b || !out8) return 1;
+    if (b->spp < 1 || !(b->step > 0.0f) || !(b->light_step > 0.0f)) return 1;
+    const orc_light dummy[1] = {{{1.0f, 0.0f, 0.0f}, {1.0f, 1.0f, 1.0f}}};
+    orc_march m0;
+    memset(&m0, 0, sizeof m0);
+    m0.step = b->step;
+    orc_frame_constants fc;
+    if (orc_frame_constants_compute(g, cam, dummy, 1, 0, med, &m0, &fc)) return 1;
+    double n6[6][3];
+    bake_lights(cam, n6);
+    float Lg[6][3], Ln[6][3];
+    orc_bake_light_constants(g, cam, Lg, Ln);
+    const int W = cam->width, H = cam->height;
+    if (!pix) n_pix = (int64_t)W * H;
+    const float hb = b->step, hbl = b->light_step;
+    const double kappa = (double)med->extinction, alpha = (double)med->albedo, ghg = (double)med->hg_g;
+    const dens_t dens = {g, vals, density_fn, density_ctx};
+
+    for (int64_t q = 0; q < n_pix; ++q) {
+        int64_t p = pix ? pix[q] : q;
+        int px = (int)(p % W), py = (int)(p / W);
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t steps = 0;
+        for (int s = 0; s < b->spp; ++s) {
+            float u4[4];
+            orc_bake_random(b->seed, frame_id, (uint32_t)p, (uint32_t)s, u4);
+            const float fx = (float)px + (u4[0] - 0.5f), fy = (float)py + (u4[1] - 0.5f);
+            float O[3], D[3], dir[3];
+            if (cam->projection == 0) {
+                for (int a = 0; a < 3; ++a) {
+                    O[a] = fmaf(fy, fc.Ey[a], fmaf(fx, fc.Ex[a], fc.B[a]));
+                    D[a] = fc.Dg[a];
+                    dir[a] = fc.fwd[a];
+                }
+            } else {
+                float d[3];
+                for (int a = 0; a < 3; ++a) d[a] = fmaf(fy, fc.Ey[a], fmaf(fx, fc.Ex[a], fc.F0[a]));
+                float qn = fmaf(d[2], d[2], fmaf(d[1], d[1], d[0] * d[0]));
+                float inv = 1.0f / sqrtf(qn);
+                for (int a = 0; a < 3; ++a) {
+                    dir[a] = d[a] * inv;
+                    D[a] = dir[a] * fc.inv_dx;
+                    O[a] = fc.Oe[a];
+                }
+            }
+            double P[6];
+            for (int l = 0; l < 6; ++l)
+                P[l] = orc_hg(ghg, ((double)Ln[l][0] * dir[0] + (double)Ln[l][1] * dir[1]) + (double)Ln[l][2] * dir[2]);
+            const float o2 = u4[2] * hb, o3 = u4[3] * hbl;
+            /* k = 0 .. k_max; every k tested (the bound only limits the loop) */
+            int64_t k_max = primary_upper_bound(g, O, D, o2, hb) + 1;
+            if (b->max_steps > 0 && k_max > b->max_steps) k_max = b->max_steps;
+            double tau = 0.0, sc[6] = {0, 0, 0, 0, 0, 0}, em = 0.0;
+            for (int64_t k = 0; k <= k_max; ++k) {
+                float t = fmaf((float)k, hb, o2);
+                float U[3] = {fmaf(t, D[0], O[0]), fmaf(t, D[1], O[1]), fmaf(t, D[2], O[2])};
+                if (!inside_support(g, U)) continue;
+                ++steps;
+                double rho = density(&dens, U);
+                if (!(rho > 0.0)) continue;
+                double sigma_t = kappa * rho;
+                double Tk = exp(-tau);
+                double wsc = alpha * sigma_t * (double)hb * Tk;          /* sigma_s h T_k */
+                em += (1.0 - alpha) * sigma_t * (double)hb * Tk;           /* sigma_a h T_k */
+                for (int l = 0; l < 6; ++l) {
+                    double sum = 0.0;
+                    for (uint32_t j = 1;; ++j) {
+                        float sj = fmaf((float)(j - 1), hbl, o3);
+                        float Y[3] = {fmaf(sj, Lg[l][0], U[0]), fmaf(sj, Lg[l][1], U[1]), fmaf(sj, Lg[l][2], U[2])};
+                        if (!inside_support(g, Y)) break;
+                        sum += kappa * density(&dens, Y);
+                        if (j > 100000000u) break;
+                    }
+                    sc[l] += wsc * exp(-(double)hbl * sum) * P[l];
+                }
+                tau += sigma_t * (double)hb;
+                if (b->t_min > 0.0f && (float)exp(-tau) < b->t_min) break;
+            }
+            /* B6 packing: (right, top, back, T) (left, bottom, front, E) */
+            acc[0] += sc[0];
+            acc[1] += sc[1];
+            acc[2] += sc[2];
+            acc[3] += exp(-tau);
+            acc[4] += sc[3];
+            acc[5] += sc[4];
+            acc[6] += sc[5];
+            acc[7] += em;
+        }
+        for (int c = 0; c < 8; ++c) out8[8 * q + c] = acc[c] / (double)b->spp;
+        if (out_steps) out_steps[q] = steps;
+    }
+    return 0;
+}

@@ -91,6 +91,23 @@ int orc_guiding_map(const orc_grid* g, const float* vals,
                     double* out_rgbt, float* out_depth, uint32_t* out_debug, double* out_margin,
                     const int32_t* forced_hit, const int32_t* forced_term, int32_t no_clip_n);
 
+/* NEXT-1 six-way bake (B1-B6). */
+typedef struct {
+    int32_t spp;                      /* samples per pixel >= 1 */
+    float step, light_step;           /* h_b, h_bl (world units) */
+    int32_t max_steps;                /* cap on k (0 = none) */
+    float t_min;                      /* early termination (0 = off) */
+    uint64_t seed;
+} orc_bake;
+
+void orc_bake_random(uint64_t seed, uint32_t frame, uint32_t pixel, uint32_t sample, float u_out[4]);
+int orc_bake_light_constants(const orc_grid* g, const orc_camera* cam, float Lg[6][3], float Ln[6][3]);
+/* out8: n_pix x 8 doubles in the Fig. 2 packing (right, top, back, T, left, bottom, front, E);
+ * out_steps: NULL or n_pix u32 = in-support primary samples summed over the spp samples. */
+int orc_sixway_bake(const orc_grid* g, const float* vals, orc_density_fn density_fn, void* density_ctx,
+                    const orc_camera* cam, const orc_medium* med, const orc_bake* b, uint32_t frame_id,
+                    int64_t n_pix, const int64_t* pix, double* out8, uint32_t* out_steps);
+
 #ifdef __cplusplus
 }
 #endif
