@@ -210,6 +210,37 @@ nsl_status nsl_plan_execute(const nsl_plan* plan, float* out_rgbt, float* out_de
                             uint64_t* counters, nsl_stream stream);
 nsl_status nsl_plan_destroy(nsl_plan* plan);
 
+/* ------------------------------------------------------------------ NEXT-1: six-way bake
+ * Reference single-scatter six-way lightmaps (B1-B6): the
+ * lightmaps {L_x^+-, L_y^+-, L_z^+-} along the camera's billboard axes
+ * (PAPER.md L219), transparency (L255) and an emissive carrier, by jittered
+ * fixed-step quadrature with `spp` counter-based samples per pixel (L477
+ * "single bounce ... g = 0 ... samples per pixel").  Volumes, cameras and
+ * medium as for nsl_guiding_map_batch (lights are fixed: six unit-white
+ * axis lights).  spp >= 1; step > 0 (h_b), light_step > 0 (h_bl); max_steps
+ * >= 0 caps k; t_min in [0,1).
+ *   out: device, F*H*W*8 floats = two float4 per pixel in the Fig. 2 packing:
+ *        (right +X, top +Y, back -Z, transparency) (left -X, bottom -Y, front +Z, emissive)
+ *   counters: device u64[1] (zeroed by the call) += trilinear gathers, or NULL. */
+typedef struct {
+    int32_t spp;
+    float step, light_step;
+    int32_t max_steps;
+    float t_min;
+    uint64_t seed;
+} nsl_bake;
+
+nsl_status nsl_sixway_bake(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                           const nsl_camera* cams, const nsl_medium* med, const nsl_bake* b,
+                           const uint32_t* frame_ids, int32_t F, float* out, uint64_t* counters,
+                           nsl_stream stream);
+
+/* The six bake light directions as the device computes them (fp64 -> fp32):
+ * Lg[l] = n_l / dx, Ln[l] = n_l in the B6 order (right, top, back, left,
+ * bottom, front); host outputs; synchronises `stream`. */
+nsl_status nsl_debug_bake_lights(const nsl_grid_desc* g, const nsl_camera* cam, float Lg[6][3], float Ln[6][3],
+                                 nsl_stream stream);
+
 /* End-to-end convenience call with HOST buffers: uploads the host density
  * grid, lays it out, marches the F frames and copies the results back into
  * host out_rgbt (F*H*W*4 floats) / out_depth (F*H*W floats); synchronises

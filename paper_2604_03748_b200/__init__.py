@@ -18,8 +18,9 @@ from typing import List, Optional, Sequence
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.environ.get("NSL_LIB") or os.path.join(_HERE, "lib", "libnsl.so")   # NSL_LIB: build variants
-CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu")]
-HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_ROOT, "include", "nsl.h")]
+CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu", "bake.cu")]
+HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_HERE, "csrc", "sampler.cuh"),
+           os.path.join(_ROOT, "include", "nsl.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
 
@@ -80,7 +81,13 @@ class FrameConstantsS(ctypes.Structure):
 EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_upload", "nsl_volume_check",
            "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_batch_counted",
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
-           "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter"]
+           "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
+           "nsl_sixway_bake", "nsl_debug_bake_lights"]
+
+
+class BakeS(ctypes.Structure):
+    _fields_ = [("spp", ctypes.c_int32), ("step", ctypes.c_float), ("light_step", ctypes.c_float),
+                ("max_steps", ctypes.c_int32), ("t_min", ctypes.c_float), ("seed", ctypes.c_uint64)]
 
 _lib = None
 
@@ -119,6 +126,8 @@ def lib():
     L.nsl_debug_frame_constants.argtypes = [P(GridDesc), P(CameraS), P(LightS), i32, i32, P(MediumS),
                                             P(MarchS), P(FrameConstantsS), vp]
     L.nsl_debug_jitter.argtypes = [P(MarchS), u32, i32, vp, vp, vp]
+    L.nsl_sixway_bake.argtypes = [P(vp), i32, P(i32), P(CameraS), P(MediumS), P(BakeS), P(u32), i32, vp, vp, vp]
+    L.nsl_debug_bake_lights.argtypes = [P(GridDesc), P(CameraS), vp, vp, vp]
     for name in EXPORTS[2:]:
         if name != "nsl_volume_bytes":
             getattr(L, name).restype = ctypes.c_int
@@ -318,6 +327,42 @@ class Plan:
 def make_plan(w, vols, march=None, stream=None) -> Plan:
     return Plan(vols, w.frame_vol, w.cameras, w.lights, w.light_mode, w.medium, march or w.march, w.frame_ids,
                 stream=stream)
+
+
+def bake_s(b) -> BakeS:
+    return BakeS(b.spp, b.step, b.light_step, b.max_steps, b.t_min, b.seed & 0xFFFFFFFFFFFFFFFF)
+
+
+def sixway_bake(vols, frame_vol, cams, medium, bake, frame_ids, out, counters=None, stream=None):
+    """NEXT-1 six-way bake.  out: cuda float32 [F, H, W, 2, 4] in the Fig. 2
+    packing (right, top, back, T)(left, bottom, front, E); counters: int64[1] (gathers) or None."""
+    F = len(cams)
+    hv = (ctypes.c_void_p * len(vols))(*[v.handle.value for v in vols])
+    fv = (ctypes.c_int32 * F)(*frame_vol)
+    cs = (CameraS * F)(*[camera_s(c) for c in cams])
+    fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+    _check(lib().nsl_sixway_bake(hv, len(vols), fv, cs, ctypes.byref(medium_s(medium)), ctypes.byref(bake_s(bake)),
+                                 fid, F, _ptr(out), _ptr(counters), _stream_handle(stream)), "nsl_sixway_bake")
+
+
+def debug_bake_lights(grid, cam, stream=None):
+    import numpy as np
+    Lg = np.zeros((6, 3), np.float32)
+    Ln = np.zeros((6, 3), np.float32)
+    _check(lib().nsl_debug_bake_lights(ctypes.byref(grid_desc(grid)), ctypes.byref(camera_s(cam)), Lg.ctypes.data,
+                                       Ln.ctypes.data, _stream_handle(stream)), "nsl_debug_bake_lights")
+    return Lg, Ln
+
+
+def run_bake(w, bake, layout: int = LAYOUT_DEFAULT, vols=None, out=None, stream=None):
+    """Six-way bake of every frame of an nsl_inputs.Workload; returns the [F, H, W, 2, 4] tensor."""
+    import torch
+    if vols is None:
+        vols = upload_workload_volumes(w, layout, stream=stream)
+    if out is None:
+        out = torch.empty((w.n_frames, w.height, w.width, 2, 4), dtype=torch.float32, device="cuda")
+    sixway_bake(vols, w.frame_vol, w.cameras, w.medium, bake, w.frame_ids, out, stream=stream)
+    return out
 
 
 def guiding_map_host(grid, host_density, layout, cams, lights, light_mode, medium, march, frame_ids,

@@ -551,6 +551,104 @@ nsl_status nsl_plan_destroy(nsl_plan* p) {
     return e == cudaSuccess ? NSL_OK : cuda_fail(e, "cudaFree(plan)");
 }
 
+// ------------------------------------------------------------------ NEXT-1 six-way bake
+static nsl_status check_bake(const nsl_bake* b) {
+    if (!b) return fail(NSL_ERR_INVALID_ARG, "bake params are NULL");
+    if (b->spp < 1 || b->spp > (1 << 20)) return fail(NSL_ERR_INVALID_ARG, "spp must be in [1, 2^20]");
+    if (!(b->step > 0.0f) || !std::isfinite(b->step)) return fail(NSL_ERR_INVALID_ARG, "bake step must be > 0");
+    if (!(b->light_step > 0.0f) || !std::isfinite(b->light_step))
+        return fail(NSL_ERR_INVALID_ARG, "bake light_step must be > 0");
+    if (b->max_steps < 0 || b->max_steps > (1 << 24)) return fail(NSL_ERR_INVALID_ARG, "max_steps out of range");
+    if (!(b->t_min >= 0.0f && b->t_min < 1.0f)) return fail(NSL_ERR_INVALID_ARG, "t_min must be in [0,1)");
+    return NSL_OK;
+}
+
+nsl_status nsl_sixway_bake(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
+                           const nsl_camera* cams, const nsl_medium* med, const nsl_bake* b,
+                           const uint32_t* frame_ids, int32_t F, float* out, uint64_t* counters,
+                           nsl_stream stream) {
+    g_err.clear();
+    if (nsl_status st = check_bake(b)) return st;
+    if (!out) return fail(NSL_ERR_INVALID_ARG, "NULL output");
+    if (reinterpret_cast<uintptr_t>(out) % 16) return fail(NSL_ERR_INVALID_ARG, "out must be 16-B aligned");
+    if (F < 1 || F > 65535) return fail(NSL_ERR_INVALID_ARG, "F must be in [1, 65535]");
+    // the six axis lights are fixed; the march constants carry only the camera/volume part
+    std::vector<nsl_light> dummy((size_t)F, nsl_light{{1.0f, 0.0f, 0.0f}, {1.0f, 1.0f, 1.0f}});
+    nsl_march m{};
+    m.step = b->step;
+    m.light_step = b->light_step;
+    m.max_steps = b->max_steps;
+    m.t_min = b->t_min;
+    m.seed = b->seed;
+    Prepared P;
+    if (nsl_status st = prepare(vols, n_vols, frame_vol, cams, dummy.data(), 1, NSL_LIGHTS_EXPLICIT, med, &m,
+                                frame_ids, F, P))
+        return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Workspace ws;
+    if (nsl_status st = build_frames(P.frames, dummy.data(), 1, P.mc, std::vector<uint32_t>(), s, ws)) return st;
+    BakeFrame* bf = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bf), sizeof(BakeFrame) * F, s);
+    if (e == cudaSuccess) e = launch_bake_setup(ws.in, ws.params, F, b->light_step, med->hg_g, bf, s);
+    if (e == cudaSuccess && counters) e = cudaMemsetAsync(counters, 0, sizeof(uint64_t), s);
+    if (e == cudaSuccess) {
+        BakeConst bc;
+        bc.hb = b->step;
+        bc.hbl = b->light_step;
+        bc.kappa = med->extinction;
+        bc.alpha = med->albedo;
+        bc.g = med->hg_g;
+        bc.t_min = b->t_min;
+        bc.spp = b->spp;
+        bc.Ncap = b->max_steps > 0 ? b->max_steps : (1 << 24);
+        bc.seed_lo = (uint32_t)(b->seed & 0xffffffffu);
+        bc.seed_hi = (uint32_t)(b->seed >> 32);
+        bc.counters = reinterpret_cast<unsigned long long*>(counters);
+        e = launch_bake(ws.params, bf, bc, F, P.W, P.H, P.proj, P.layout, reinterpret_cast<float4*>(out), s);
+    }
+    if (bf) cudaFreeAsync(bf, s);
+    cudaFreeAsync(ws.base, s);
+    if (e != cudaSuccess) return cuda_fail(e, "six-way bake launch");
+    return NSL_OK;
+}
+
+nsl_status nsl_debug_bake_lights(const nsl_grid_desc* g, const nsl_camera* cam, float Lg[6][3], float Ln[6][3],
+                                 nsl_stream stream) {
+    g_err.clear();
+    if (nsl_status st = check_grid(g)) return st;
+    if (!cam || !Lg || !Ln) return fail(NSL_ERR_INVALID_ARG, "NULL camera/output");
+    if (nsl_status st = check_camera(cam, 0)) return st;
+    std::vector<FrameIn> frames(1);
+    memset(frames.data(), 0, sizeof(FrameIn));
+    frames[0].cam = *cam;
+    frames[0].vol.nx = g->nx;
+    frames[0].vol.ny = g->ny;
+    frames[0].vol.nz = g->nz;
+    frames[0].vol.layout = kQuadF32;
+    for (int a = 0; a < 3; ++a) frames[0].vol.origin[a] = g->origin[a];
+    frames[0].vol.dx = g->voxel_width;
+    nsl_light dummy{{1.0f, 0.0f, 0.0f}, {1.0f, 1.0f, 1.0f}};
+    nsl_medium med{0.0f, 1.0f, 0.0f};
+    nsl_march m{};
+    m.step = g->voxel_width;
+    const MarchConst mc = make_const(1, NSL_LIGHTS_EXPLICIT, &med, &m);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Workspace ws;
+    if (nsl_status st = build_frames(frames, &dummy, 1, mc, std::vector<uint32_t>(), s, ws)) return st;
+    BakeFrame* bf = nullptr;
+    BakeFrame h;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bf), sizeof(BakeFrame), s);
+    if (e == cudaSuccess) e = launch_bake_setup(ws.in, ws.params, 1, m.step, 0.0f, bf, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bf, sizeof h, cudaMemcpyDeviceToHost, s);
+    if (bf) cudaFreeAsync(bf, s);
+    cudaFreeAsync(ws.base, s);
+    if (e != cudaSuccess) return cuda_fail(e, "bake light setup");
+    NSL_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    memcpy(Lg, h.Lg, sizeof h.Lg);
+    memcpy(Ln, h.Ln, sizeof h.Ln);
+    return NSL_OK;
+}
+
 nsl_status nsl_debug_frame_constants(const nsl_grid_desc* g, const nsl_camera* cam, const nsl_light* lights,
                                      int32_t n_lights, int32_t light_mode, const nsl_medium* med, const nsl_march* m,
                                      nsl_frame_constants* out, nsl_stream stream) {

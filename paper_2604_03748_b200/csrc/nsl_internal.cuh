@@ -85,6 +85,20 @@ struct MarchConst {
     float axis[3];
 };
 
+// NEXT-1 six-way bake: per-frame light constants and call constants.
+struct BakeFrame {
+    float Lg[6][3], Ln[6][3], P[6];
+    float lim[6][3], ilh[6][3], alim[6][3];
+    int32_t lz0;
+    int32_t pad[3];
+};
+struct BakeConst {
+    float hb, hbl, kappa, alpha, g, t_min;
+    int32_t spp, Ncap;
+    uint32_t seed_lo, seed_hi;
+    unsigned long long* counters;   // NULL or [0] += trilinear gathers executed
+};
+
 // layouts
 constexpr int kLinearF32 = NSL_LAYOUT_LINEAR_F32;
 constexpr int kQuadF32 = NSL_LAYOUT_QUAD_F32;
@@ -102,6 +116,10 @@ cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int
                          unsigned long long* counters, const uint32_t* tile_order, cudaStream_t s);
 int march_tile_w();
 int march_tile_h();
+cudaError_t launch_bake_setup(const FrameIn* in, const FrameParams* fps, int F, float hbl, float g, BakeFrame* out,
+                              cudaStream_t s);
+cudaError_t launch_bake(const FrameParams* fp, const BakeFrame* bf, const BakeConst& bc, int F, int W, int H,
+                        int projection, int layout, float4* out, cudaStream_t s);
 cudaError_t launch_jitter_debug(const MarchConst& mc, uint32_t frame_id, int n, uint32_t* hash, float* delta,
                                 cudaStream_t s);
 

@@ -1,0 +1,374 @@
+// sampler.cuh — device code shared by the march (march.cu) and the six-way bake
+// (bake.cu): build-variant switches, the C1 trilinear sampler with the exact
+// occupancy skip, the C4 hash, ray/slab helpers and the exact C8 light counts.
+// Included inside each translation unit's anonymous namespace usage below.
+#pragma once
+#include <cuda_fp16.h>
+
+#include "nsl_internal.cuh"
+
+namespace nsl {
+namespace {
+
+#ifndef NSL_TILEH
+#define NSL_TILEH 8      // CTA tile 16 x NSL_TILEH pixels (warps of 8x4): 8 -> 128 threads (measured best), 16 -> 256
+#endif
+constexpr int kTileW = 16, kTileH = NSL_TILEH, kThreads = 2 * NSL_TILEH * 8;
+#ifndef NSL_BLOCKIDX
+#define NSL_BLOCKIDX 0   // occupancy block index: 1 exact fp32 FMAs, 0 integer shifts of the cell floor (measured equal, profiles/r1_sweep.txt)
+#endif
+#ifndef NSL_MASKREAD
+#define NSL_MASKREAD 0   // mask word read: 1 ld.shared via a 32-bit address, 0 extern shared array
+#endif
+#ifndef NSL_PAIRWALK
+#define NSL_PAIRWALK 0   // paired top/bottom march: 1 combined chord walk, 0 lock-step both sides (measured better)
+#endif
+#ifndef NSL_STAGE
+#define NSL_STAGE 0      // 1: stage FrameParams + occupancy region in shared memory per CTA; 0: read them
+                         //    through the read-only path from global memory (L1-resident; measured equal or
+                         //    better, no __syncthreads, all of L1 for the volume)
+#endif
+#ifndef NSL_MINB
+#define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
+                     // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)
+#endif
+constexpr int kFast = 0, kDebug = 1, kCounted = 2;
+
+struct Vol {
+    const void* __restrict__ data;
+    const uint32_t* __restrict__ occ;   // occupancy region in global memory (NSL_STAGE == 0)
+    uint32_t mask_sa;             // shared-space byte address of the occupancy mask
+    int sy, sz;
+    float inv_b, nbx_f, nbxy_f;   // 2^-shift, blocks per x row, blocks per z slab (exact in fp32)
+    int shift, nbx, nby;
+    float sx1, sy1, sz1;          // support upper bounds n+1
+};
+
+// Dynamic shared memory of march_kernel: [FrameParams | occupancy mask words].
+// Indexed through this file-scope array so the mask test is one LDS with an
+// immediate offset (no generic->shared address conversion in the loops).
+extern __shared__ __align__(16) uint32_t nsl_smem[];
+#if NSL_STAGE
+constexpr int kMaskWord0 = (int)(sizeof(FrameParams) / 4);
+#endif
+
+__device__ __forceinline__ float lerpf(float a, float b, float t) { return __fmaf_rn(t, b - a, a); }
+
+__device__ __forceinline__ bool inside(const Vol& v, float x, float y, float z) {
+    return x > 0.0f && x < v.sx1 && y > 0.0f && y < v.sy1 && z > 0.0f && z < v.sz1;
+}
+
+// C1 trilinear at an in-support padded-index position (corners always exist
+// thanks to the apron).  floor and fraction are exact in fp32.  Samples in an
+// empty occupancy block return 0 without touching global memory.
+// floor on the FMA pipe: for 0 <= x < 2^22, x + 1.5*2^23 rounded toward -inf is
+// exactly floor(x) + 1.5*2^23 (unit spacing there), so the integer sits in the
+// low mantissa bits and r - 1.5*2^23 is floor(x) exactly.  No F2I/FRND (the
+// quarter-rate XU pipe) per sample.  Positions in support satisfy 0 < x < n+1.
+constexpr float kFloorBias = 12582912.0f;   // 1.5 * 2^23, bit pattern 0x4B400000
+#if NSL_BLOCKIDX == 1
+__device__ __forceinline__ void cellof(float x, int& i, float& frac) {
+    const float r = __fadd_rd(x, kFloorBias);
+    i = __float_as_int(r) - 0x4B400000;
+    frac = __fsub_rn(x, __fsub_rn(r, kFloorBias));
+}
+#endif
+
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
+#if NSL_BLOCKIDX == 1
+    // occupancy block index in exact fp32: floor(x / B) via fma rounded toward -inf
+    // onto the 1.5*2^23 grid (x * 2^-s is exact), then the linear index with two
+    // exact FMAs (every term is an integer < 2^24); the bias stays in the x term.
+    const float bx = __fmaf_rd(x, v.inv_b, kFloorBias);
+    const float by = __fsub_rn(__fmaf_rd(y, v.inv_b, kFloorBias), kFloorBias);
+    const float bz = __fsub_rn(__fmaf_rd(z, v.inv_b, kFloorBias), kFloorBias);
+    const int b = __float_as_int(__fmaf_rn(bz, v.nbxy_f, __fmaf_rn(by, v.nbx_f, bx))) - 0x4B400000;
+#else
+    // cell floors (shared with the gather below), block = cell >> shift
+    const float rx = __fadd_rd(x, kFloorBias), ry = __fadd_rd(y, kFloorBias), rz = __fadd_rd(z, kFloorBias);
+    const int ix = __float_as_int(rx) - 0x4B400000, iy = __float_as_int(ry) - 0x4B400000,
+              iz = __float_as_int(rz) - 0x4B400000;
+    const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
+#endif
+#if NSL_MASKREAD == 1
+    uint32_t word;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(v.mask_sa + ((uint32_t)b >> 5) * 4u));
+#else
+#if NSL_STAGE
+    const uint32_t word = nsl_smem[kMaskWord0 + (b >> 5)];
+#else
+    const uint32_t word = __ldg(v.occ + (b >> 5));
+#endif
+#endif
+    if (!((word >> (b & 31)) & 1u)) return 0.0f;
+    if (COUNT) ++gathers;
+#if NSL_BLOCKIDX == 1
+    int ix, iy, iz;
+    float fx, fy, fz;
+    cellof(x, ix, fx);
+    cellof(y, iy, fy);
+    cellof(z, iz, fz);
+#else
+    const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias)),
+                fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
+#endif
+    const int e = ix + iy * v.sy + iz * v.sz;
+    if (LAYOUT == kLinearF32) {
+        const float* p = static_cast<const float*>(v.data) + e;
+        const float c000 = __ldg(p), c100 = __ldg(p + 1);
+        const float c010 = __ldg(p + v.sy), c110 = __ldg(p + v.sy + 1);
+        const float c001 = __ldg(p + v.sz), c101 = __ldg(p + v.sz + 1);
+        const float c011 = __ldg(p + v.sz + v.sy), c111 = __ldg(p + v.sz + v.sy + 1);
+        const float x00 = lerpf(c000, c100, fx), x10 = lerpf(c010, c110, fx);
+        const float x01 = lerpf(c001, c101, fx), x11 = lerpf(c011, c111, fx);
+        return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
+    } else if (LAYOUT == kQuadF32) {
+        const float4* p = static_cast<const float4*>(v.data) + e;
+        const float4 q0 = __ldg(p), q1 = __ldg(p + v.sz);     // (c0, c1 - c0, c2, c3 - c2)
+        const float x00 = __fmaf_rn(fx, q0.y, q0.x), x10 = __fmaf_rn(fx, q0.w, q0.z);
+        const float x01 = __fmaf_rn(fx, q1.y, q1.x), x11 = __fmaf_rn(fx, q1.w, q1.z);
+        return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
+    } else {
+        const uint4 u = __ldg(static_cast<const uint4*>(v.data) + e);
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+        const float2 bb = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+        const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+        const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+        const float x00 = lerpf(a.x, a.y, fx), x10 = lerpf(bb.x, bb.y, fx);
+        const float x01 = lerpf(c.x, c.y, fx), x11 = lerpf(d.x, d.y, fx);
+        return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
+    }
+}
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+// C4: hash chain keyed by (seed, frame, pixel)
+__device__ __forceinline__ uint32_t jitter_hash(uint32_t seed_lo, uint32_t seed_hi, uint32_t frame, uint32_t pixel) {
+    uint32_t h = fmix32(seed_lo ^ 0x9E3779B9u);
+    h = fmix32(h ^ seed_hi);
+    h = fmix32(h ^ frame);
+    return fmix32(h ^ pixel);
+}
+__device__ __forceinline__ float jitter_delta(uint32_t h32, float h) {
+    const float u = __fmul_rn(__uint2float_rn(h32 >> 8), 5.9604644775390625e-08f);  // exact: 24-bit int * 2^-24
+    return __fmul_rn(u, h);
+}
+
+struct Ray {
+    float ox, oy, oz, dx, dy, dz, delta, h;
+    __device__ __forceinline__ void at(int n, float& t, float& x, float& y, float& z) const {
+        atf((float)n, t, x, y, z);
+    }
+    __device__ __forceinline__ void atf(float nf, float& t, float& x, float& y, float& z) const {
+        t = __fmaf_rn(nf, h, delta);
+        x = __fmaf_rn(t, dx, ox);
+        y = __fmaf_rn(t, dy, oy);
+        z = __fmaf_rn(t, dz, oz);
+    }
+    __device__ __forceinline__ bool in(const Vol& v, int n) const {
+        float t, x, y, z;
+        at(n, t, x, y, z);
+        return inside(v, x, y, z);
+    }
+};
+
+// inv: 1/d (per-frame constant for orthographic cameras, computed per ray otherwise)
+__device__ __forceinline__ void slab(float o, float d, float inv, float s, float eps, float& t0, float& t1,
+                                     bool& miss) {
+    if (d != 0.0f) {
+        float ta = (-eps - o) * inv, tb = (s + eps - o) * inv;
+        if (ta > tb) {
+            const float tt = ta;
+            ta = tb;
+            tb = tt;
+        }
+        t0 = fmaxf(t0, ta);
+        t1 = fminf(t1, tb);
+    } else if (!(o > -eps && o < s + eps)) {
+        miss = true;
+    }
+}
+
+// C5: exact first/last in-support step in [1, Ncap] (0,-1 if none).  A float
+// slab test on the box expanded by 1e-3 index units brackets the range to
+// within one step; exact per-sample tests then shrink it (the in-support set
+// is contiguous because every coordinate is monotone in n).
+__device__ __forceinline__ void clip_ray(const Ray& r, const Vol& v, const float inv[3], float inv_h, int Ncap,
+                                         int& n0, int& n1) {
+    n0 = 0;
+    n1 = -1;
+    const float eps = 1e-3f;
+    float t0 = -3.0e38f, t1 = 3.0e38f;
+    bool miss = false;
+    slab(r.ox, r.dx, inv[0], v.sx1, eps, t0, t1, miss);
+    slab(r.oy, r.dy, inv[1], v.sy1, eps, t0, t1, miss);
+    slab(r.oz, r.dz, inv[2], v.sz1, eps, t0, t1, miss);
+    if (miss || !(t0 <= t1)) return;
+    float a = floorf((t0 - r.delta) * inv_h) - 1.0f, b = ceilf((t1 - r.delta) * inv_h) + 1.0f;
+    a = fmaxf(a, 1.0f);
+    b = fminf(b, (float)Ncap);
+    if (!(a <= b)) return;
+    int na = (int)a, nb = (int)b;
+    while (na <= nb && !r.in(v, na)) ++na;
+    while (nb >= na && !r.in(v, nb)) --nb;
+    if (na > nb) return;
+    n0 = na;
+    n1 = nb;
+}
+
+// C8: M = number of leading in-support light samples Y_j = fma(j*h_l, L, U).
+// lim/ilh: per-frame exit plane and 1/(L*h_l) per axis (FrameParams) -> estimate, then exact fix-up.
+__device__ __forceinline__ int light_count(const Vol& v, float ux, float uy, float uz, float lx, float ly, float lz,
+                                           float hl, const float lim[3], const float ilh[3]) {
+    const float m = fminf(fminf((lim[0] - ux) * ilh[0], (lim[1] - uy) * ilh[1]), (lim[2] - uz) * ilh[2]);
+    const float mf = fminf(fmaxf(floorf(m), 0.0f), 16777216.0f);
+    int M = (int)mf;
+    auto in_j = [&](int j) {
+        const float s = __fmul_rn((float)j, hl);
+        return inside(v, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), __fmaf_rn(s, lz, uz));
+    };
+    while (M > 0 && !in_j(M)) --M;
+    while (in_j(M + 1)) ++M;
+    return M;
+}
+
+// sum of rho over j = 1..M along the light (all in support); two independent
+// accumulators give the scheduler two gathers in flight per thread.
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ float light_sum(const Vol& v, float ux, float uy, float uz, float lx, float ly, float lz,
+                                           float hl, int M, uint32_t& gathers) {
+    float acc0 = 0.0f, acc1 = 0.0f;
+    int j = 1;
+    float jf = 1.0f;   // exact float copy of j (j < 2^24): no I2F in the loop
+    for (; j + 1 <= M; j += 2, jf += 2.0f) {
+        const float s0 = __fmul_rn(jf, hl), s1 = __fmul_rn(jf + 1.0f, hl);
+        acc0 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
+        acc1 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s1, lx, ux), __fmaf_rn(s1, ly, uy), __fmaf_rn(s1, lz, uz), gathers);
+    }
+    if (j <= M) {
+        const float s0 = __fmul_rn(jf, hl);
+        acc0 += sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
+    }
+    return acc0 + acc1;
+}
+
+// The guide set's top and bottom lights are exact opposites (L_g,2 = -L_g,1 bit
+// for bit): both marches walk the same line through U in opposite directions.
+// One loop serves both: s_j is shared and fma(-s, L, U) == fma(s, -L, U) exactly,
+// so the positions are the canonical ones of C8 for each light.
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy, float uz, float lx, float ly,
+                                               float lz, float hl, int Ma, int Mb, float& sa, float& sb,
+                                               uint32_t& gathers) {
+#if NSL_PAIRWALK == 1
+    // Walk the combined chord k = 0 .. Ma+Mb-1 (j = k+1 on the +L side, then j = k-Ma+1
+    // on the -L side) two samples per iteration: no lane idles on the shorter side.
+    // jf carries the sign of the side, so s = jf*h_l = +-fl(j*h_l) exactly.
+    float a = 0.0f, b = 0.0f;
+    const int K = Ma + Mb;
+    const float maf = (float)Ma;
+    float kf = 0.0f;
+    int k = 0;
+    for (; k + 1 < K; k += 2, kf += 2.0f) {
+        const float j0 = kf < maf ? kf + 1.0f : maf - kf - 1.0f;
+        const float j1 = kf + 1.0f < maf ? kf + 2.0f : maf - kf - 2.0f;
+        const float s0 = __fmul_rn(j0, hl), s1 = __fmul_rn(j1, hl);
+        const float r0 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
+        const float r1 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s1, lx, ux), __fmaf_rn(s1, ly, uy), __fmaf_rn(s1, lz, uz), gathers);
+        if (j0 > 0.0f) a += r0; else b += r0;
+        if (j1 > 0.0f) a += r1; else b += r1;
+    }
+    if (k < K) {
+        const float j0 = kf < maf ? kf + 1.0f : maf - kf - 1.0f;
+        const float s0 = __fmul_rn(j0, hl);
+        const float r0 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
+        if (j0 > 0.0f) a += r0; else b += r0;
+    }
+#else
+    float a = 0.0f, b = 0.0f;
+    const int M = max(Ma, Mb);
+    float jf = 1.0f;
+    for (int j = 1; j <= M; ++j, jf += 1.0f) {
+        const float s = __fmul_rn(jf, hl);
+        if (j <= Ma) a += sample<LAYOUT, COUNT>(v, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), __fmaf_rn(s, lz, uz), gathers);
+        if (j <= Mb)
+            b += sample<LAYOUT, COUNT>(v, __fmaf_rn(-s, lx, ux), __fmaf_rn(-s, ly, uy), __fmaf_rn(-s, lz, uz), gathers);
+    }
+#endif
+    sa = a;
+    sb = b;
+}
+
+// Fast-path bound on the light samples that can be nonzero: the estimate of the
+// support count plus one (>= the exact count), capped by the occupied-box
+// count, then shrunk with exact prescribed-op tests until the last sample is in
+// support (so every index is valid).  Every in-support sample inside the
+// occupied box is covered, hence the sum equals the canonical one (C8).
+__device__ __forceinline__ int light_bound(const Vol& v, float ux, float uy, float uz, float lx, float ly, float lz,
+                                           float hl, const float lim[3], const float ilh[3], const float alim[3]) {
+    const float ms = fminf(fminf((lim[0] - ux) * ilh[0], (lim[1] - uy) * ilh[1]), (lim[2] - uz) * ilh[2]);
+    const float mb = fminf(fminf((alim[0] - ux) * ilh[0], (alim[1] - uy) * ilh[1]), (alim[2] - uz) * ilh[2]);
+    float m = fminf(floorf(ms), floorf(mb)) + 1.0f;
+    m = fminf(fmaxf(m, 0.0f), 16777216.0f);
+    while (m > 0.0f) {
+        const float s = __fmul_rn(m, hl);
+        if (inside(v, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), __fmaf_rn(s, lz, uz))) break;
+        m -= 1.0f;
+    }
+    return (int)m;
+}
+
+// Conservative count of leading light samples inside the occupied box (one
+// extra for rounding): samples beyond it are exactly 0 and need not be taken.
+__device__ __forceinline__ int box_count(float ux, float uy, float uz, const float alim[3], const float ilh[3]) {
+    const float m = fminf(fminf((alim[0] - ux) * ilh[0], (alim[1] - uy) * ilh[1]), (alim[2] - uz) * ilh[2]);
+    return (int)fminf(fmaxf(floorf(m), -1.0f), 16777215.0f) + 1;
+}
+
+// Exit planes of the region that can hold nonzero samples of light l's march from
+// height uz: for a horizontal light (L_z == 0 exactly, so every Y_j,z == uz and the
+// march stays in the z block-slab of uz) the slab's 2-D box of non-empty blocks;
+// otherwise the occupied 3-D box.  Either way samples beyond it are exactly 0.
+__device__ __forceinline__ void march_region(const FrameParams& sp, const Vol& v, int l, float uz, float out[3]) {
+    if ((sp.lz0 >> l) & 1) {
+        const int iz = __float_as_int(__fadd_rd(uz, kFloorBias)) - 0x4B400000;
+        const int bz = iz >> v.shift;
+#if NSL_STAGE
+        const int* slab = reinterpret_cast<const int*>(nsl_smem) + kMaskWord0 + sp.slab_off;
+        const int2 mn = *reinterpret_cast<const int2*>(slab + 2 * bz);
+        const int2 mx = *reinterpret_cast<const int2*>(slab + 2 * sp.occ_nbz + 2 * bz);
+#else
+        const int* slab = reinterpret_cast<const int*>(v.occ) + sp.slab_off;
+        const int2 mn = __ldg(reinterpret_cast<const int2*>(slab + 2 * bz));
+        const int2 mx = __ldg(reinterpret_cast<const int2*>(slab + 2 * sp.occ_nbz + 2 * bz));
+#endif
+        const float B = (float)(1 << v.shift);
+        const float lox = (float)mn.x * B, hix = fminf((float)(mx.x + 1) * B, v.sx1);
+        const float loy = (float)mn.y * B, hiy = fminf((float)(mx.y + 1) * B, v.sy1);
+        const float Lx = sp.Lg[l][0], Ly = sp.Lg[l][1];
+        out[0] = Lx > 0.0f ? hix : (Lx < 0.0f ? lox : 3.0e38f);
+        out[1] = Ly > 0.0f ? hiy : (Ly < 0.0f ? loy : 3.0e38f);
+        out[2] = 3.0e38f;
+    } else {
+        out[0] = sp.alim[l][0];
+        out[1] = sp.alim[l][1];
+        out[2] = sp.alim[l][2];
+    }
+}
+
+__device__ __forceinline__ float hg32(float g, float c) {
+    const float d = (1.0f + g * g) - 2.0f * g * c;
+    return (1.0f - g * g) / (12.566370614359172f * d * sqrtf(d));
+}
+
+
+}  // namespace
+}  // namespace nsl
