@@ -281,3 +281,59 @@ def sixway_bake(grid, vals, cam, medium, bake, frame_id: int = 0, pixels=None, d
     if rc:
         raise ValueError("orc_sixway_bake rejected its arguments")
     return {"out": out, "steps": steps, "pixels": np.arange(n, dtype=np.int64) if pix is None else pix}
+
+
+# ------------------------------------------------------------------ NEXT-2/3 relight + shadow
+def _load_relight():
+    L = _load_bake()
+    if not getattr(L, "_relight_ready", False):
+        P = ctypes.POINTER
+        L.orc_relight_weights.argtypes = [P(OrcCamera), P(OrcLight), ctypes.c_int32, ctypes.c_void_p]
+        L.orc_relight.argtypes = [P(OrcCamera), ctypes.c_void_p, ctypes.c_void_p, P(OrcLight), ctypes.c_int32,
+                                  P(ctypes.c_float), P(ctypes.c_float), ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_float, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p]
+        L.orc_relight.restype = ctypes.c_int
+        L._relight_ready = True
+    return L
+
+
+def relight_weights(cam, lights):
+    c = np.zeros((len(lights), 3), np.float32)
+    _load_relight().orc_relight_weights(ctypes.byref(_camera(cam)), _lights(lights), len(lights), c.ctypes.data)
+    return c
+
+
+def relight(cam, maps8, lights, bg=(0.0, 0.0, 0.0), emis=(0.0, 0.0, 0.0), depth=None, shadow_cams=None,
+            shadow_maps=None, bias=2e-3, pixels=None) -> dict:
+    """Oracle of R1-R3.  maps8: float32 [H, W, 8] (Fig. 2 packing); depth: float32 [H, W] or None;
+    shadow_cams / shadow_maps: per light (Camera, float32 [Hs, Ws] or None).  Returns out (n, 4) f64
+    (r, g, b, alpha), margin (n,), pixels."""
+    L = _load_relight()
+    W, H = cam.width, cam.height
+    m = np.ascontiguousarray(maps8, dtype=np.float32).reshape(-1)
+    d = None if depth is None else np.ascontiguousarray(depth, dtype=np.float32).reshape(-1)
+    pix = None if pixels is None else np.ascontiguousarray(np.asarray(pixels, np.int64))
+    n = W * H if pix is None else int(pix.size)
+    out = np.zeros((n, 4), np.float64)
+    margin = np.zeros((n,), np.float64)
+    sc_arr = None
+    sm_ptrs = None
+    keep = []
+    if shadow_cams is not None:
+        sc_arr = (OrcCamera * len(lights))(*[_camera(c) if c is not None else OrcCamera() for c in shadow_cams])
+        sm_ptrs = (ctypes.c_void_p * len(lights))()
+        for i, smap in enumerate(shadow_maps):
+            if smap is not None:
+                a = np.ascontiguousarray(smap, dtype=np.float32)
+                keep.append(a)
+                sm_ptrs[i] = a.ctypes.data
+    f3 = ctypes.c_float * 3
+    rc = L.orc_relight(ctypes.byref(_camera(cam)), m.ctypes.data, None if d is None else d.ctypes.data,
+                       _lights(lights), len(lights), f3(*bg), f3(*emis),
+                       None if sc_arr is None else ctypes.addressof(sc_arr),
+                       None if sm_ptrs is None else ctypes.addressof(sm_ptrs), bias, n,
+                       None if pix is None else pix.ctypes.data, out.ctypes.data, margin.ctypes.data)
+    if rc:
+        raise ValueError("orc_relight rejected its arguments")
+    return {"out": out, "margin": margin, "pixels": np.arange(n, dtype=np.int64) if pix is None else pix}

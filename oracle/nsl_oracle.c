@@ -522,3 +522,101 @@ int orc_sixway_bake(const orc_grid* g, const float* vals, orc_density_fn density
     }
     return 0;
 }
+
+/* ================================================================ NEXT-2/3: relight, composite, shadow
+ * DESIGN.md §11 (R1-R3): directionally weighted interpolation of the six-way
+ * maps, composite (L213-218), depth-based obstacle shadow
+ * (L458-462).  fp64 arithmetic; the shadow test reports its decision margins. */
+
+static void pixel_ray_world(const orc_camera* cam, double px, double py, double o[3], double dir[3]) {
+    double f[3], r[3], u[3];
+    camera_axes(cam, f, r, u);
+    const double W = cam->width, H = cam->height;
+    const double sx = 2.0 * (px + 0.5) / W - 1.0, sy = 1.0 - 2.0 * (py + 0.5) / H;
+    const double ay = 0.5 * cam->extent, ax = ay * W / H;
+    if (cam->projection == 0) {
+        for (int a = 0; a < 3; ++a) {
+            o[a] = cam->position[a] + sx * ax * r[a] + sy * ay * u[a];
+            dir[a] = f[a];
+        }
+    } else {
+        double d[3];
+        for (int a = 0; a < 3; ++a) {
+            o[a] = cam->position[a];
+            d[a] = f[a] + sx * ax * r[a] + sy * ay * u[a];
+        }
+        double nd = norm3(d);
+        for (int a = 0; a < 3; ++a) dir[a] = d[a] / nd;
+    }
+}
+
+/* R1 per-light billboard components c = (n.r, n.u, -n.f), rounded to fp32 */
+int orc_relight_weights(const orc_camera* cam, const orc_light* lights, int32_t n_lights, float c_out[][3]) {
+    if (!cam || !lights || n_lights < 1) return 1;
+    double f[3], r[3], u[3];
+    camera_axes(cam, f, r, u);
+    for (int l = 0; l < n_lights; ++l) {
+        double n[3] = {lights[l].to_light[0], lights[l].to_light[1], lights[l].to_light[2]};
+        double nn = norm3(n);
+        for (int a = 0; a < 3; ++a) n[a] /= nn;
+        c_out[l][0] = (float)dot3(n, r);
+        c_out[l][1] = (float)dot3(n, u);
+        c_out[l][2] = (float)(-dot3(n, f));
+    }
+    return 0;
+}
+
+int orc_relight(const orc_camera* cam, const float* maps8, const float* depth, const orc_light* lights,
+                int32_t n_lights, const float bg[3], const float emis[3], const orc_camera* shadow_cams,
+                const float* const* shadow_maps, float bias, int64_t n_pix, const int64_t* pix, double* out4,
+                double* out_margin) {
+    if (!cam || !maps8 || !lights || n_lights < 1 || n_lights > 4 || !bg || !emis || !out4) return 1;
+    float c[4][3];
+    orc_relight_weights(cam, lights, n_lights, c);
+    const int W = cam->width, H = cam->height;
+    if (!pix) n_pix = (int64_t)W * H;
+    for (int64_t q = 0; q < n_pix; ++q) {
+        const int64_t p = pix ? pix[q] : q;
+        const float* m = maps8 + 8 * p;
+        /* Fig. 2 packing: m0 right(+x) m1 top(+y) m2 back(-z) m3 T | m4 left(-x) m5 bottom(-y) m6 front(+z) m7 E */
+        const double Lpos[3] = {m[0], m[1], m[6]}, Lneg[3] = {m[4], m[5], m[2]};
+        const double T = m[3], E = m[7];
+        double out[3] = {0, 0, 0};
+        double margin = INFINITY;
+        for (int l = 0; l < n_lights; ++l) {
+            double S = 0.0;
+            for (int a = 0; a < 3; ++a) {
+                if (c[l][a] > 0.0f) S += (double)c[l][a] * Lpos[a];
+                else if (c[l][a] < 0.0f) S += (double)(-c[l][a]) * Lneg[a];
+            }
+            double v = 1.0;
+            if (shadow_cams && shadow_maps && shadow_maps[l] && depth && depth[p] > 0.0f) {
+                const orc_camera* sc = &shadow_cams[l];
+                double o[3], dir[3], pt[3];
+                pixel_ray_world(cam, (double)(p % W), (double)(p / W), o, dir);
+                for (int a = 0; a < 3; ++a) pt[a] = o[a] + (double)depth[p] * dir[a];
+                double sf[3], sr[3], su[3];
+                camera_axes(sc, sf, sr, su);
+                double d[3] = {pt[0] - sc->position[0], pt[1] - sc->position[1], pt[2] - sc->position[2]};
+                const double say = 0.5 * sc->extent, sax = say * sc->width / sc->height;
+                const double a_ = dot3(d, sr) / sax, b_ = dot3(d, su) / say, z = dot3(d, sf);
+                const double fi = (a_ + 1.0) * sc->width / 2.0, fj = (1.0 - b_) * sc->height / 2.0;
+                const double i = floor(fi), j = floor(fj);
+                double mg = fmin(fmin(fi - i, 1.0 - (fi - i)), fmin(fj - j, 1.0 - (fj - j)));
+                if (i >= 0 && j >= 0 && i < sc->width && j < sc->height) {
+                    const double zs = (double)shadow_maps[l][(size_t)j * sc->width + (size_t)i];
+                    if (isfinite(zs)) {
+                        mg = fmin(mg, fabs(zs + (double)bias - z) / fmax(fabs(z), 1.0));
+                        if (zs + (double)bias < z) v = 0.0;
+                    }
+                }
+                if (mg < margin) margin = mg;
+            }
+            for (int k = 0; k < 3; ++k) out[k] += (double)lights[l].rgb[k] * v * S;
+        }
+        for (int k = 0; k < 3; ++k) out4[4 * q + k] = out[k] + (double)emis[k] * E + T * (double)bg[k];
+        out4[4 * q + 3] = 1.0 - T;
+        if (out_margin) out_margin[q] = margin;
+    }
+    return 0;
+}

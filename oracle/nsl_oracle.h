@@ -108,6 +108,17 @@ int orc_sixway_bake(const orc_grid* g, const float* vals, orc_density_fn density
                     const orc_camera* cam, const orc_medium* med, const orc_bake* b, uint32_t frame_id,
                     int64_t n_pix, const int64_t* pix, double* out8, uint32_t* out_steps);
 
+/* NEXT-2/3 relight + composite + depth shadow (R1-R3).
+ * maps8: W*H*8 floats (Fig. 2 packing), depth: W*H floats or NULL; shadow_cams /
+ * shadow_maps: NULL or per light (a NULL map = no shadow for that light);
+ * out4: n_pix x 4 doubles (r, g, b, alpha); out_margin: NULL or n_pix doubles
+ * (smallest shadow decision margin: pixel-boundary distance / relative depth gap). */
+int orc_relight_weights(const orc_camera* cam, const orc_light* lights, int32_t n_lights, float c_out[][3]);
+int orc_relight(const orc_camera* cam, const float* maps8, const float* depth, const orc_light* lights,
+                int32_t n_lights, const float bg[3], const float emis[3], const orc_camera* shadow_cams,
+                const float* const* shadow_maps, float bias, int64_t n_pix, const int64_t* pix, double* out4,
+                double* out_margin);
+
 #ifdef __cplusplus
 }
 #endif
