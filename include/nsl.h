@@ -241,6 +241,24 @@ nsl_status nsl_sixway_bake(const nsl_volume* const* vols, int32_t n_vols, const 
 nsl_status nsl_debug_bake_lights(const nsl_grid_desc* g, const nsl_camera* cam, float Lg[6][3], float Ln[6][3],
                                  nsl_stream stream);
 
+/* ------------------------------------------------------------------ NEXT-2/3: relight + shadow
+ * Six-way relighting, composite and depth-based obstacle shadow (DESIGN.md
+ * §11, R1-R3): per pixel out = sum_l rgb_l * v_l * sum_p |c_p| L_p^sign(c_p)
+ * + emis * E + T * bg, alpha = 1 - T (Fig. 2 packing),
+ * with v_l the shadow visibility of the smoke shell (guiding-map depth D)
+ * against light l's orthographic shadow map (L458-462).
+ *   cams[F] (same W, H); maps: device F*H*W*8 floats (Fig. 2 packing);
+ *   depth: device F*H*W floats or NULL (no shadows); lights[F*n_lights]
+ *   (1..4, unit to_light); bg[3], emis[3] host; shadow_cams: host F*n_lights
+ *   cameras (projection 0, looking along -to_light) or NULL; shadow_maps:
+ *   host array of F*n_lights DEVICE pointers (Hs*Ws floats, world depth along
+ *   the shadow camera's forward, +inf = empty) with NULL entries allowed, or
+ *   NULL; bias >= 0.  out: device F*H*W float4 (r, g, b, alpha). */
+nsl_status nsl_relight(const nsl_camera* cams, int32_t F, const float* maps, const float* depth,
+                       const nsl_light* lights, int32_t n_lights, const float bg[3], const float emis[3],
+                       const nsl_camera* shadow_cams, const float* const* shadow_maps, float bias,
+                       float* out, nsl_stream stream);
+
 /* End-to-end convenience call with HOST buffers: uploads the host density
  * grid, lays it out, marches the F frames and copies the results back into
  * host out_rgbt (F*H*W*4 floats) / out_depth (F*H*W floats); synchronises

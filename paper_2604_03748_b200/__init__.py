@@ -18,7 +18,8 @@ from typing import List, Optional, Sequence
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.environ.get("NSL_LIB") or os.path.join(_HERE, "lib", "libnsl.so")   # NSL_LIB: build variants
-CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu", "bake.cu")]
+CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu", "bake.cu",
+                                                  "runtime.cu")]
 HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_HERE, "csrc", "sampler.cuh"),
            os.path.join(_ROOT, "include", "nsl.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -82,7 +83,7 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_batch_counted",
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
-           "nsl_sixway_bake", "nsl_debug_bake_lights"]
+           "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight"]
 
 
 class BakeS(ctypes.Structure):
@@ -128,6 +129,8 @@ def lib():
     L.nsl_debug_jitter.argtypes = [P(MarchS), u32, i32, vp, vp, vp]
     L.nsl_sixway_bake.argtypes = [P(vp), i32, P(i32), P(CameraS), P(MediumS), P(BakeS), P(u32), i32, vp, vp, vp]
     L.nsl_debug_bake_lights.argtypes = [P(GridDesc), P(CameraS), vp, vp, vp]
+    L.nsl_relight.argtypes = [P(CameraS), i32, vp, vp, P(LightS), i32, P(ctypes.c_float), P(ctypes.c_float),
+                              vp, vp, ctypes.c_float, vp, vp]
     for name in EXPORTS[2:]:
         if name != "nsl_volume_bytes":
             getattr(L, name).restype = ctypes.c_int
@@ -352,6 +355,41 @@ def debug_bake_lights(grid, cam, stream=None):
     _check(lib().nsl_debug_bake_lights(ctypes.byref(grid_desc(grid)), ctypes.byref(camera_s(cam)), Lg.ctypes.data,
                                        Ln.ctypes.data, _stream_handle(stream)), "nsl_debug_bake_lights")
     return Lg, Ln
+
+
+def relight(cams, maps, lights, out, depth=None, bg=(0.0, 0.0, 0.0), emis=(0.0, 0.0, 0.0), shadow_cams=None,
+            shadow_maps=None, bias: float = 2e-3, stream=None):
+    """NEXT-2/3 relight + composite + depth shadow.  maps: cuda float32 [F,H,W,2,4]
+    (Fig. 2 packing); depth: cuda [F,H,W] or None; lights: F rows of n lights; shadow_cams /
+    shadow_maps: F rows of n entries (Camera / cuda float32 [Hs,Ws] or None).  out: cuda [F,H,W,4]."""
+    RelightCall(cams, maps, lights, out, depth, bg, emis, shadow_cams, shadow_maps, bias)(stream)
+
+
+class RelightCall:
+    """nsl_relight with its arguments marshalled once (for repeated launches on the same
+    buffers, e.g. per-frame relighting of a resident batch); ``call(stream)`` launches."""
+
+    def __init__(self, cams, maps, lights, out, depth=None, bg=(0.0, 0.0, 0.0), emis=(0.0, 0.0, 0.0),
+                 shadow_cams=None, shadow_maps=None, bias: float = 2e-3):
+        F = len(cams)
+        n = len(lights[0])
+        f3 = ctypes.c_float * 3
+        self._keep = [maps, depth, out, shadow_maps]
+        self.cs = (CameraS * F)(*[camera_s(c) for c in cams])
+        self.ls = lights_s(lights)
+        self.bg, self.emis = f3(*bg), f3(*emis)
+        self.sc = self.sm = None
+        if shadow_maps is not None:
+            self.sc = (CameraS * (F * n))(*[camera_s(c) if c is not None else CameraS()
+                                            for row in shadow_cams for c in row])
+            self.sm = (ctypes.c_void_p * (F * n))(*[None if t is None else t.data_ptr()
+                                                    for row in shadow_maps for t in row])
+        self.args = (self.cs, F, _ptr(maps), _ptr(depth), self.ls, n, self.bg, self.emis,
+                     None if self.sc is None else ctypes.addressof(self.sc),
+                     None if self.sm is None else ctypes.addressof(self.sm), bias, _ptr(out))
+
+    def __call__(self, stream=None):
+        _check(lib().nsl_relight(*self.args, _stream_handle(stream)), "nsl_relight")
 
 
 def run_bake(w, bake, layout: int = LAYOUT_DEFAULT, vols=None, out=None, stream=None):

@@ -612,6 +612,70 @@ nsl_status nsl_sixway_bake(const nsl_volume* const* vols, int32_t n_vols, const 
     return NSL_OK;
 }
 
+nsl_status nsl_relight(const nsl_camera* cams, int32_t F, const float* maps, const float* depth,
+                       const nsl_light* lights, int32_t n_lights, const float bg[3], const float emis[3],
+                       const nsl_camera* shadow_cams, const float* const* shadow_maps, float bias,
+                       float* out, nsl_stream stream) {
+    g_err.clear();
+    if (F < 1 || F > (1 << 20)) return fail(NSL_ERR_INVALID_ARG, "F out of range");
+    if (!cams || !maps || !lights || !bg || !emis || !out) return fail(NSL_ERR_INVALID_ARG, "NULL argument");
+    if (n_lights < 1 || n_lights > 4) return fail(NSL_ERR_INVALID_ARG, "n_lights must be in [1,4]");
+    if (reinterpret_cast<uintptr_t>(maps) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+        return fail(NSL_ERR_INVALID_ARG, "maps/out must be 16-B aligned");
+    if (!(bias >= 0.0f) || !std::isfinite(bias)) return fail(NSL_ERR_INVALID_ARG, "bias must be finite and >= 0");
+    if (!finite3(bg) || !finite3(emis)) return fail(NSL_ERR_INVALID_ARG, "bg/emis must be finite");
+    const int W = cams[0].width, H = cams[0].height;
+    std::vector<RelightIn> in((size_t)F);
+    bool any_shadow = false;
+    for (int f = 0; f < F; ++f) {
+        if (nsl_status st = check_camera(&cams[f], f)) return st;
+        if (cams[f].width != W || cams[f].height != H) return fail(NSL_ERR_INVALID_ARG, "camera[%d]: size differs", f);
+        if (nsl_status st = check_lights(lights + (size_t)f * n_lights, n_lights, NSL_LIGHTS_EXPLICIT, f)) return st;
+        RelightIn& ri = in[f];
+        memset(&ri, 0, sizeof ri);
+        ri.cam = cams[f];
+        for (int l = 0; l < n_lights; ++l) {
+            ri.lights[l] = lights[(size_t)f * n_lights + l];
+            const float* sm = shadow_maps ? shadow_maps[(size_t)f * n_lights + l] : nullptr;
+            if (sm) {
+                if (!depth) return fail(NSL_ERR_INVALID_ARG, "shadow maps need the depth map");
+                if (!shadow_cams) return fail(NSL_ERR_INVALID_ARG, "shadow maps need shadow cameras");
+                const nsl_camera& sc = shadow_cams[(size_t)f * n_lights + l];
+                if (nsl_status st = check_camera(&sc, f)) return st;
+                if (sc.projection != 0) return fail(NSL_ERR_UNSUPPORTED, "shadow cameras must be orthographic");
+                ri.shadow_cam[l] = sc;
+                ri.shadow_map[l] = sm;
+                any_shadow = true;
+            }
+        }
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    retain_pool_once();
+    void* ws = nullptr;
+    const size_t b_in = align_up(sizeof(RelightIn) * F, 256);
+    NSL_CUDA(cudaMallocAsync(&ws, b_in + sizeof(RelightFrame) * F, s), "cudaMallocAsync(relight tables)");
+    cudaError_t e = cudaMemcpyAsync(ws, in.data(), sizeof(RelightIn) * F, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        RelightConst rc;
+        rc.F = F;
+        rc.W = W;
+        rc.H = H;
+        rc.n_lights = n_lights;
+        rc.any_shadow = any_shadow ? 1 : 0;
+        rc.bias = bias;
+        for (int a = 0; a < 3; ++a) {
+            rc.bg[a] = bg[a];
+            rc.emis[a] = emis[a];
+        }
+        e = launch_relight(static_cast<const RelightIn*>(ws), F, n_lights,
+                           reinterpret_cast<RelightFrame*>(static_cast<char*>(ws) + b_in), rc,
+                           reinterpret_cast<const float4*>(maps), depth, reinterpret_cast<float4*>(out), s);
+    }
+    cudaFreeAsync(ws, s);
+    if (e != cudaSuccess) return cuda_fail(e, "relight launch");
+    return NSL_OK;
+}
+
 nsl_status nsl_debug_bake_lights(const nsl_grid_desc* g, const nsl_camera* cam, float Lg[6][3], float Ln[6][3],
                                  nsl_stream stream) {
     g_err.clear();

@@ -99,6 +99,37 @@ struct BakeConst {
     unsigned long long* counters;   // NULL or [0] += trilinear gathers executed
 };
 
+// NEXT-2/3 relight + composite + depth shadow
+struct RelightIn {                  // raw per-frame input
+    nsl_camera cam;
+    nsl_light lights[4];
+    nsl_camera shadow_cam[4];
+    const float* shadow_map[4];     // device, or NULL (no shadow for that light)
+};
+// Per-frame constants (fp64 -> fp32 once, by relight_setup_kernel).  Channels ch of a pixel:
+// 0 right(+x) 1 top(+y) 2 back(-z) 3 T | 4 left(-x) 5 bottom(-y) 6 front(+z) 7 E (Fig. 2).
+struct RelightShadowed {            // a light with a shadow map
+    float w[8];                     // R1 weights |c_p| on the selected channels (0 on 3, 7)
+    float rgb[3];
+    float q[3][4];                  // fi, fj, z = q0 + px q1 + py q2 + D q3 (ortho view), or
+    float g[3][3];                  //           = q0 + D (dir . g)            (persp view)
+    int32_t Ws, Hs;
+    const float* map;
+};
+struct RelightFrame {
+    float M[3][8];                  // unshadowed lights (R1+R2) + composite (bg on ch 3, emis on ch 7)
+    float W0[3], Ex[3], Ey[3], F0[3];   // pixel ray (ortho origin / persp direction of pixel (0,0))
+    int32_t ns, projection;         // number of shadowed lights
+    RelightShadowed sl[4];
+};
+struct RelightConst {
+    int32_t F, W, H, n_lights, any_shadow;
+    float bias;
+    float bg[3], emis[3];
+};
+cudaError_t launch_relight(const RelightIn* in, int F, int n_lights, RelightFrame* frames, const RelightConst& rc,
+                           const float4* maps, const float* depth, float4* out, cudaStream_t s);
+
 // layouts
 constexpr int kLinearF32 = NSL_LAYOUT_LINEAR_F32;
 constexpr int kQuadF32 = NSL_LAYOUT_QUAD_F32;
