@@ -62,10 +62,13 @@ size_t body_bytes(const nsl_grid_desc* g, int layout) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// storage = [layout body | occupancy mask | tail counter], each 256-B aligned
+// storage = [layout body | occupancy region | build scratch | tail counter], each 256-B aligned
 size_t mask_offset(const nsl_grid_desc* g, int layout) { return align_up(body_bytes(g, layout), 256); }
-size_t tail_offset(const nsl_grid_desc* g, int layout) {
+size_t scratch_offset(const nsl_grid_desc* g, int layout) {
     return mask_offset(g, layout) + align_up((size_t)occ_geom(g->nx, g->ny, g->nz).words_total * 4, 256);
+}
+size_t tail_offset(const nsl_grid_desc* g, int layout) {
+    return scratch_offset(g, layout) + align_up((size_t)occ_geom(g->nx, g->ny, g->nz).scratch_words * 4, 256);
 }
 
 nsl_status check_grid(const nsl_grid_desc* g) {
@@ -287,8 +290,7 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     v->og = occ_geom(g->nx, g->ny, g->nz);
     v->aabb = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(v->invalid) + 16);
     auto bail = [&](nsl_status st) { delete v; return st; };
-    cudaError_t e = cudaMemsetAsync(v->invalid, 0, sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemsetAsync"));
+    cudaError_t e = cudaSuccess;
     const float* raw = density;
     void* staging = nullptr;
     if (!density_on_device) {
@@ -299,10 +301,10 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
         if (e != cudaSuccess) return bail(cuda_fail(e, "density upload"));
         raw = static_cast<const float*>(staging);
     }
-    e = launch_layout(raw, desc_of(v), device_storage, v->invalid, s);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "layout kernel launch"));
-    e = launch_occupancy(raw, desc_of(v), v->occ, v->aabb, s);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "occupancy kernel launch"));
+    e = launch_volume_build(raw, desc_of(v), device_storage,
+                            reinterpret_cast<uint32_t*>(static_cast<char*>(device_storage) + scratch_offset(g, layout)),
+                            v->invalid, s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "volume build launch"));
     if (staging) {
         e = cudaFreeAsync(staging, s);
         if (e != cudaSuccess) return bail(cuda_fail(e, "cudaFreeAsync(staging)"));

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
     const int f = (int)(blockIdx.x % (unsigned)F);
     const uint32_t tile = __ldg(tile_order + blockIdx.x / (unsigned)F);
     const int tx = (int)(tile & 0xffffu), ty = (int)(tile >> 16);
+    pdl_wait();                        // launched with PDL after frame_setup_kernel: its FrameParams
 #if NSL_STAGE
     {
         const uint4* src = reinterpret_cast<const uint4*>(fps + f);
@@ -359,8 +360,7 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k<<<grid, kThreads, smem, s>>>(fp, mc, rgbt, depth, debug, counters, W, H, tile_order, F);
-    return cudaGetLastError();
+    return launch_pdl(k, grid, dim3(kThreads), smem, s, fp, mc, rgbt, depth, debug, counters, W, H, tile_order, F);
 }
 
 template <int LAYOUT, int PROJ>

@@ -17,6 +17,9 @@ struct OccGeom {
     int32_t shift, nbx, nby, nbz;
     int32_t words;             // ceil(nbx*nby*nbz / 32), padded to a multiple of 4
     int32_t words_total;       // mask + per-slab boxes: words + 4*nbz (a multiple of 4)
+    int32_t rowwords, rows;    // build scratch: per block row (by, bz) ceil(nbx/32) flag words, then
+    int32_t info_off;          // at word info_off (a multiple of 4) a 4-word record per row
+    int32_t scratch_words;     // (min bx, max bx, invalid voxels, -)
 };
 // Occupancy region (device, staged to shared memory by the march):
 //   [mask: words u32][slab_min: nbz x (bx, by) int32][slab_max: nbz x (bx, by) int32]
@@ -130,15 +133,38 @@ struct RelightConst {
 cudaError_t launch_relight(const RelightIn* in, int F, int n_lights, RelightFrame* frames, const RelightConst& rc,
                            const float4* maps, const float* depth, float4* out, cudaStream_t s);
 
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while
+// its predecessor in the stream runs, once every CTA of the predecessor has called
+// pdl_trigger(); it must call pdl_wait() (full completion + visibility of the predecessor)
+// before touching anything the predecessor writes.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();            // NSL_PDL=0 disables the attribute (A/B measurement)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // layouts
 constexpr int kLinearF32 = NSL_LAYOUT_LINEAR_F32;
 constexpr int kQuadF32 = NSL_LAYOUT_QUAD_F32;
 constexpr int kCornerF16 = NSL_LAYOUT_CORNER_F16;
 
 // Launch helpers implemented in the .cu files.
-cudaError_t launch_layout(const float* raw, const VolDesc& v, void* storage, unsigned long long* invalid,
-                          cudaStream_t s);
-cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, int32_t* aabb, cudaStream_t s);
+// layout + occupancy + AABB + invalid-voxel count from the raw grid (two launches, no memsets)
+cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storage, uint32_t* scratch,
+                                unsigned long long* invalid, cudaStream_t s);
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s);
 // mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path

@@ -38,8 +38,12 @@ __device__ __forceinline__ double hg64(double g, double c) {
 
 __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_light* __restrict__ lights, int F,
                                    MarchConst mc, FrameParams* __restrict__ out) {
+    pdl_trigger();                     // the march (PDL) may launch now; it waits for this grid
     int fi = blockIdx.x * blockDim.x + threadIdx.x;
-    if (fi >= F) return;
+    if (fi >= F) {
+        pdl_wait();
+        return;
+    }
     const FrameIn& fr = in[fi];
     const nsl_camera& cam = fr.cam;
     FrameParams p;
@@ -173,6 +177,7 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
     for (int q = 0; q < 3; ++q) pair = pair && (p.Lg[2][q] == -p.Lg[1][q]);
     p.pair12 = pair ? 1 : 0;
     // occupied box in padded-index positions: cells [bmin*B, (bmax+1)*B) -> U in [lo, hi), clipped to the support
+    pdl_wait();                        // launched with PDL after the volume build: the AABB is its output
     if (fr.vol.aabb) {
         const int B = 1 << fr.vol.og.shift;
         for (int q = 0; q < 3; ++q) {
@@ -208,8 +213,7 @@ cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F
                                FrameParams* out, cudaStream_t s) {
     int threads = 64;
     int blocks = (F + threads - 1) / threads;
-    frame_setup_kernel<<<blocks, threads, 0, s>>>(in, lights, F, mc, out);
-    return cudaGetLastError();
+    return launch_pdl(frame_setup_kernel, dim3(blocks), dim3(threads), 0, s, in, lights, F, mc, out);
 }
 
 }  // namespace nsl

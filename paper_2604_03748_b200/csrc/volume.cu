@@ -43,48 +43,57 @@ struct Raw {
     }
 };
 
-__device__ __forceinline__ void check(float x, unsigned long long* invalid) {
-    if (!(x >= 0.0f) || isinf(x)) atomicAdd(invalid, 1ull);
+// ---------------------------------------------------------------- layout role (one CTA = 256
+// consecutive elements of one padded z-plane, i fastest; 32-bit index arithmetic)
+__device__ __forceinline__ void layout_linear_cta(const Raw& r, float* __restrict__ out, int pb, int kb, int kstep) {
+    const int px = r.nx + 2, py = r.ny + 2, plane = px * py;
+    const int e2 = pb * 256 + threadIdx.x;
+    if (e2 >= plane) return;
+    const int i = e2 % px, j = e2 / px;
+    for (int k = kb; k < r.nz + 2; k += kstep) out[(size_t)k * plane + e2] = r.at(i, j, k);
 }
 
-__global__ void layout_linear_kernel(Raw r, float* __restrict__ out, unsigned long long* invalid, size_t total) {
-    const int px = r.nx + 2, py = r.ny + 2;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-        int i = (int)(e % px);
-        size_t rest = e / px;
-        int j = (int)(rest % py), k = (int)(rest / py);
-        float x = r.at(i, j, k);
-        if (i >= 1 && j >= 1 && k >= 1 && i <= r.nx && j <= r.ny && k <= r.nz) check(x, invalid);
-        out[e] = x;
+// QUAD: each thread writes kQuadPlanes planes (k, k + kstep, ...) with all raw loads issued
+// before the stores (more bytes in flight per thread; HBM-bound).
+constexpr int kQuadPlanes = 2;
+__device__ __forceinline__ void layout_quad_cta(const Raw& r, float4* __restrict__ out, int pb, int kb, int kstep) {
+    const int qx = r.nx + 1, qy = r.ny + 1, plane = qx * qy;
+    const int e2 = pb * 256 + threadIdx.x;
+    if (e2 >= plane) return;
+    const int i = e2 % qx, j = e2 / qx;
+    for (; kb < r.nz + 2; kb += kstep * kQuadPlanes) {
+        float c[kQuadPlanes][4];
+#pragma unroll
+        for (int t = 0; t < kQuadPlanes; ++t) {
+            const int k = kb + t * kstep;
+            c[t][0] = r.at(i, j, k);
+            c[t][1] = r.at(i + 1, j, k);
+            c[t][2] = r.at(i, j + 1, k);
+            c[t][3] = r.at(i + 1, j + 1, k);
+        }
+#pragma unroll
+        for (int t = 0; t < kQuadPlanes; ++t) {
+            const int k = kb + t * kstep;
+            if (k >= r.nz + 2) break;
+            // (c000, c100 - c000, c010, c110 - c010): the x-lerps of the march become one
+            // FMA each, fma(fx, c100 - c000, c000), with the difference rounded exactly as
+            // the kernel's own lerp would round it (bit-identical to the LINEAR layout)
+            out[(size_t)k * plane + e2] =
+                make_float4(c[t][0], __fsub_rn(c[t][1], c[t][0]), c[t][2], __fsub_rn(c[t][3], c[t][2]));
+        }
     }
 }
 
-__global__ void layout_quad_kernel(Raw r, float4* __restrict__ out, unsigned long long* invalid, size_t total) {
-    const int qx = r.nx + 1, qy = r.ny + 1;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-        int i = (int)(e % qx);
-        size_t rest = e / qx;
-        int j = (int)(rest % qy), k = (int)(rest / qy);
-        // (c000, c100 - c000, c010, c110 - c010): the x-lerps of the march become one
-        // FMA each, fma(fx, c100 - c000, c000), with the difference rounded exactly as
-        // the kernel's own lerp would round it (bit-identical to the LINEAR layout)
-        const float c000 = r.at(i, j, k), c100 = r.at(i + 1, j, k);
-        const float c010 = r.at(i, j + 1, k), c110 = r.at(i + 1, j + 1, k);
-        if (i >= 1 && j >= 1 && k >= 1 && k <= r.nz) check(c000, invalid);
-        out[e] = make_float4(c000, __fsub_rn(c100, c000), c010, __fsub_rn(c110, c010));
-    }
-}
-
-__global__ void layout_corner_f16_kernel(Raw r, uint4* __restrict__ out, unsigned long long* invalid, size_t total) {
-    const int qx = r.nx + 1, qy = r.ny + 1;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-        int i = (int)(e % qx);
-        size_t rest = e / qx;
-        int j = (int)(rest % qy), k = (int)(rest / qy);
+__device__ __forceinline__ void layout_corner_f16_cta(const Raw& r, uint4* __restrict__ out, int pb, int kb,
+                                                      int kstep) {
+    const int qx = r.nx + 1, qy = r.ny + 1, plane = qx * qy;
+    const int e2 = pb * 256 + threadIdx.x;
+    if (e2 >= plane) return;
+    const int i = e2 % qx, j = e2 / qx;
+    for (int k = kb; k < r.nz + 1; k += kstep) {
         float c[8];
 #pragma unroll
         for (int b = 0; b < 8; ++b) c[b] = r.at(i + (b & 1), j + ((b >> 1) & 1), k + (b >> 2));
-        if (i >= 1 && j >= 1 && k >= 1) check(c[0], invalid);
         __half2 h0 = __floats2half2_rn(c[0], c[1]), h1 = __floats2half2_rn(c[2], c[3]);
         __half2 h2 = __floats2half2_rn(c[4], c[5]), h3 = __floats2half2_rn(c[6], c[7]);
         uint4 u;
@@ -92,44 +101,205 @@ __global__ void layout_corner_f16_kernel(Raw r, uint4* __restrict__ out, unsigne
         u.y = *reinterpret_cast<unsigned*>(&h1);
         u.z = *reinterpret_cast<unsigned*>(&h2);
         u.w = *reinterpret_cast<unsigned*>(&h3);
-        out[e] = u;
+        out[(size_t)k * plane + e2] = u;
     }
 }
 
-// One thread per occupancy block: the block is non-empty iff some padded
-// voxel in [b*B, b*B + B]^3 (the corners of its cells) is nonzero.
-__global__ void occupancy_kernel(Raw r, uint32_t* __restrict__ mask, OccGeom g, int32_t* __restrict__ aabb) {
-    const int B = 1 << g.shift;
-    const int total = g.nbx * g.nby * g.nbz;
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < total; b += gridDim.x * blockDim.x) {
-        const int bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
-        const int x0 = max(bx * B, 1), x1 = min(bx * B + B, r.nx);
-        const int y0 = max(by * B, 1), y1 = min(by * B + B, r.ny);
-        const int z0 = max(bz * B, 1), z1 = min(bz * B + B, r.nz);
-        bool any = false;
-        for (int k = z0; k <= z1 && !any; ++k)
-            for (int j = y0; j <= y1 && !any; ++j)
-                for (int i = x0; i <= x1; ++i)
-                    if (r.at(i, j, k) != 0.0f) {
-                        any = true;
-                        break;
+// ---------------------------------------------------------------- occupancy role
+// Block (bx, by, bz) is non-empty iff some padded voxel in [b*B, b*B + B]^3 (the corners of
+// its cells) is nonzero; voxel i is a corner of the cells i-1 and i, i.e. of the blocks
+// (i-1)>>s and i>>s.  One CTA per block row (by, bz): its warps stream the (B+1)^2 raw
+// x-rows of the row (coalesced, kOccChunks x 32 voxels in flight per warp, one ballot per
+// 32), OR the x-block flags into shared memory and write them, with the row's x extent and
+// its count of invalid voxels (the rows j in [by B, by B + B), k in [bz B, bz B + B) only, so
+// each voxel is counted once), to the row's scratch record: plain stores, no atomics, no
+// initialisation.  occ_finalize_kernel assembles mask, slab boxes, AABB and the count.
+constexpr int kOccChunks = 4;   // 32-voxel chunks per row loaded at once
+constexpr int kOccRows = 2;     // rows per warp loaded at once
+__device__ __forceinline__ void occupancy_cta(const Raw& r, const OccGeom& g, uint32_t* __restrict__ scratch,
+                                              int row_id, uint32_t* xflag, int* red) {
+    const int s = g.shift, B = 1 << s;
+    const int by = row_id % g.nby, bz = row_id / g.nby;
+    for (int w = threadIdx.x; w < g.rowwords; w += blockDim.x) xflag[w] = 0u;
+    if (threadIdx.x == 0) {
+        red[0] = 0x7fffffff;
+        red[1] = -1;
+        red[2] = 0;
+    }
+    __syncthreads();
+    const int j0 = max(by * B, 1), j1 = min(by * B + B, r.ny);
+    const int k0 = max(bz * B, 1), k1 = min(bz * B + B, r.nz);
+    const int nj = j1 - j0 + 1, nrows = nj > 0 && k1 >= k0 ? nj * (k1 - k0 + 1) : 0;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+    int bad = 0;
+    for (int row0 = warp; row0 < nrows; row0 += nwarps * kOccRows) {
+        // kOccRows rows x kOccChunks chunks of 32 voxels: all loads in flight together
+        float x[kOccRows][kOccChunks];
+#pragma unroll
+        for (int q = 0; q < kOccRows; ++q) {
+            const int row = row0 + q * nwarps;
+            const int j = j0 + row % nj, k = k0 + row / nj;
+            const float* src = r.v + ((size_t)(k - 1) * r.ny + (j - 1)) * r.nx;
+#pragma unroll
+            for (int t = 0; t < kOccChunks; ++t) {
+                const int i = 1 + 32 * t + lane;
+                x[q][t] = row < nrows && i <= r.nx ? __ldg(src + (i - 1)) : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kOccRows; ++q) {
+            const int row = row0 + q * nwarps;
+            if (row >= nrows) break;
+            const int j = j0 + row % nj, k = k0 + row / nj;
+            const bool counted = j < by * B + B && k < bz * B + B;
+            const float* src = r.v + ((size_t)(k - 1) * r.ny + (j - 1)) * r.nx;
+            for (int g0 = 1; g0 <= r.nx; g0 += 32 * kOccChunks) {
+                float xv[kOccChunks];
+#pragma unroll
+                for (int t = 0; t < kOccChunks; ++t) {
+                    const int i = g0 + 32 * t + lane;
+                    xv[t] = g0 == 1 ? x[q][t] : (i <= r.nx ? __ldg(src + (i - 1)) : 0.0f);
+                }
+#pragma unroll
+                for (int t = 0; t < kOccChunks; ++t) {
+                    const int c0 = g0 + 32 * t, i = c0 + lane;
+                    bad += counted && i <= r.nx && (!(xv[t] >= 0.0f) || isinf(xv[t]));
+                    const bool nz = xv[t] != 0.0f;
+                    if (!__any_sync(0xffffffffu, nz)) continue;
+                    // x-blocks of this chunk lie in bit words wa, wa+1 (32 voxels span <= 32/B + 2 blocks)
+                    const int wa = ((c0 - 1) >> s) >> 5;
+                    unsigned b0 = 0u, b1 = 0u;
+                    if (nz) {
+                        const int xa = (i - 1) >> s, xb = i >> s;
+                        (xa >> 5 == wa ? b0 : b1) |= 1u << (xa & 31);
+                        if (xb < g.nbx) (xb >> 5 == wa ? b0 : b1) |= 1u << (xb & 31);
                     }
-        if (any) {
-            atomicOr(mask + (b >> 5), 1u << (b & 31));
-            int32_t* smin = reinterpret_cast<int32_t*>(mask + g.words);
-            int32_t* smax = smin + 2 * g.nbz;
-            atomicMin(smin + 2 * bz, bx);
-            atomicMin(smin + 2 * bz + 1, by);
-            atomicMax(smax + 2 * bz, bx);
-            atomicMax(smax + 2 * bz + 1, by);
-            atomicMin(aabb + 0, bx);
-            atomicMin(aabb + 1, by);
-            atomicMin(aabb + 2, bz);
-            atomicMax(aabb + 3, bx);
-            atomicMax(aabb + 4, by);
-            atomicMax(aabb + 5, bz);
+                    b0 = __reduce_or_sync(0xffffffffu, b0);
+                    b1 = __reduce_or_sync(0xffffffffu, b1);
+                    if (lane == 0) {
+                        if (b0) atomicOr(xflag + wa, b0);
+                        if (b1) atomicOr(xflag + wa + 1, b1);
+                    }
+                }
+            }
         }
     }
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicAdd(red + 2, bad);
+    __syncthreads();
+    for (int bx = threadIdx.x; bx < g.nbx; bx += blockDim.x)
+        if (xflag[bx >> 5] >> (bx & 31) & 1u) {
+            atomicMin(red + 0, bx);
+            atomicMax(red + 1, bx);
+        }
+    uint32_t* flags = scratch + (size_t)row_id * g.rowwords;
+    for (int w = threadIdx.x; w < g.rowwords; w += blockDim.x) flags[w] = xflag[w];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t* info = reinterpret_cast<int32_t*>(scratch + g.info_off) + 4 * row_id;
+        info[0] = red[0];
+        info[1] = red[1];
+        info[2] = red[2];
+    }
+}
+
+// Horizontal fusion of the two independent passes over the raw grid: CTAs [0, rows) are
+// occupancy rows, the rest write the sampler layout.  Triggers its dependent (the
+// PDL-launched occ_finalize_kernel) at once so that launch overlaps this grid.
+template <int LAYOUT>
+__global__ void __launch_bounds__(256, 6) volume_build_kernel(Raw r, void* __restrict__ out, OccGeom g,
+                                                              uint32_t* __restrict__ scratch, int plane_blocks,
+                                                              int kstep, int occ_stride) {
+    extern __shared__ uint32_t xflag[];
+    __shared__ int red[3];
+    pdl_trigger();
+    // occupancy CTAs interleaved with the layout CTAs (every occ_stride-th of the first
+    // rows*occ_stride) so that every wave mixes latency-bound scans with HBM streaming
+    const int b = blockIdx.x;
+    int lb;
+    if (b < g.rows * occ_stride) {
+        if (b % occ_stride == 0) {
+            occupancy_cta(r, g, scratch, b / occ_stride, xflag, red);
+            return;
+        }
+        lb = b - (b / occ_stride + 1);
+    } else {
+        lb = b - g.rows;
+    }
+    const int pb = lb % plane_blocks, kb = lb / plane_blocks;
+    if (LAYOUT == kLinearF32) layout_linear_cta(r, static_cast<float*>(out), pb, kb, kstep);
+    if (LAYOUT == kQuadF32) layout_quad_cta(r, static_cast<float4*>(out), pb, kb, kstep);
+    if (LAYOUT == kCornerF16) layout_corner_f16_cta(r, static_cast<uint4*>(out), pb, kb, kstep);
+}
+
+// The occupancy region [mask: words][slab_min: nbz x (bx, by)][slab_max: nbz x (bx, by)], the
+// occupied-block AABB (bmin xyz, bmax xyz; bmin > bmax: empty) and the invalid-voxel count, from
+// the rows' scratch records.  CTA 0 reduces the records (one thread per record, shared-memory
+// min/max per slab; empty slab: min = 0x7f7f7f7f, max = -1); CTAs 1.. assemble the mask, one
+// warp per 32-bit word, one lane per bit (a single gather each, then a ballot).
+constexpr int kFinThreads = 1024;
+__global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, const uint32_t* __restrict__ scratch,
+                                                                   uint32_t* __restrict__ mask,
+                                                                   int32_t* __restrict__ aabb,
+                                                                   unsigned long long* __restrict__ invalid) {
+    pdl_trigger();
+    pdl_wait();
+    const int32_t* info = reinterpret_cast<const int32_t*>(scratch + g.info_off);
+    if (blockIdx.x > 0) {
+        const long bits = (long)g.nbx * g.nby * g.nbz;
+        const int w = (blockIdx.x - 1) * (kFinThreads / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+        if (w >= g.words) return;
+        const long b = 32L * w + lane;
+        bool bit = false;
+        if (b < bits) {
+            const int row = (int)(b / g.nbx), bx = (int)(b - (long)row * g.nbx);
+            bit = __ldg(scratch + (size_t)row * g.rowwords + (bx >> 5)) >> (bx & 31) & 1u;
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) mask[w] = word;
+        return;
+    }
+    extern __shared__ int32_t sl[];                   // [4][nbz]: x0, y0, x1, y1
+    __shared__ int am[6];
+    __shared__ unsigned long long nbad;
+    for (int i = threadIdx.x; i < 4 * g.nbz; i += kFinThreads) sl[i] = i < 2 * g.nbz ? 0x7f7f7f7f : -1;
+    if (threadIdx.x < 6) am[threadIdx.x] = threadIdx.x < 3 ? 0x7f7f7f7f : -1;
+    if (threadIdx.x == 0) nbad = 0ull;
+    __syncthreads();
+    unsigned long long mybad = 0ull;
+    for (int rid = threadIdx.x; rid < g.rows; rid += kFinThreads) {
+        const int4 rec = __ldg(reinterpret_cast<const int4*>(info) + rid);
+        mybad += (unsigned long long)rec.z;
+        if (rec.y >= 0) {
+            const int by = rid % g.nby, bz = rid / g.nby;
+            atomicMin(sl + bz, rec.x);
+            atomicMin(sl + g.nbz + bz, by);
+            atomicMax(sl + 2 * g.nbz + bz, rec.y);
+            atomicMax(sl + 3 * g.nbz + bz, by);
+        }
+    }
+    if (mybad) atomicAdd(&nbad, mybad);
+    __syncthreads();
+    int32_t* smin = reinterpret_cast<int32_t*>(mask + g.words);
+    int32_t* smax = smin + 2 * g.nbz;
+    for (int bz = threadIdx.x; bz < g.nbz; bz += kFinThreads) {
+        const int x0 = sl[bz], y0 = sl[g.nbz + bz], x1 = sl[2 * g.nbz + bz], y1 = sl[3 * g.nbz + bz];
+        smin[2 * bz] = x0;
+        smin[2 * bz + 1] = y0;
+        smax[2 * bz] = x1;
+        smax[2 * bz + 1] = y1;
+        if (x1 >= 0) {
+            atomicMin(am + 0, x0);
+            atomicMin(am + 1, y0);
+            atomicMin(am + 2, bz);
+            atomicMax(am + 3, x1);
+            atomicMax(am + 4, y1);
+            atomicMax(am + 5, bz);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) aabb[threadIdx.x] = am[threadIdx.x];
+    if (threadIdx.x == 0) *invalid = nbad;
 }
 
 }  // namespace
@@ -153,6 +323,10 @@ OccGeom occ_geom(int nx, int ny, int nz) {
         const long bits = (long)g.nbx * g.nby * g.nbz;
         g.words = (int)(((bits + 31) / 32 + 3) / 4 * 4);
         g.words_total = g.words + 4 * g.nbz;
+        g.rowwords = (g.nbx + 31) / 32;
+        g.rows = g.nby * g.nbz;
+        g.info_off = (g.rows * g.rowwords + 3) / 4 * 4;
+        g.scratch_words = g.info_off + 4 * g.rows;
         if ((forced > 0 && s >= forced) || (long)g.words * 4 <= budget) {
             if ((long)g.words * 4 <= 16 * 1024 && g.nbz <= 1024) break;
         }
@@ -160,43 +334,48 @@ OccGeom occ_geom(int nx, int ny, int nz) {
     return g;
 }
 
-cudaError_t launch_occupancy(const float* raw, const VolDesc& v, uint32_t* mask, int32_t* aabb, cudaStream_t s) {
-    Raw r{raw, v.nx, v.ny, v.nz};
-    cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)v.og.words * 4, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(mask + v.og.words, 0x7f, (size_t)v.og.nbz * 8, s);                 // slab min
-    if (e == cudaSuccess) e = cudaMemsetAsync(mask + v.og.words + 2 * v.og.nbz, 0xff, (size_t)v.og.nbz * 8, s);  // slab max
-    if (e == cudaSuccess) e = cudaMemsetAsync(aabb, 0x7f, 3 * sizeof(int32_t), s);      // bmin = 0x7f7f7f7f
-    if (e == cudaSuccess) e = cudaMemsetAsync(aabb + 3, 0xff, 3 * sizeof(int32_t), s);  // bmax = -1
-    if (e != cudaSuccess) return e;
-    const int total = v.og.nbx * v.og.nby * v.og.nbz;
-    occupancy_kernel<<<(total + 127) / 128, 128, 0, s>>>(r, mask, v.og, aabb);
-    return cudaGetLastError();
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("NSL_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
-cudaError_t launch_layout(const float* raw, const VolDesc& v, void* storage, unsigned long long* invalid,
-                          cudaStream_t s) {
+// Volume build: one fused launch (layout + occupancy rows), then the PDL-launched finalize.
+cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storage, uint32_t* scratch,
+                                unsigned long long* invalid, cudaStream_t s) {
     Raw r{raw, v.nx, v.ny, v.nz};
-    size_t total = layout_elems(v.layout, v.nx, v.ny, v.nz);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    size_t want = (total + 255) / 256;
-    unsigned blocks = (unsigned)(want < (size_t)sms * 16 ? want : (size_t)sms * 16);
-    if (blocks == 0) blocks = 1;
+    const int plane = v.layout == kLinearF32 ? (v.nx + 2) * (v.ny + 2) : (v.nx + 1) * (v.ny + 1);
+    const int planes = v.layout == kCornerF16 ? v.nz + 1 : v.nz + 2;
+    const int plane_blocks = (plane + 255) / 256;
+    int kstep = v.layout == kQuadF32 ? (planes + kQuadPlanes - 1) / kQuadPlanes : planes;
+    const long max_layout_ctas = 2000000000L - v.og.rows;
+    if ((long)plane_blocks * kstep > max_layout_ctas) kstep = (int)(max_layout_ctas / plane_blocks);
+    const unsigned grid = (unsigned)(v.og.rows + (long)plane_blocks * kstep);
+    const int occ_stride = (int)(grid / (unsigned)v.og.rows);
+    const size_t smem = (size_t)v.og.rowwords * 4;
     switch (v.layout) {
         case kLinearF32:
-            layout_linear_kernel<<<blocks, 256, 0, s>>>(r, static_cast<float*>(storage), invalid, total);
+            volume_build_kernel<kLinearF32><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
+                                                                          occ_stride);
             break;
         case kQuadF32:
-            layout_quad_kernel<<<blocks, 256, 0, s>>>(r, static_cast<float4*>(storage), invalid, total);
+            volume_build_kernel<kQuadF32><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
+                                                                          occ_stride);
             break;
         case kCornerF16:
-            layout_corner_f16_kernel<<<blocks, 256, 0, s>>>(r, static_cast<uint4*>(storage), invalid, total);
+            volume_build_kernel<kCornerF16><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
+                                                                          occ_stride);
             break;
         default:
             return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const unsigned fin_ctas = 1u + (unsigned)((v.og.words + kFinThreads / 32 - 1) / (kFinThreads / 32));
+    return launch_pdl(occ_finalize_kernel, dim3(fin_ctas), dim3(kFinThreads), (size_t)v.og.nbz * 16, s, v.og, (const uint32_t*)scratch,
+                      const_cast<uint32_t*>(v.occ), const_cast<int32_t*>(v.aabb), invalid);
 }
 
 }  // namespace nsl
