@@ -60,12 +60,15 @@ def test_volume_bytes(nsl):
     lin = nsl.volume_bytes(g, nsl.LAYOUT_LINEAR_F32)
     quad = nsl.volume_bytes(g, nsl.LAYOUT_QUAD_F32)
     f16 = nsl.volume_bytes(g, nsl.LAYOUT_CORNER_F16)
-    # body | occupancy mask (2x2x2-cell blocks: 3*3*4 bits -> 4 words -> one 256-B slot) | 256-B tail
-    tail = 256 + 256
+    oct_ = nsl.volume_bytes(g, nsl.LAYOUT_OCT_F32)
+    # body | occupancy region (2x2x2-cell blocks: 3*3*4 bits -> 4 words + 4 nbz slab words) | build scratch
+    # (12 block rows x 1 flag word + 12 4-word records = 60 words) | 256-B tail: one 256-B slot each
+    tail = 256 + 256 + 256
     up = lambda x: (x + 255) // 256 * 256
     assert lin == up(6 * 7 * 8 * 4) + tail
     assert quad == up(5 * 6 * 8 * 16) + tail
     assert f16 == up(5 * 6 * 7 * 16) + tail
+    assert oct_ == up(5 * 6 * 7 * 32) + tail
     L = nsl.lib()
     assert L.nsl_volume_bytes(ctypes.byref(nsl.grid_desc(I.Grid(0, 5, 6, (0, 0, 0), 0.25))), 1) == 0
     assert L.nsl_volume_bytes(ctypes.byref(nsl.grid_desc(g)), 7) == 0
