@@ -63,12 +63,16 @@ typedef struct {
  *  QUAD_F32   : per padded cell (i,j,k), i<=nx, j<=ny, k<=nz+1, a float4 of the
  *               x/y 2x2 corner quad (2 x 16-B gathers/sample), exact fp32 values
  *  CORNER_F16 : per padded cell (i,j,k), i<=nx, j<=ny, k<=nz, all 8 corners as
- *               fp16 (1 x 16-B gather/sample); values rounded RNE to fp16  */
+ *               fp16 (1 x 16-B gather/sample); values rounded RNE to fp16
+ *  OCT_F32    : per padded cell (i,j,k), i<=nx, j<=ny, k<=nz, the QUAD float4 of
+ *               planes k and k+1 side by side (32 B: one 256-bit gather/sample),
+ *               exact fp32 values; storage must be 32-B aligned  */
 typedef enum {
     NSL_LAYOUT_LINEAR_F32 = 0,
     NSL_LAYOUT_QUAD_F32 = 1,
     NSL_LAYOUT_CORNER_F16 = 2,
-    NSL_LAYOUT_DEFAULT = 1
+    NSL_LAYOUT_OCT_F32 = 3,
+    NSL_LAYOUT_DEFAULT = 3
 } nsl_layout;
 
 typedef struct nsl_volume nsl_volume;             /* opaque, immutable after upload */

@@ -153,12 +153,8 @@ __global__ void __launch_bounds__(kBakeThreads) bake_kernel(const FrameParams* _
     Vol v;
     v.data = sp.data;
     v.occ = sp.occ;
-    v.mask_sa = 0;
     v.sy = sp.sy;
     v.sz = sp.sz;
-    v.inv_b = __int_as_float((127 - sp.occ_shift) << 23);
-    v.nbx_f = (float)sp.occ_nbx;
-    v.nbxy_f = (float)(sp.occ_nbx * sp.occ_nby);
     v.shift = sp.occ_shift;
     v.nbx = sp.occ_nbx;
     v.nby = sp.occ_nby;
@@ -318,6 +314,7 @@ cudaError_t launch_bake(const FrameParams* fp, const BakeFrame* bf, const BakeCo
         case kLinearF32: return launch_bake_l<kLinearF32>(fp, bf, bc, F, W, H, projection, out, s);
         case kQuadF32: return launch_bake_l<kQuadF32>(fp, bf, bc, F, W, H, projection, out, s);
         case kCornerF16: return launch_bake_l<kCornerF16>(fp, bf, bc, F, W, H, projection, out, s);
+        case kOctF32: return launch_bake_l<kOctF32>(fp, bf, bc, F, W, H, projection, out, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -83,7 +83,7 @@ nsl_status check_grid(const nsl_grid_desc* g) {
 }
 
 nsl_status check_layout(int layout) {
-    if (layout != kLinearF32 && layout != kQuadF32 && layout != kCornerF16)
+    if (layout != kLinearF32 && layout != kQuadF32 && layout != kCornerF16 && layout != kOctF32)
         return fail(NSL_ERR_INVALID_ARG, "unknown layout %d", layout);
     return NSL_OK;
 }
@@ -210,6 +210,7 @@ struct Workspace {
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
     uint32_t* order = nullptr;
+    uint8_t* cull = nullptr;           // march_cull_bytes workspace (march calls only)
 };
 
 // March tile order: centre-out by the distance of the tile centre from the image
@@ -237,13 +238,15 @@ nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lig
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
     const size_t b_o = align_up(sizeof(uint32_t) * order.size(), 256);
-    const size_t b_p = sizeof(FrameParams) * F;
+    const size_t b_p = align_up(sizeof(FrameParams) * F, 256);
+    const size_t b_c = order.empty() ? 0 : march_cull_bytes(F, frames[0].cam.width, frames[0].cam.height);
     retain_pool_once();
-    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_o + b_p, s), "cudaMallocAsync(frame tables)");
+    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_o + b_p + b_c, s), "cudaMallocAsync(frame tables)");
     ws.in = reinterpret_cast<FrameIn*>(ws.base);
     ws.lights = reinterpret_cast<nsl_light*>(static_cast<char*>(ws.base) + b_in);
     ws.order = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.base) + b_in + b_l);
     ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l + b_o);
+    ws.cull = b_c ? reinterpret_cast<uint8_t*>(ws.base) + b_in + b_l + b_o + b_p : nullptr;
     std::vector<char> host(b_in + b_l + b_o);
     memcpy(host.data(), frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
@@ -271,7 +274,8 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     if (nsl_status st = check_grid(g)) return st;
     if (nsl_status st = check_layout(layout)) return st;
     if (!density || !device_storage || !out) return fail(NSL_ERR_INVALID_ARG, "NULL density/storage/out");
-    if (reinterpret_cast<uintptr_t>(device_storage) % 16) return fail(NSL_ERR_INVALID_ARG, "storage must be 16-B aligned");
+    if (reinterpret_cast<uintptr_t>(device_storage) % (layout == kOctF32 ? 32 : 16))
+        return fail(NSL_ERR_INVALID_ARG, "storage must be %d-B aligned", layout == kOctF32 ? 32 : 16);
     const size_t need = nsl_volume_bytes(g, layout);
     if (storage_bytes < need) return fail(NSL_ERR_INVALID_ARG, "storage_bytes %zu < required %zu", storage_bytes, need);
     const size_t n = (size_t)g->nx * g->ny * g->nz;
@@ -333,7 +337,7 @@ nsl_status nsl_volume_release(nsl_volume* v) {
 struct Prepared {
     std::vector<FrameIn> frames;
     MarchConst mc;
-    int F = 0, W = 0, H = 0, proj = 0, layout = 0, max_words = 0, n_lights = 0;
+    int F = 0, W = 0, H = 0, proj = 0, layout = 0, n_lights = 0;
 };
 
 static nsl_status prepare(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
@@ -347,13 +351,13 @@ static nsl_status prepare(const nsl_volume* const* vols, int32_t n_vols, const i
     for (int i = 0; i < n_vols; ++i)
         if (!vols[i]) return fail(NSL_ERR_INVALID_ARG, "vols[%d] is NULL", i);
     P.layout = vols[0]->layout;
-    P.max_words = 0;
-    for (int i = 0; i < n_vols; ++i) {
+    for (int i = 0; i < n_vols; ++i)
         if (vols[i]->layout != P.layout) return fail(NSL_ERR_UNSUPPORTED, "all volumes of a batch must share a layout");
-        P.max_words = vols[i]->og.words_total > P.max_words ? vols[i]->og.words_total : P.max_words;
-    }
     P.W = cams[0].width;
     P.H = cams[0].height;
+    if ((long)((P.W + march_tile_w() - 1) / march_tile_w()) * ((P.H + march_tile_h() - 1) / march_tile_h()) > 65535)
+        return fail(NSL_ERR_UNSUPPORTED, "image too large: more than 65535 march tiles (16x%d pixels) per frame",
+                    march_tile_h());
     P.proj = cams[0].projection;
     P.F = F;
     P.n_lights = n_lights;
@@ -394,8 +398,8 @@ static nsl_status batch_impl(const nsl_volume* const* vols, int32_t n_vols, cons
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
     if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, tile_order(P.W, P.H), s, ws)) return st;
-    cudaError_t e = launch_march(ws.params, P.mc, P.F, P.W, P.H, P.proj, P.layout, P.max_words,
-                                 reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug, counters, ws.order, s);
+    cudaError_t e = launch_march(ws.params, P.mc, P.F, P.W, P.H, P.proj, P.layout, reinterpret_cast<float4*>(out_rgbt),
+                                 out_depth, out_debug, counters, ws.order, ws.cull, s);
     cudaError_t e2 = cudaFreeAsync(ws.base, s);
     if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
     if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(frame tables)");
@@ -487,6 +491,7 @@ struct nsl_plan {
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
     uint32_t* order = nullptr;
+    uint8_t* cull = nullptr;
 };
 
 nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
@@ -504,8 +509,9 @@ nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const 
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
     const size_t b_o = align_up(sizeof(uint32_t) * order.size(), 256);
-    const size_t b_p = sizeof(FrameParams) * F;
-    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_o + b_p);
+    const size_t b_p = align_up(sizeof(FrameParams) * F, 256);
+    const size_t b_c = march_cull_bytes(F, p->P.W, p->P.H);
+    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_o + b_p + b_c);
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaMalloc(plan)");
@@ -514,6 +520,7 @@ nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const 
     p->lights = reinterpret_cast<nsl_light*>(static_cast<char*>(p->dev) + b_in);
     p->order = reinterpret_cast<uint32_t*>(static_cast<char*>(p->dev) + b_in + b_l);
     p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_o);
+    p->cull = reinterpret_cast<uint8_t*>(p->dev) + b_in + b_l + b_o + b_p;
     std::vector<char> host(b_in + b_l + b_o);
     memcpy(host.data(), p->P.frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
@@ -539,9 +546,9 @@ nsl_status nsl_plan_execute(const nsl_plan* p, float* out_rgbt, float* out_depth
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (counters) NSL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint64_t), s), "cudaMemsetAsync(counters)");
     NSL_CUDA(launch_frame_setup(p->in, p->lights, p->P.F, p->P.mc, p->params, s), "frame_setup_kernel launch");
-    NSL_CUDA(launch_march(p->params, p->P.mc, p->P.F, p->P.W, p->P.H, p->P.proj, p->P.layout, p->P.max_words,
+    NSL_CUDA(launch_march(p->params, p->P.mc, p->P.F, p->P.W, p->P.H, p->P.proj, p->P.layout,
                           reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug,
-                          reinterpret_cast<unsigned long long*>(counters), p->order, s),
+                          reinterpret_cast<unsigned long long*>(counters), p->order, p->cull, s),
              "march_kernel launch");
     return NSL_OK;
 }

@@ -2,124 +2,100 @@
 // L394-407; C3-C12) for sm_100a.
 //
 // One thread per pixel; a warp marches a coherent 8x4 pixel tile, a CTA a
-// 16x16 tile (8 warps); blockIdx.z is the frame of the batch (row a9).
-// Sample positions use only explicitly rounded fp32 operations (__fmaf_rn,
-// __fmul_rn) so that every index decision is bit-identical to the oracle
-// (C14); values are fp32 with FMA lerps.  The step range is
-// clipped exactly (C5) and each light march's length is computed exactly
-// (C8) so the inner loops carry no bounds tests.
+// 16x8 tile (4 warps).  Grid (frame, tile rank): frames fastest, tiles in
+// centre-out order.  Sample positions use only explicitly rounded fp32
+// operations (__fmaf_rn, __fmul_rn) so that every index decision is
+// bit-identical to the oracle (C14); values are fp32 with FMA
+// lerps.  The step range is clipped exactly (C5) and each light march's
+// length is computed exactly (C8) so the inner loops carry no bounds tests.
 //
-// The path is bound by L1 data-pipe wavefronts of the trilinear gathers
-// (profiles/).  Before gathering, every sample tests the
-// volume's occupancy bitmask, staged per CTA in shared memory: a sample
-// whose cell lies in an all-zero block is exactly 0 (C1), so skipping its
-// loads changes no bit of the result while removing most of the wavefronts
-// (empty space outside the smoke).
+// Before gathering, every sample tests the volume's occupancy bitmask (L1
+// resident): a sample whose cell lies in an all-zero block is exactly 0 (C1),
+// so skipping its load changes no bit of the result.  Whole tiles whose rays
+// miss the occupied box are culled by tile_cull_kernel beforehand (exact:
+// DESIGN.md §6), so their CTAs only write the empty map.  The kernel is
+// issue-bound (profiles/).
 #include "sampler.cuh"
 
 namespace nsl {
 namespace {
+
+// Tile culling (exact, orthographic views): every ray of a tile is parallel to D_g with
+// its origin within tile_r of the centre ray; if the centre ray misses a box expanded by
+// tile_r, no sample of the tile lies in the box.  bit 0: misses the occupied box (FAST:
+// every sample outside it is exactly 0); bit 1: misses the support box (DEBUG/COUNTED,
+// which report n_lo/n_hi: C5).  One thread per (frame, tile).
+__global__ void tile_cull_kernel(const FrameParams* __restrict__ fps, int F, int tiles_x, int tiles,
+                                 uint8_t* __restrict__ cull) {
+    pdl_trigger();
+    pdl_wait();                        // the FrameParams of frame_setup_kernel
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)F * tiles) return;
+    const int f = (int)(idx / (unsigned)tiles), t = (int)(idx - (size_t)f * tiles);
+    const int tx = t % tiles_x, ty = t / tiles_x;
+    const FrameParams& sp = fps[f];
+    const float cx = (float)(tx * kTileW) + 0.5f * (kTileW - 1), cy = (float)(ty * kTileH) + 0.5f * (kTileH - 1);
+    const float c[3] = {fmaf(cy, sp.Ey[0], fmaf(cx, sp.Ex[0], sp.B[0])), fmaf(cy, sp.Ey[1], fmaf(cx, sp.Ex[1], sp.B[1])),
+                        fmaf(cy, sp.Ey[2], fmaf(cx, sp.Ex[2], sp.B[2]))};
+    const float rr = sp.tile_r;
+    uint8_t bits = 0;
+    for (int box = 0; box < 2; ++box) {
+        float t0 = -3.0e38f, t1 = 3.0e38f;
+        bool miss = false;
+        for (int q = 0; q < 3; ++q) {
+            const float lo = box == 0 ? sp.alo[q] : 0.0f, hi = box == 0 ? sp.ahi[q] : sp.supp[q];
+            slab(c[q] - lo + rr, sp.Dg[q], sp.invD[q], hi - lo + 2.0f * rr, 0.0f, t0, t1, miss);
+        }
+        if (miss || !(t0 <= t1) || t1 < 0.0f) bits |= (uint8_t)(1u << box);
+    }
+    cull[idx] = bits;
+}
 
 template <int LAYOUT, int PROJ, int MODE>
 __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H,
-                                                         const uint32_t* __restrict__ tile_order, int F) {
+                                                         const uint32_t* __restrict__ tile_order,
+                                                         const uint8_t* __restrict__ cull, int tiles_x) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
-#if NSL_STAGE
-    uint4* smem = reinterpret_cast<uint4*>(nsl_smem);
-    FrameParams& sp = *reinterpret_cast<FrameParams*>(smem);
-    uint4* smask4 = smem + sizeof(FrameParams) / 16;
-#endif
-    // 1-D grid over (tile rank, frame), frame fastest; tiles in centre-out order
+    // grid (frame, tile rank): frames fastest in launch order; tiles centre-out
     // (tile_order) so the heavy tiles of every frame start first and the tail of
     // the launch is made of cheap border tiles.
-    const int f = (int)(blockIdx.x % (unsigned)F);
-    const uint32_t tile = __ldg(tile_order + blockIdx.x / (unsigned)F);
+    const int f = (int)blockIdx.x;
+    const uint32_t tile = __ldg(tile_order + blockIdx.y);
     const int tx = (int)(tile & 0xffffu), ty = (int)(tile >> 16);
-    pdl_wait();                        // launched with PDL after frame_setup_kernel: its FrameParams
-#if NSL_STAGE
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(fps + f);
-        for (int i = threadIdx.x; i < (int)(sizeof(FrameParams) / 16); i += blockDim.x) smem[i] = src[i];
-    }
-    __syncthreads();
-#else
+    pdl_wait();                        // launched with PDL after frame_setup / tile_cull: their outputs
     const FrameParams& sp = fps[f];
-#endif
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx * kTileW + (warp & 1) * 8 + (lane & 7);
     const int py = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);
     const bool valid = px < W && py < H;
-    const size_t o = (size_t)f * (size_t)W * (size_t)H + (size_t)py * W + px;
+    const size_t o = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
+
+    if (PROJ == 0 && (__ldg(cull + (size_t)f * gridDim.y + ty * tiles_x + tx) & (DEBUG || COUNT ? 2 : 1))) {
+        if (valid) {                   // the empty map: L = 0, T = 1, D = 0, counters 0
+            out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
+            out_depth[o] = 0.0f;
+            if (DEBUG) {
+                uint32_t* dbg = out_debug + o * 6;
+                dbg[0] = dbg[1] = dbg[2] = dbg[3] = dbg[4] = dbg[5] = 0u;
+            }
+        }
+        return;                        // uniform over the CTA
+    }
 
     Vol v;
     v.data = sp.data;
     v.sy = sp.sy;
     v.sz = sp.sz;
-#if NSL_STAGE
-    v.mask_sa = (uint32_t)__cvta_generic_to_shared(smask4);
-#else
-    v.mask_sa = 0;
-#endif
     v.occ = sp.occ;
-    v.inv_b = __int_as_float((127 - sp.occ_shift) << 23);   // 2^-shift exactly
-    v.nbx_f = (float)sp.occ_nbx;
-    v.nbxy_f = (float)(sp.occ_nbx * sp.occ_nby);
     v.shift = sp.occ_shift;
     v.nbx = sp.occ_nbx;
     v.nby = sp.occ_nby;
     v.sx1 = sp.supp[0];
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
-
-    if (PROJ == 0) {
-        // Tile culling (exact): every ray of the tile is parallel to D_g with its origin
-        // within tile_r of the centre ray; if the centre ray misses the support box
-        // expanded by tile_r, no sample of the tile is in support (C5) and the
-        // output is the empty map (L = 0, T = 1, D = 0, counters 0).
-        const float cx = (float)(tx * kTileW) + 0.5f * (kTileW - 1), cy = (float)(ty * kTileH) + 0.5f * (kTileH - 1);
-        Ray c;
-        c.ox = fmaf(cy, sp.Ey[0], fmaf(cx, sp.Ex[0], sp.B[0]));
-        c.oy = fmaf(cy, sp.Ey[1], fmaf(cx, sp.Ex[1], sp.B[1]));
-        c.oz = fmaf(cy, sp.Ey[2], fmaf(cx, sp.Ex[2], sp.B[2]));
-        // FAST mode culls against the occupied box (every sample outside it is 0, and
-        // FAST writes no counters); DEBUG/COUNTED need the support box for n_lo/n_hi.
-        float t0 = -3.0e38f, t1 = 3.0e38f;
-        bool miss = false;
-        const float rr = sp.tile_r;
-        float lo[3] = {0.0f, 0.0f, 0.0f}, hi[3] = {v.sx1, v.sy1, v.sz1};
-        if (!DEBUG && !COUNT) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                lo[q] = sp.alo[q];
-                hi[q] = sp.ahi[q];
-            }
-        }
-        slab(c.ox - lo[0] + rr, sp.Dg[0], sp.invD[0], hi[0] - lo[0] + 2.0f * rr, 0.0f, t0, t1, miss);
-        slab(c.oy - lo[1] + rr, sp.Dg[1], sp.invD[1], hi[1] - lo[1] + 2.0f * rr, 0.0f, t0, t1, miss);
-        slab(c.oz - lo[2] + rr, sp.Dg[2], sp.invD[2], hi[2] - lo[2] + 2.0f * rr, 0.0f, t0, t1, miss);
-        if (miss || !(t0 <= t1) || t1 < 0.0f) {
-            if (valid) {
-                out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
-                out_depth[o] = 0.0f;
-                if (DEBUG) {
-                    uint32_t* dbg = out_debug + o * 6;
-                    dbg[0] = dbg[1] = dbg[2] = dbg[3] = dbg[4] = dbg[5] = 0u;
-                }
-            }
-            return;   // uniform over the CTA
-        }
-    }
-#if NSL_STAGE
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(sp.occ);
-        const int n4 = sp.occ_words >> 2;
-        for (int i = threadIdx.x; i < n4; i += blockDim.x) smask4[i] = __ldg(src + i);
-    }
-    __syncthreads();
-#endif
     if (!COUNT && !valid) return;
 
     uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0, c_tp = 0, c_tl = 0;
@@ -350,33 +326,35 @@ __global__ void jitter_debug_kernel(MarchConst mc, uint32_t frame, int n, uint32
 }
 
 template <int LAYOUT, int PROJ, int MODE>
-cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, size_t smem, float4* rgbt,
-                       float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* tile_order,
+cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
+                       uint32_t* debug, unsigned long long* counters, const uint32_t* tile_order, uint8_t* cull,
                        cudaStream_t s) {
-    const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
-    dim3 grid((unsigned)(tiles_x * tiles_y) * (unsigned)F);
-    auto k = march_kernel<LAYOUT, PROJ, MODE>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH, tiles = tiles_x * tiles_y;
+    if (tiles > 65535) return cudaErrorInvalidConfiguration;
+    if (PROJ == 0) {
+        const size_t n = (size_t)F * tiles;
+        cudaError_t e = launch_pdl(tile_cull_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, fp, F, tiles_x,
+                                   tiles, cull);
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(k, grid, dim3(kThreads), smem, s, fp, mc, rgbt, depth, debug, counters, W, H, tile_order, F);
+    return launch_pdl(march_kernel<LAYOUT, PROJ, MODE>, dim3((unsigned)F, (unsigned)tiles), dim3(kThreads), 0, s, fp,
+                      mc, rgbt, depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x);
 }
 
 template <int LAYOUT, int PROJ>
-cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, size_t smem, float4* rgbt,
-                      float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* to, cudaStream_t s) {
-    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
-    if (counters) return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
-    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
+cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
+                      uint32_t* debug, unsigned long long* counters, const uint32_t* to, uint8_t* cull, cudaStream_t s) {
+    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
+    if (counters) return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
+    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
 }
 
 template <int LAYOUT>
-cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, size_t smem,
-                     float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* to,
+cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, float4* rgbt,
+                     float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* to, uint8_t* cull,
                      cudaStream_t s) {
-    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s)
-                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, smem, rgbt, depth, debug, counters, to, s);
+    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s)
+                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
 }
 
 }  // namespace
@@ -384,17 +362,18 @@ cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, 
 int march_tile_w() { return kTileW; }
 int march_tile_h() { return kTileH; }
 
+size_t march_cull_bytes(int F, int W, int H) {
+    return (size_t)F * ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
+}
+
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection, int layout,
-                         int max_occ_words, float4* rgbt, float* depth, uint32_t* debug,
-                         unsigned long long* counters, const uint32_t* tile_order, cudaStream_t s) {
-    const size_t smem = NSL_STAGE ? sizeof(FrameParams) + (size_t)max_occ_words * 4 : 0;
+                         float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
+                         const uint32_t* tile_order, uint8_t* cull, cudaStream_t s) {
     switch (layout) {
-        case kLinearF32:
-            return launch_l<kLinearF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, tile_order, s);
-        case kQuadF32:
-            return launch_l<kQuadF32>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, tile_order, s);
-        case kCornerF16:
-            return launch_l<kCornerF16>(fp, mc, F, W, H, projection, smem, rgbt, depth, debug, counters, tile_order, s);
+        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
+        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
+        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
+        case kOctF32: return launch_l<kOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
     }
     return cudaErrorInvalidValue;
 }

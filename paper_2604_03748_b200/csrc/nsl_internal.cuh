@@ -160,6 +160,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 constexpr int kLinearF32 = NSL_LAYOUT_LINEAR_F32;
 constexpr int kQuadF32 = NSL_LAYOUT_QUAD_F32;
 constexpr int kCornerF16 = NSL_LAYOUT_CORNER_F16;
+constexpr int kOctF32 = NSL_LAYOUT_OCT_F32;
 
 // Launch helpers implemented in the .cu files.
 // layout + occupancy + AABB + invalid-voxel count from the raw grid (two launches, no memsets)
@@ -167,10 +168,12 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
                                 unsigned long long* invalid, cudaStream_t s);
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s);
-// mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path
+// mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path.
+// cull: march_cull_bytes(F, W, H) bytes of device workspace (orthographic views: per-tile cull flags).
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection,
-                         int layout, int max_occ_words, float4* rgbt, float* depth, uint32_t* debug,
-                         unsigned long long* counters, const uint32_t* tile_order, cudaStream_t s);
+                         int layout, float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
+                         const uint32_t* tile_order, uint8_t* cull, cudaStream_t s);
+size_t march_cull_bytes(int F, int W, int H);
 int march_tile_w();
 int march_tile_h();
 cudaError_t launch_bake_setup(const FrameIn* in, const FrameParams* fps, int F, float hbl, float g, BakeFrame* out,

@@ -14,20 +14,6 @@ namespace {
 #define NSL_TILEH 8      // CTA tile 16 x NSL_TILEH pixels (warps of 8x4): 8 -> 128 threads (measured best), 16 -> 256
 #endif
 constexpr int kTileW = 16, kTileH = NSL_TILEH, kThreads = 2 * NSL_TILEH * 8;
-#ifndef NSL_BLOCKIDX
-#define NSL_BLOCKIDX 0   // occupancy block index: 1 exact fp32 FMAs, 0 integer shifts of the cell floor (measured equal, profiles/r1_sweep.txt)
-#endif
-#ifndef NSL_MASKREAD
-#define NSL_MASKREAD 0   // mask word read: 1 ld.shared via a 32-bit address, 0 extern shared array
-#endif
-#ifndef NSL_PAIRWALK
-#define NSL_PAIRWALK 0   // paired top/bottom march: 1 combined chord walk, 0 lock-step both sides (measured better)
-#endif
-#ifndef NSL_STAGE
-#define NSL_STAGE 0      // 1: stage FrameParams + occupancy region in shared memory per CTA; 0: read them
-                         //    through the read-only path from global memory (L1-resident; measured equal or
-                         //    better, no __syncthreads, all of L1 for the volume)
-#endif
 #ifndef NSL_MINB
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
                      // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)
@@ -36,21 +22,11 @@ constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
     const void* __restrict__ data;
-    const uint32_t* __restrict__ occ;   // occupancy region in global memory (NSL_STAGE == 0)
-    uint32_t mask_sa;             // shared-space byte address of the occupancy mask
+    const uint32_t* __restrict__ occ;   // occupancy region (mask | slab boxes), read through the read-only path
     int sy, sz;
-    float inv_b, nbx_f, nbxy_f;   // 2^-shift, blocks per x row, blocks per z slab (exact in fp32)
     int shift, nbx, nby;
     float sx1, sy1, sz1;          // support upper bounds n+1
 };
-
-// Dynamic shared memory of march_kernel: [FrameParams | occupancy mask words].
-// Indexed through this file-scope array so the mask test is one LDS with an
-// immediate offset (no generic->shared address conversion in the loops).
-extern __shared__ __align__(16) uint32_t nsl_smem[];
-#if NSL_STAGE
-constexpr int kMaskWord0 = (int)(sizeof(FrameParams) / 4);
-#endif
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return __fmaf_rn(t, b - a, a); }
 
@@ -66,53 +42,18 @@ __device__ __forceinline__ bool inside(const Vol& v, float x, float y, float z) 
 // low mantissa bits and r - 1.5*2^23 is floor(x) exactly.  No F2I/FRND (the
 // quarter-rate XU pipe) per sample.  Positions in support satisfy 0 < x < n+1.
 constexpr float kFloorBias = 12582912.0f;   // 1.5 * 2^23, bit pattern 0x4B400000
-#if NSL_BLOCKIDX == 1
-__device__ __forceinline__ void cellof(float x, int& i, float& frac) {
-    const float r = __fadd_rd(x, kFloorBias);
-    i = __float_as_int(r) - 0x4B400000;
-    frac = __fsub_rn(x, __fsub_rn(r, kFloorBias));
-}
-#endif
-
 template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
-#if NSL_BLOCKIDX == 1
-    // occupancy block index in exact fp32: floor(x / B) via fma rounded toward -inf
-    // onto the 1.5*2^23 grid (x * 2^-s is exact), then the linear index with two
-    // exact FMAs (every term is an integer < 2^24); the bias stays in the x term.
-    const float bx = __fmaf_rd(x, v.inv_b, kFloorBias);
-    const float by = __fsub_rn(__fmaf_rd(y, v.inv_b, kFloorBias), kFloorBias);
-    const float bz = __fsub_rn(__fmaf_rd(z, v.inv_b, kFloorBias), kFloorBias);
-    const int b = __float_as_int(__fmaf_rn(bz, v.nbxy_f, __fmaf_rn(by, v.nbx_f, bx))) - 0x4B400000;
-#else
     // cell floors (shared with the gather below), block = cell >> shift
     const float rx = __fadd_rd(x, kFloorBias), ry = __fadd_rd(y, kFloorBias), rz = __fadd_rd(z, kFloorBias);
     const int ix = __float_as_int(rx) - 0x4B400000, iy = __float_as_int(ry) - 0x4B400000,
               iz = __float_as_int(rz) - 0x4B400000;
     const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
-#endif
-#if NSL_MASKREAD == 1
-    uint32_t word;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(v.mask_sa + ((uint32_t)b >> 5) * 4u));
-#else
-#if NSL_STAGE
-    const uint32_t word = nsl_smem[kMaskWord0 + (b >> 5)];
-#else
     const uint32_t word = __ldg(v.occ + (b >> 5));
-#endif
-#endif
     if (!((word >> (b & 31)) & 1u)) return 0.0f;
     if (COUNT) ++gathers;
-#if NSL_BLOCKIDX == 1
-    int ix, iy, iz;
-    float fx, fy, fz;
-    cellof(x, ix, fx);
-    cellof(y, iy, fy);
-    cellof(z, iz, fz);
-#else
     const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias)),
                 fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
-#endif
     const int e = ix + iy * v.sy + iz * v.sz;
     if (LAYOUT == kLinearF32) {
         const float* p = static_cast<const float*>(v.data) + e;
@@ -128,6 +69,15 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
         const float4 q0 = __ldg(p), q1 = __ldg(p + v.sz);     // (c0, c1 - c0, c2, c3 - c2)
         const float x00 = __fmaf_rn(fx, q0.y, q0.x), x10 = __fmaf_rn(fx, q0.w, q0.z);
         const float x01 = __fmaf_rn(fx, q1.y, q1.x), x11 = __fmaf_rn(fx, q1.w, q1.z);
+        return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
+    } else if (LAYOUT == kOctF32) {
+        // one 256-bit gather: (c000, c100 - c000, c010, c110 - c010 | the same for plane k+1)
+        float a0, a1, a2, a3, b0, b1, b2, b3;
+        asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
+            : "l"(static_cast<const float*>(v.data) + 8 * (size_t)e));
+        const float x00 = __fmaf_rn(fx, a1, a0), x10 = __fmaf_rn(fx, a3, a2);
+        const float x01 = __fmaf_rn(fx, b1, b0), x11 = __fmaf_rn(fx, b3, b2);
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
     } else {
         const uint4 u = __ldg(static_cast<const uint4*>(v.data) + e);
@@ -268,31 +218,6 @@ template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy, float uz, float lx, float ly,
                                                float lz, float hl, int Ma, int Mb, float& sa, float& sb,
                                                uint32_t& gathers) {
-#if NSL_PAIRWALK == 1
-    // Walk the combined chord k = 0 .. Ma+Mb-1 (j = k+1 on the +L side, then j = k-Ma+1
-    // on the -L side) two samples per iteration: no lane idles on the shorter side.
-    // jf carries the sign of the side, so s = jf*h_l = +-fl(j*h_l) exactly.
-    float a = 0.0f, b = 0.0f;
-    const int K = Ma + Mb;
-    const float maf = (float)Ma;
-    float kf = 0.0f;
-    int k = 0;
-    for (; k + 1 < K; k += 2, kf += 2.0f) {
-        const float j0 = kf < maf ? kf + 1.0f : maf - kf - 1.0f;
-        const float j1 = kf + 1.0f < maf ? kf + 2.0f : maf - kf - 2.0f;
-        const float s0 = __fmul_rn(j0, hl), s1 = __fmul_rn(j1, hl);
-        const float r0 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
-        const float r1 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s1, lx, ux), __fmaf_rn(s1, ly, uy), __fmaf_rn(s1, lz, uz), gathers);
-        if (j0 > 0.0f) a += r0; else b += r0;
-        if (j1 > 0.0f) a += r1; else b += r1;
-    }
-    if (k < K) {
-        const float j0 = kf < maf ? kf + 1.0f : maf - kf - 1.0f;
-        const float s0 = __fmul_rn(j0, hl);
-        const float r0 = sample<LAYOUT, COUNT>(v, __fmaf_rn(s0, lx, ux), __fmaf_rn(s0, ly, uy), __fmaf_rn(s0, lz, uz), gathers);
-        if (j0 > 0.0f) a += r0; else b += r0;
-    }
-#else
     float a = 0.0f, b = 0.0f;
     const int M = max(Ma, Mb);
     float jf = 1.0f;
@@ -302,7 +227,6 @@ __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy,
         if (j <= Mb)
             b += sample<LAYOUT, COUNT>(v, __fmaf_rn(-s, lx, ux), __fmaf_rn(-s, ly, uy), __fmaf_rn(-s, lz, uz), gathers);
     }
-#endif
     sa = a;
     sb = b;
 }
@@ -341,15 +265,9 @@ __device__ __forceinline__ void march_region(const FrameParams& sp, const Vol& v
     if ((sp.lz0 >> l) & 1) {
         const int iz = __float_as_int(__fadd_rd(uz, kFloorBias)) - 0x4B400000;
         const int bz = iz >> v.shift;
-#if NSL_STAGE
-        const int* slab = reinterpret_cast<const int*>(nsl_smem) + kMaskWord0 + sp.slab_off;
-        const int2 mn = *reinterpret_cast<const int2*>(slab + 2 * bz);
-        const int2 mx = *reinterpret_cast<const int2*>(slab + 2 * sp.occ_nbz + 2 * bz);
-#else
         const int* slab = reinterpret_cast<const int*>(v.occ) + sp.slab_off;
         const int2 mn = __ldg(reinterpret_cast<const int2*>(slab + 2 * bz));
         const int2 mx = __ldg(reinterpret_cast<const int2*>(slab + 2 * sp.occ_nbz + 2 * bz));
-#endif
         const float B = (float)(1 << v.shift);
         const float lox = (float)mn.x * B, hix = fminf((float)(mx.x + 1) * B, v.sx1);
         const float loy = (float)mn.y * B, hiy = fminf((float)(mx.y + 1) * B, v.sy1);

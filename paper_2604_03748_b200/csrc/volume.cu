@@ -18,6 +18,7 @@ size_t layout_elems(int layout, int nx, int ny, int nz) {
         case kLinearF32: return (size_t)(nx + 2) * (ny + 2) * (nz + 2);
         case kQuadF32: return (size_t)(nx + 1) * (ny + 1) * (nz + 2);
         case kCornerF16: return (size_t)(nx + 1) * (ny + 1) * (nz + 1);
+        case kOctF32: return (size_t)(nx + 1) * (ny + 1) * (nz + 1);
     }
     return 0;
 }
@@ -27,6 +28,7 @@ size_t layout_elem_bytes(int layout) {
         case kLinearF32: return 4;
         case kQuadF32: return 16;
         case kCornerF16: return 16;
+        case kOctF32: return 32;
     }
     return 0;
 }
@@ -102,6 +104,28 @@ __device__ __forceinline__ void layout_corner_f16_cta(const Raw& r, uint4* __res
         u.z = *reinterpret_cast<unsigned*>(&h2);
         u.w = *reinterpret_cast<unsigned*>(&h3);
         out[(size_t)k * plane + e2] = u;
+    }
+}
+
+// OCT: the QUAD float4 of planes k and k+1 of cell (i, j, k) in one 32-B element (k <= nz).
+__device__ __forceinline__ void layout_oct_cta(const Raw& r, float4* __restrict__ out, int pb, int kb, int kstep) {
+    const int qx = r.nx + 1, qy = r.ny + 1, plane = qx * qy;
+    const int e2 = pb * 256 + threadIdx.x;
+    if (e2 >= plane) return;
+    const int i = e2 % qx, j = e2 / qx;
+    for (int k = kb; k < r.nz + 1; k += kstep) {
+        float c[2][4];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            c[t][0] = r.at(i, j, k + t);
+            c[t][1] = r.at(i + 1, j, k + t);
+            c[t][2] = r.at(i, j + 1, k + t);
+            c[t][3] = r.at(i + 1, j + 1, k + t);
+        }
+        float4* d = out + 2 * ((size_t)k * plane + e2);
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+            d[t] = make_float4(c[t][0], __fsub_rn(c[t][1], c[t][0]), c[t][2], __fsub_rn(c[t][3], c[t][2]));
     }
 }
 
@@ -230,6 +254,7 @@ __global__ void __launch_bounds__(256, 6) volume_build_kernel(Raw r, void* __res
     if (LAYOUT == kLinearF32) layout_linear_cta(r, static_cast<float*>(out), pb, kb, kstep);
     if (LAYOUT == kQuadF32) layout_quad_cta(r, static_cast<float4*>(out), pb, kb, kstep);
     if (LAYOUT == kCornerF16) layout_corner_f16_cta(r, static_cast<uint4*>(out), pb, kb, kstep);
+    if (LAYOUT == kOctF32) layout_oct_cta(r, static_cast<float4*>(out), pb, kb, kstep);
 }
 
 // The occupancy region [mask: words][slab_min: nbz x (bx, by)][slab_max: nbz x (bx, by)], the
@@ -347,7 +372,7 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
                                 unsigned long long* invalid, cudaStream_t s) {
     Raw r{raw, v.nx, v.ny, v.nz};
     const int plane = v.layout == kLinearF32 ? (v.nx + 2) * (v.ny + 2) : (v.nx + 1) * (v.ny + 1);
-    const int planes = v.layout == kCornerF16 ? v.nz + 1 : v.nz + 2;
+    const int planes = v.layout == kCornerF16 || v.layout == kOctF32 ? v.nz + 1 : v.nz + 2;
     const int plane_blocks = (plane + 255) / 256;
     int kstep = v.layout == kQuadF32 ? (planes + kQuadPlanes - 1) / kQuadPlanes : planes;
     const long max_layout_ctas = 2000000000L - v.og.rows;
@@ -366,6 +391,10 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
             break;
         case kCornerF16:
             volume_build_kernel<kCornerF16><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
+                                                                          occ_stride);
+            break;
+        case kOctF32:
+            volume_build_kernel<kOctF32><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
                                                                           occ_stride);
             break;
         default:

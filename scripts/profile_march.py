@@ -1,6 +1,6 @@
 """Minimal driver for ncu: the C2 batch (60 frames 512^2 over 128^3, guide lights),
 2 warm-up launches then N profiled launches of march_kernel.
-    python scripts/profile_march.py [--layout quad_f32] [--launches 1] [--config C2]"""
+    python scripts/profile_march.py [--layout oct_f32] [--launches 1] [--config C2]"""
 import argparse
 import os
 import sys
@@ -12,7 +12,7 @@ import nsl_inputs as I  # noqa: E402
 import paper_2604_03748_b200 as nsl  # noqa: E402
 
 p = argparse.ArgumentParser()
-p.add_argument("--layout", default="quad_f32")
+p.add_argument("--layout", default="oct_f32")
 p.add_argument("--launches", type=int, default=1)
 p.add_argument("--config", default="C2")
 p.add_argument("--frames", type=int, default=0)

@@ -89,7 +89,7 @@ def test_jitter_matches_golden_and_oracle(nsl):
 
 
 # ------------------------------------------------------------------ C1 full frames
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("layout", [0, 1, 3])
 @pytest.mark.parametrize("kw", [{}, {"single_light": True}, {"perspective": True},
                                 {"perspective": True, "single_light": True}])
 def test_parity_C1(nsl, layout, kw):
@@ -117,9 +117,10 @@ def test_parity_C1_corner_f16(nsl):
 def test_layouts_agree_bitwise(nsl):
     w = I.make_workload("C2", frames=[3])
     a = run(nsl, w, layout=0)
-    b = run(nsl, w, layout=1)
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y)
+    for lay in (1, 3):
+        b = run(nsl, w, layout=lay)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
 
 
 # ------------------------------------------------------------------ C2/C3 (frames 0 and 30), C4, C5 (subsampled)
@@ -216,7 +217,7 @@ def test_device_upload_reports_invalid_values(nsl):
     d = torch.ones((8, 8, 8), device="cuda")
     d[1, 2, 3] = float("nan")
     d[4, 4, 4] = -2.0
-    for layout in (0, 1, 2):
+    for layout in (0, 1, 2, 3):
         v = nsl.Volume(g, d, layout)
         assert v.check() == 2
     v = nsl.Volume(g, torch.ones((8, 8, 8), device="cuda"), 1)
