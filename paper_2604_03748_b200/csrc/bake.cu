@@ -98,14 +98,14 @@ __global__ void bake_setup_kernel(const FrameIn* __restrict__ in, const FramePar
 }
 
 // Number of leading light samples (B4, jittered offset o3 = u3 h_bl) that can be
-// nonzero: estimate of the support count (+1 slack) capped by the region count,
-// then shrunk with exact prescribed-op support tests.
+// nonzero: estimate of the region count (+1 slack; the region lies inside the
+// support, so its estimate never exceeds the support's), then shrunk with exact
+// prescribed-op support tests.
 __device__ __forceinline__ int bake_light_bound(const Vol& v, float ux, float uy, float uz, float lx, float ly,
-                                                float lz, float hbl, float o3, float u3, const float lim[3],
-                                                const float ilh[3], const float reg[3]) {
-    const float ms = fminf(fminf((lim[0] - ux) * ilh[0], (lim[1] - uy) * ilh[1]), (lim[2] - uz) * ilh[2]);
+                                                float lz, float hbl, float o3, float u3, const float ilh[3],
+                                                const float reg[3]) {
     const float mr = fminf(fminf((reg[0] - ux) * ilh[0], (reg[1] - uy) * ilh[1]), (reg[2] - uz) * ilh[2]);
-    float m = fminf(floorf(ms - u3), floorf(mr - u3)) + 2.0f;
+    float m = floorf(mr - u3) + 2.0f;
     m = fminf(fmaxf(m, 0.0f), 16777216.0f);
     while (m > 0.0f) {
         const float s = __fmaf_rn(m - 1.0f, hbl, o3);
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kBakeThreads) bake_kernel(const FrameParams* _
                 const float lx = bf.Lg[l][0], ly = bf.Lg[l][1], lz = bf.Lg[l][2];
                 float reg[3];
                 bake_region(sp, bf, v, l, z, reg);
-                const int m = bake_light_bound(v, x, y, z, lx, ly, lz, hbl, o3, u4[3], bf.lim[l], bf.ilh[l], reg);
+                const int m = bake_light_bound(v, x, y, z, lx, ly, lz, hbl, o3, u4[3], bf.ilh[l], reg);
                 float sum = 0.0f;
                 float jf = 0.0f;
                 for (int j = 1; j <= m; ++j, jf += 1.0f) {

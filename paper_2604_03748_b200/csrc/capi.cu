@@ -466,21 +466,56 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     nsl_volume* vol = nullptr;
     std::vector<int32_t> fv((size_t)F, 0);
     nsl_status st = nsl_volume_upload(g, host_density, 0, layout, vstore, vb, stream, &vol);
+    // Frame chunks: chunk c marches on `stream` while chunk c-1's results stream back to the
+    // host on a side stream (PCIe D2H overlaps the march; the copies dominate for fp32 maps).
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> evs;
+    const size_t npf = (size_t)cams[0].width * cams[0].height;
+    const int nchunks = F < 8 ? F : 8, per = (F + nchunks - 1) / nchunks;
     if (st == NSL_OK) {
-        const nsl_volume* vp = vol;
-        st = nsl_guiding_map_batch(&vp, 1, fv.data(), cams, lights, n_lights, light_mode, med, m, frame_ids, F, d_rgbt,
-                                   d_depth, nullptr, stream);
+        e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+        if (e != cudaSuccess) st = cuda_fail(e, "cudaStreamCreate(side)");
     }
-    if (st == NSL_OK) {
-        e = cudaMemcpyAsync(host_rgbt, d_rgbt, npix * 16, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(host_depth, d_depth, npix * 4, cudaMemcpyDeviceToHost, s);
+    const nsl_volume* vp = vol;
+    for (int f0 = 0; st == NSL_OK && f0 < F; f0 += per) {
+        const int n = F - f0 < per ? F - f0 : per;
+        st = batch_impl(&vp, 1, fv.data(), cams + f0, lights ? lights + (size_t)f0 * n_lights : nullptr, n_lights,
+                        light_mode, med, m, frame_ids ? frame_ids + f0 : nullptr, n, d_rgbt + (size_t)f0 * npf * 4,
+                        d_depth + (size_t)f0 * npf, nullptr, nullptr, stream);
+        if (st != NSL_OK) break;
+        cudaEvent_t ev = nullptr;
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) {
+            evs.push_back(ev);
+            e = cudaEventRecord(ev, s);
+        }
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(host_rgbt + (size_t)f0 * npf * 4, d_rgbt + (size_t)f0 * npf * 4, (size_t)n * npf * 16,
+                                cudaMemcpyDeviceToHost, side);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(host_depth + (size_t)f0 * npf, d_depth + (size_t)f0 * npf, (size_t)n * npf * 4,
+                                cudaMemcpyDeviceToHost, side);
         if (e != cudaSuccess) st = cuda_fail(e, "result download");
+    }
+    if (side) {                                   // `stream` resumes after the last copy
+        cudaEvent_t done = nullptr;
+        if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess) {
+            evs.push_back(done);
+            cudaEventRecord(done, side);
+            cudaStreamWaitEvent(s, done, 0);
+        } else {
+            cudaStreamSynchronize(side);
+        }
     }
     cudaFreeAsync(dout, s);
     cudaFreeAsync(vstore, s);
     nsl_volume_release(vol);
+    cudaError_t es = cudaStreamSynchronize(s);
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    if (side) cudaStreamDestroy(side);
     if (st != NSL_OK) return st;
-    NSL_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    if (es != cudaSuccess) return cuda_fail(es, "cudaStreamSynchronize");
     return NSL_OK;
 }
 

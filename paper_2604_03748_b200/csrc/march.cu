@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
                         float ra[3], rb[3];
                         march_region(sp, v, 1, z, ra);
                         march_region(sp, v, 2, z, rb);
-                        ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1], ra);
-                        mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2], rb);
+                        ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.ilh[1], ra);
+                        mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.ilh[2], rb);
                     }
                     if (COUNT) c_tl += (uint32_t)(ma + mb);
                     float sa, sb;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
                                 M = 0;
                                 float rl[3];
                                 march_region(sp, v, l, z, rl);
-                                mm = light_bound(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l], rl);
+                                mm = light_bound(v, x, y, z, lx, ly, lz, mc.hl, sp.ilh[l], rl);
                             }
                             if (COUNT) c_tl += (uint32_t)mm;
                             const float sum = light_sum<LAYOUT, COUNT>(v, x, y, z, lx, ly, lz, mc.hl, mm, c_gath);

@@ -232,15 +232,16 @@ __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy,
 }
 
 // Fast-path bound on the light samples that can be nonzero: the estimate of the
-// support count plus one (>= the exact count), capped by the occupied-box
-// count, then shrunk with exact prescribed-op tests until the last sample is in
+// region count plus one (>= the exact count of in-region samples), then shrunk with exact prescribed-op tests until the last sample is in
 // support (so every index is valid).  Every in-support sample inside the
 // occupied box is covered, hence the sum equals the canonical one (C8).
+// The region (occupied box or slab box) lies inside the support on every axis and the
+// estimate (plane - u) * ilh is monotone in the plane, so the region's estimate is never
+// above the support's: it alone bounds the count.
 __device__ __forceinline__ int light_bound(const Vol& v, float ux, float uy, float uz, float lx, float ly, float lz,
-                                           float hl, const float lim[3], const float ilh[3], const float alim[3]) {
-    const float ms = fminf(fminf((lim[0] - ux) * ilh[0], (lim[1] - uy) * ilh[1]), (lim[2] - uz) * ilh[2]);
+                                           float hl, const float ilh[3], const float alim[3]) {
     const float mb = fminf(fminf((alim[0] - ux) * ilh[0], (alim[1] - uy) * ilh[1]), (alim[2] - uz) * ilh[2]);
-    float m = fminf(floorf(ms), floorf(mb)) + 1.0f;
+    float m = floorf(mb) + 1.0f;
     m = fminf(fmaxf(m, 0.0f), 16777216.0f);
     while (m > 0.0f) {
         const float s = __fmul_rn(m, hl);

@@ -333,9 +333,10 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
 // the per-CTA shared-memory budget (default 16 KB; NSL_OCC_BUDGET / NSL_OCC_SHIFT
 // override for experiments).
 OccGeom occ_geom(int nx, int ny, int nz) {
+    constexpr long kMaxMask = 256 * 1024;   // hard cap (the march reads the mask through L1)
     long budget = 16 * 1024;   // ~33 blocks per axis; measured best on C2 (profiles/r1_sweep.txt)
     if (const char* e = getenv("NSL_OCC_BUDGET")) budget = atol(e);
-    if (budget > 16 * 1024) budget = 16 * 1024;   // <= 2^17 blocks: the march's fp32 block index stays exact
+    if (budget > kMaxMask) budget = kMaxMask;
     int forced = 0;
     if (const char* e = getenv("NSL_OCC_SHIFT")) forced = atoi(e);
     OccGeom g{};
@@ -353,7 +354,7 @@ OccGeom occ_geom(int nx, int ny, int nz) {
         g.info_off = (g.rows * g.rowwords + 3) / 4 * 4;
         g.scratch_words = g.info_off + 4 * g.rows;
         if ((forced > 0 && s >= forced) || (long)g.words * 4 <= budget) {
-            if ((long)g.words * 4 <= 16 * 1024 && g.nbz <= 1024) break;
+            if ((long)g.words * 4 <= kMaxMask && g.nbz <= 1024) break;
         }
     }
     return g;
