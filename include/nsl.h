@@ -266,9 +266,13 @@ nsl_status nsl_relight(const nsl_camera* cams, int32_t F, const float* maps, con
 /* End-to-end convenience call with HOST buffers: uploads the host density
  * grid, lays it out, marches the F frames and copies the results back into
  * host out_rgbt (F*H*W*4 floats) / out_depth (F*H*W floats); synchronises
- * `stream` before returning.  All device memory is transient (stream-ordered
- * pool).  Host buffers may be pageable; pinned memory makes the copies
- * asynchronous DMA. */
+ * `stream` before returning.  The frames are marched in chunks on `stream`
+ * while the previous chunk's results stream back on an internal side stream.
+ * The density is validated on the device (the build kernel's count): a
+ * non-finite or negative value makes the call return NSL_ERR_INVALID_ARG
+ * (the host outputs are then unspecified).  All device memory is transient
+ * (stream-ordered pool).  Host buffers may be pageable; pinned memory makes
+ * the copies asynchronous DMA. */
 nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_density, int32_t layout,
                                 const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
                                 int32_t light_mode, const nsl_medium* med, const nsl_march* m,

@@ -268,8 +268,20 @@ size_t nsl_volume_bytes(const nsl_grid_desc* g, int32_t layout) {
     return tail_offset(g, layout) + kTail;
 }
 
+static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* density, int32_t density_on_device,
+                                     int32_t layout, void* device_storage, size_t storage_bytes, nsl_stream stream,
+                                     nsl_volume** out, bool validate_host);
+
 nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32_t density_on_device, int32_t layout,
                              void* device_storage, size_t storage_bytes, nsl_stream stream, nsl_volume** out) {
+    return volume_upload_impl(g, density, density_on_device, layout, device_storage, storage_bytes, stream, out, true);
+}
+
+// validate_host = false: host values are checked on the device only (the build kernel's
+// invalid-voxel count); the caller must read it (nsl_guiding_map_host does, after its sync).
+static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* density, int32_t density_on_device,
+                                     int32_t layout, void* device_storage, size_t storage_bytes, nsl_stream stream,
+                                     nsl_volume** out, bool validate_host) {
     g_err.clear();
     if (nsl_status st = check_grid(g)) return st;
     if (nsl_status st = check_layout(layout)) return st;
@@ -280,7 +292,7 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
     if (storage_bytes < need) return fail(NSL_ERR_INVALID_ARG, "storage_bytes %zu < required %zu", storage_bytes, need);
     const size_t n = (size_t)g->nx * g->ny * g->nz;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (!density_on_device) {
+    if (!density_on_device && validate_host) {
         for (size_t i = 0; i < n; ++i)
             if (!(density[i] >= 0.0f) || !std::isfinite(density[i]))
                 return fail(NSL_ERR_INVALID_ARG, "density[%zu] = %g is not finite and >= 0", i, (double)density[i]);
@@ -465,7 +477,7 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     float* d_depth = d_rgbt + npix * 4;
     nsl_volume* vol = nullptr;
     std::vector<int32_t> fv((size_t)F, 0);
-    nsl_status st = nsl_volume_upload(g, host_density, 0, layout, vstore, vb, stream, &vol);
+    nsl_status st = volume_upload_impl(g, host_density, 0, layout, vstore, vb, stream, &vol, false);
     // Frame chunks: chunk c marches on `stream` while chunk c-1's results stream back to the
     // host on a side stream (PCIe D2H overlaps the march; the copies dominate for fp32 maps).
     cudaStream_t side = nullptr;
@@ -508,6 +520,8 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
             cudaStreamSynchronize(side);
         }
     }
+    unsigned long long n_invalid = 0;
+    if (vol) cudaMemcpyAsync(&n_invalid, vol->invalid, sizeof n_invalid, cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(dout, s);
     cudaFreeAsync(vstore, s);
     nsl_volume_release(vol);
@@ -516,6 +530,7 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     if (side) cudaStreamDestroy(side);
     if (st != NSL_OK) return st;
     if (es != cudaSuccess) return cuda_fail(es, "cudaStreamSynchronize");
+    if (n_invalid) return fail(NSL_ERR_INVALID_ARG, "density has %llu non-finite or negative values", n_invalid);
     return NSL_OK;
 }
 

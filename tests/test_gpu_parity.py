@@ -199,16 +199,33 @@ def test_frame_sharding_is_bitwise_invariant(nsl):
             assert np.array_equal(part[1], full[1][frames])
 
 
-def test_host_api_equals_device_api(nsl):
+@pytest.mark.parametrize("frames,layout", [([5, 6], 1), (list(range(0, 55, 5)), 3)])
+def test_host_api_equals_device_api(nsl, frames, layout):
+    """The chunked host pipeline (11 frames -> chunks 2,2,2,2,2,1 with overlapped D2H) returns
+    exactly the device API's maps."""
     import torch
-    w = I.make_workload("C2", frames=[5, 6])
-    dev = run(nsl, w, debug=False)
+    w = I.make_workload("C2", frames=frames)
+    F = len(frames)
+    dev = run(nsl, w, layout=layout, debug=False)
     dens = torch.from_numpy(w.volume(0)).pin_memory()
-    hr = torch.empty((2, w.height, w.width, 4)).pin_memory()
-    hd = torch.empty((2, w.height, w.width)).pin_memory()
-    nsl.guiding_map_host(w.grid, dens, 1, w.cameras, w.lights, w.light_mode, w.medium, w.march, w.frame_ids, hr, hd)
+    hr = torch.empty((F, w.height, w.width, 4)).pin_memory()
+    hd = torch.empty((F, w.height, w.width)).pin_memory()
+    nsl.guiding_map_host(w.grid, dens, layout, w.cameras, w.lights, w.light_mode, w.medium, w.march, w.frame_ids,
+                         hr, hd)
     assert np.array_equal(hr.numpy(), dev[0])
     assert np.array_equal(hd.numpy(), dev[1])
+
+
+def test_host_api_rejects_invalid_density(nsl):
+    import torch
+    w = I.make_workload("C1")
+    dens = torch.from_numpy(w.volume(0).copy())
+    dens[3, 4, 5] = float("nan")
+    hr = torch.empty((1, w.height, w.width, 4))
+    hd = torch.empty((1, w.height, w.width))
+    with pytest.raises(nsl.NslError, match="non-finite or negative"):
+        nsl.guiding_map_host(w.grid, dens, 3, w.cameras, w.lights, w.light_mode, w.medium, w.march, w.frame_ids,
+                             hr, hd)
 
 
 def test_device_upload_reports_invalid_values(nsl):
