@@ -21,8 +21,8 @@ namespace nsl {
 namespace {
 
 // Tile culling (exact, orthographic views): every ray of a tile is parallel to D_g with
-// its origin within tile_r of the centre ray; if the centre ray misses a box expanded by
-// tile_r, no sample of the tile lies in the box.  bit 0: misses the occupied box (FAST:
+// its origin within the tile radius r of the centre ray; if the centre ray misses a box expanded by
+// r, no sample of the tile lies in the box.  bit 0: misses the occupied box (FAST:
 // every sample outside it is exactly 0); bit 1: misses the support box (DEBUG/COUNTED,
 // which report n_lo/n_hi: C5).  One thread per (frame, tile).
 __global__ void tile_cull_kernel(const FrameParams* __restrict__ fps, int F, int tiles_x, int tiles,
@@ -37,7 +37,13 @@ __global__ void tile_cull_kernel(const FrameParams* __restrict__ fps, int F, int
     const float cx = (float)(tx * kTileW) + 0.5f * (kTileW - 1), cy = (float)(ty * kTileH) + 0.5f * (kTileH - 1);
     const float c[3] = {fmaf(cy, sp.Ey[0], fmaf(cx, sp.Ex[0], sp.B[0])), fmaf(cy, sp.Ey[1], fmaf(cx, sp.Ex[1], sp.B[1])),
                         fmaf(cy, sp.Ey[2], fmaf(cx, sp.Ex[2], sp.B[2]))};
-    const float rr = sp.tile_r;
+    // tile radius in index units: half extents of the tile (+1 pixel) along E_x, E_y, +1 for rounding
+    float rr = 0.0f;
+    for (int q = 0; q < 3; ++q) {
+        const float e = (0.5f * kTileW + 1.0f) * fabsf(sp.Ex[q]) + (0.5f * kTileH + 1.0f) * fabsf(sp.Ey[q]);
+        rr = fmaf(e, e, rr);
+    }
+    rr = sqrtf(rr) * 1.001f + 1.0f;
     uint8_t bits = 0;
     for (int box = 0; box < 2; ++box) {
         float t0 = -3.0e38f, t1 = 3.0e38f;
@@ -68,8 +74,8 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
     pdl_wait();                        // launched with PDL after frame_setup / tile_cull: their outputs
     const FrameParams& sp = fps[f];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int px = tx * kTileW + (warp & 1) * 8 + (lane & 7);
-    const int py = ty * kTileH + (warp >> 1) * 4 + (lane >> 3);
+    const int px = tx * kTileW + (warp % kWarpsX) * kWarpW + lane % kWarpW;
+    const int py = ty * kTileH + (warp / kWarpsX) * kWarpH + lane / kWarpW;
     const bool valid = px < W && py < H;
     const size_t o = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
 

@@ -66,14 +66,13 @@ struct FrameParams {
     float invD[3];             // ortho: 1/D_g per axis (0 where D_g = 0)
     float lim[4][3];           // light march exit plane per axis (n+1, 0, or 3e38 if L = 0)
     float ilh[4][3];           // 1 / (L_g * h_l) per axis (1 if L = 0)
-    float tile_r;              // ortho: half-diagonal of a 16x16 pixel tile in index units
     int32_t pair12;            // guide set: light 2 == -light 1 bit-exactly (paired side march)
     // occupied box [alo, ahi) in padded-index positions: every sample outside it is exactly 0
     float alo[3], ahi[3];
     float alim[4][3];          // light march exit plane of the occupied box per axis
     int32_t slab_off;          // word offset of the slab boxes in the staged occupancy region
     int32_t lz0;               // bit l: L_g,l,z == 0 exactly (the march of light l stays in its z slab)
-    int32_t pad2[2];
+    int32_t pad2[3];
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 

@@ -10,10 +10,19 @@
 namespace nsl {
 namespace {
 
-#ifndef NSL_TILEH
-#define NSL_TILEH 8      // CTA tile 16 x NSL_TILEH pixels (warps of 8x4): 8 -> 128 threads (measured best), 16 -> 256
+#ifndef NSL_TILEW
+#define NSL_TILEW 16     // CTA tile NSL_TILEW x NSL_TILEH pixels, one thread per pixel
 #endif
-constexpr int kTileW = 16, kTileH = NSL_TILEH, kThreads = 2 * NSL_TILEH * 8;
+#ifndef NSL_TILEH
+#define NSL_TILEH 8      // 16 x 8 -> 128 threads (measured best; 16 x 16 -> 256)
+#endif
+#ifndef NSL_WARPW
+#define NSL_WARPW 8      // warp footprint NSL_WARPW x (32 / NSL_WARPW) pixels (8 x 4 measured best)
+#endif
+constexpr int kTileW = NSL_TILEW, kTileH = NSL_TILEH, kThreads = NSL_TILEW * NSL_TILEH;
+constexpr int kWarpW = NSL_WARPW, kWarpH = 32 / NSL_WARPW, kWarpsX = NSL_TILEW / NSL_WARPW;
+static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (32 / NSL_WARPW) == 0,
+              "CTA tile must be a whole number of warp footprints");
 #ifndef NSL_MINB
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
                      // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)

@@ -164,15 +164,6 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
             p.lim[l][q] = L > 0.0f ? p.supp[q] : (L < 0.0f ? 0.0f : 3.0e38f);
             p.ilh[l][q] = L != 0.0f ? 1.0f / (L * mc.hl) : 1.0f;
         }
-    {
-        // 16x16 tile: half extents 8|Ex| + 8|Ey| (index units), plus one pixel of slack
-        double rr = 0.0;
-        for (int q = 0; q < 3; ++q) {
-            const double e = 9.0 * (fabs((double)p.Ex[q]) + fabs((double)p.Ey[q]));
-            rr += e * e;
-        }
-        p.tile_r = (float)sqrt(rr) + 1.0f;
-    }
     bool pair = mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3;
     for (int q = 0; q < 3; ++q) pair = pair && (p.Lg[2][q] == -p.Lg[1][q]);
     p.pair12 = pair ? 1 : 0;
