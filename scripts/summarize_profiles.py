@@ -19,6 +19,9 @@ round_tag = tag[:2]
 shutil.copy(os.path.join(G, "bench.json"), os.path.join(P, f"{round_tag}_bench.json"))
 shutil.copy(os.path.join(G, "bench_ref.json"), os.path.join(P, f"{round_tag}_bench_reference.json"))
 shutil.copy(os.path.join(G, "gpu_tests.log"), os.path.join(P, f"{round_tag}_gpu_tests.log"))
+for extra in ("bench_relight.json", "bench_bake.json", "smoke.log"):
+    if os.path.exists(os.path.join(G, extra)):
+        shutil.copy(os.path.join(G, extra), os.path.join(P, f"{round_tag}_{extra}"))
 shutil.copy(os.path.join(G, "launches.csv"), os.path.join(P, f"{round_tag}_launches.csv"))
 rep = os.path.join(P, f"{round_tag}_march_kernel_full.ncu-rep")
 shutil.copy(os.path.join(G, f"prof_march_{tag}.ncu-rep"), rep)
@@ -71,7 +74,7 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio"]
-lines = ["# ncu --set full of march_kernel<QUAD_F32, ORTHO, FAST> on C2 (60 frames 512^2 over 128^3, guide lights)",
+lines = ["# ncu --set full of march_kernel<OCT_F32, ORTHO, FAST> on C2 (60 frames 512^2 over 128^3, guide lights)",
          "# command: ncu --set full --clock-control none --import-source on -k regex:march_kernel -s 2 -c 1 "
          "python scripts/profile_march.py", f"# report: {os.path.relpath(rep, ROOT)}", ""]
 for k in keys:
@@ -81,7 +84,7 @@ open(os.path.join(P, f"{round_tag}_ncu_march_summary.txt"), "w").write("\n".join
 mult = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}
 traffic = (float(d["dram__bytes_read.sum"][1]) * mult[d["dram__bytes_read.sum"][0]]
            + float(d["dram__bytes_write.sum"][1]) * mult[d["dram__bytes_write.sum"][0]])
-json.dump({"config": "C2", "layout": "quad_f32", "frames": 60, "dram_bytes_per_launch": traffic,
+json.dump({"config": "C2", "layout": "oct_f32", "frames": 60, "dram_bytes_per_launch": traffic,
            "source": f"{os.path.relpath(rep, ROOT)} (dram__bytes_read.sum + dram__bytes_write.sum)"},
           open(os.path.join(P, "ncu_march_traffic.json"), "w"), indent=1)
 print("\n".join(lines))
