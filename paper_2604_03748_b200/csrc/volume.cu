@@ -108,24 +108,34 @@ __device__ __forceinline__ void layout_corner_f16_cta(const Raw& r, uint4* __res
 }
 
 // OCT: the QUAD float4 of planes k and k+1 of cell (i, j, k) in one 32-B element (k <= nz).
-__device__ __forceinline__ void layout_oct_cta(const Raw& r, float4* __restrict__ out, int pb, int kb, int kstep) {
+// Each thread walks a run of kOctRun consecutive planes carrying plane k+1's quad into the
+// next element (4 raw loads per element instead of 8) and writes each element with one
+// 256-bit store.
+constexpr int kOctRun = 8;
+__device__ __forceinline__ void st256(float* p, const float (&c)[8]) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(c[0]), "f"(c[1]),
+                 "f"(c[2]), "f"(c[3]), "f"(c[4]), "f"(c[5]), "f"(c[6]), "f"(c[7])
+                 : "memory");
+}
+__device__ __forceinline__ void layout_oct_cta(const Raw& r, float* __restrict__ out, int pb, int kb, int kstep) {
     const int qx = r.nx + 1, qy = r.ny + 1, plane = qx * qy;
     const int e2 = pb * 256 + threadIdx.x;
     if (e2 >= plane) return;
     const int i = e2 % qx, j = e2 / qx;
-    for (int k = kb; k < r.nz + 1; k += kstep) {
-        float c[2][4];
+    for (int k0 = kb * kOctRun; k0 < r.nz + 1; k0 += kstep * kOctRun) {
+        const int k1 = min(k0 + kOctRun, r.nz + 1);
+        float q[4] = {r.at(i, j, k0), r.at(i + 1, j, k0), r.at(i, j + 1, k0), r.at(i + 1, j + 1, k0)};
+        for (int k = k0; k < k1; ++k) {
+            const float n[4] = {r.at(i, j, k + 1), r.at(i + 1, j, k + 1), r.at(i, j + 1, k + 1),
+                                r.at(i + 1, j + 1, k + 1)};
+            // (c000, c100 - c000, c010, c110 - c010 | the same for plane k+1): the differences are
+            // rounded exactly as the sampler's lerp rounds them (bit-identical to LINEAR)
+            const float c[8] = {q[0], __fsub_rn(q[1], q[0]), q[2], __fsub_rn(q[3], q[2]),
+                                n[0], __fsub_rn(n[1], n[0]), n[2], __fsub_rn(n[3], n[2])};
+            st256(out + 8 * ((size_t)k * plane + e2), c);
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            c[t][0] = r.at(i, j, k + t);
-            c[t][1] = r.at(i + 1, j, k + t);
-            c[t][2] = r.at(i, j + 1, k + t);
-            c[t][3] = r.at(i + 1, j + 1, k + t);
+            for (int t = 0; t < 4; ++t) q[t] = n[t];
         }
-        float4* d = out + 2 * ((size_t)k * plane + e2);
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-            d[t] = make_float4(c[t][0], __fsub_rn(c[t][1], c[t][0]), c[t][2], __fsub_rn(c[t][3], c[t][2]));
     }
 }
 
@@ -254,7 +264,7 @@ __global__ void __launch_bounds__(256, 6) volume_build_kernel(Raw r, void* __res
     if (LAYOUT == kLinearF32) layout_linear_cta(r, static_cast<float*>(out), pb, kb, kstep);
     if (LAYOUT == kQuadF32) layout_quad_cta(r, static_cast<float4*>(out), pb, kb, kstep);
     if (LAYOUT == kCornerF16) layout_corner_f16_cta(r, static_cast<uint4*>(out), pb, kb, kstep);
-    if (LAYOUT == kOctF32) layout_oct_cta(r, static_cast<float4*>(out), pb, kb, kstep);
+    if (LAYOUT == kOctF32) layout_oct_cta(r, static_cast<float*>(out), pb, kb, kstep);
 }
 
 // The occupancy region [mask: words][slab_min: nbz x (bx, by)][slab_max: nbz x (bx, by)], the
@@ -375,7 +385,9 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
     const int plane = v.layout == kLinearF32 ? (v.nx + 2) * (v.ny + 2) : (v.nx + 1) * (v.ny + 1);
     const int planes = v.layout == kCornerF16 || v.layout == kOctF32 ? v.nz + 1 : v.nz + 2;
     const int plane_blocks = (plane + 255) / 256;
-    int kstep = v.layout == kQuadF32 ? (planes + kQuadPlanes - 1) / kQuadPlanes : planes;
+    int kstep = v.layout == kQuadF32  ? (planes + kQuadPlanes - 1) / kQuadPlanes
+                : v.layout == kOctF32 ? (planes + kOctRun - 1) / kOctRun
+                                      : planes;
     const long max_layout_ctas = 2000000000L - v.og.rows;
     if ((long)plane_blocks * kstep > max_layout_ctas) kstep = (int)(max_layout_ctas / plane_blocks);
     const unsigned grid = (unsigned)(v.og.rows + (long)plane_blocks * kstep);
