@@ -122,6 +122,7 @@ class March:
     seed: int = 0x26040374
     guide_axis: tuple = (0.0, 0.0, 1.0)
     front_identity: int = 1   # allow the GPU front-light shortcut (C9); oracle ignores
+    light_model: int = 0      # 0 canonical light march (C8), 1 transmittance volume
 
 
 @dataclass

@@ -59,7 +59,7 @@ class OrcMarch(ctypes.Structure):
                 ("max_steps", ctypes.c_int32), ("depth_tau", ctypes.c_float),
                 ("t_min", ctypes.c_float), ("opacity_form", ctypes.c_int32),
                 ("jitter", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("guide_axis", ctypes.c_float * 3)]
+                ("guide_axis", ctypes.c_float * 3), ("light_model", ctypes.c_int32)]
 
 
 class OrcFrameConstants(ctypes.Structure):
@@ -128,7 +128,8 @@ def _medium(m) -> OrcMedium:
 
 def _march(m) -> OrcMarch:
     return OrcMarch(m.step, m.light_step, m.max_steps, m.depth_tau, m.t_min, m.opacity_form,
-                    m.jitter, m.seed & 0xFFFFFFFFFFFFFFFF, (ctypes.c_float * 3)(*m.guide_axis))
+                    m.jitter, m.seed & 0xFFFFFFFFFFFFFFFF, (ctypes.c_float * 3)(*m.guide_axis),
+                    getattr(m, "light_model", 0))
 
 
 def hg(g: float, cos_theta: float) -> float:
@@ -337,3 +338,61 @@ def relight(cam, maps8, lights, bg=(0.0, 0.0, 0.0), emis=(0.0, 0.0, 0.0), depth=
     if rc:
         raise ValueError("orc_relight rejected its arguments")
     return {"out": out, "margin": margin, "pixels": np.arange(n, dtype=np.int64) if pix is None else pix}
+
+
+# ------------------------------------------------------------------ NEXT-4 transmittance volume
+class OrcTvLattice(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_double * 3), ("dhat", ctypes.c_double * 3), ("ell", ctypes.c_double),
+                ("e1", ctypes.c_double * 3), ("e2", ctypes.c_double * 3),
+                ("a0", ctypes.c_int64), ("b0", ctypes.c_int64), ("k0", ctypes.c_int64),
+                ("A", ctypes.c_int64), ("B", ctypes.c_int64), ("K", ctypes.c_int64)]
+
+
+def _load_tv():
+    L = _load()
+    if not getattr(L, "_tv_ready", False):
+        P = ctypes.POINTER
+        L.orc_tv_lattice_compute.argtypes = [P(OrcGrid), P(ctypes.c_float), ctypes.c_float, P(OrcTvLattice)]
+        L.orc_tv_build.argtypes = [P(OrcGrid), ctypes.c_void_p, DENSITY_FN, ctypes.c_void_p, P(OrcTvLattice),
+                                   ctypes.c_float, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_tv_lookup.argtypes = [P(OrcTvLattice), ctypes.c_void_p, P(ctypes.c_float)]
+        L.orc_tv_lookup.restype = ctypes.c_double
+        L.orc_light_tau.argtypes = [P(OrcGrid), ctypes.c_void_p, DENSITY_FN, ctypes.c_void_p, P(ctypes.c_float),
+                                    P(ctypes.c_float), ctypes.c_float, ctypes.c_double]
+        L.orc_light_tau.restype = ctypes.c_double
+        L._tv_ready = True
+    return L
+
+
+def tv_lattice(grid, Lg, hl: float) -> OrcTvLattice:
+    """V2 lattice of the light step vector hl * Lg (index units)."""
+    lat = OrcTvLattice()
+    if _load_tv().orc_tv_lattice_compute(ctypes.byref(_grid(grid)), (ctypes.c_float * 3)(*Lg), hl, ctypes.byref(lat)):
+        raise ValueError("orc_tv_lattice_compute rejected its arguments")
+    return lat
+
+
+def tv_build(grid, vals, lat: OrcTvLattice, hl: float, kappa: float, density_fn=None):
+    """V3/V4: (tau_plus, tau_minus) as [B, K, A] float64 arrays."""
+    shape = (lat.B, lat.K, lat.A)
+    tp, tm = np.zeros(shape, np.float64), np.zeros(shape, np.float64)
+    v = None if vals is None else np.ascontiguousarray(vals, dtype=np.float32)
+    cb = DENSITY_FN(density_fn) if density_fn is not None else DENSITY_FN()
+    if _load_tv().orc_tv_build(ctypes.byref(_grid(grid)), None if v is None else v.ctypes.data, cb, None,
+                               ctypes.byref(lat), hl, kappa, tp.ctypes.data, tm.ctypes.data):
+        raise ValueError("orc_tv_build rejected its arguments")
+    return tp, tm
+
+
+def tv_lookup(lat: OrcTvLattice, tau: np.ndarray, U) -> float:
+    t = np.ascontiguousarray(tau, dtype=np.float64)
+    return _load_tv().orc_tv_lookup(ctypes.byref(lat), t.ctypes.data, (ctypes.c_float * 3)(*U))
+
+
+def light_tau(grid, vals, U, Lg, hl: float, kappa: float, density_fn=None) -> float:
+    """C8's optical depth from U (the canonical light march)."""
+    v = None if vals is None else np.ascontiguousarray(vals, dtype=np.float32)
+    cb = DENSITY_FN(density_fn) if density_fn is not None else DENSITY_FN()
+    return _load_tv().orc_light_tau(ctypes.byref(_grid(grid)), None if v is None else v.ctypes.data, cb, None,
+                                    (ctypes.c_float * 3)(*U), (ctypes.c_float * 3)(*Lg), hl, kappa)
+

@@ -9,6 +9,7 @@
 #include "nsl_oracle.h"
 
 #include <math.h>
+#include <stdlib.h>
 #include <stddef.h>
 #include <string.h>
 
@@ -235,6 +236,117 @@ static int64_t primary_upper_bound(const orc_grid* g, const float O[3], const fl
     return (int64_t)nmax;
 }
 
+/* ================================================================ NEXT-4: transmittance volume
+ * DESIGN.md §12 (V2-V5), written out plainly in fp64: the lattice of the light
+ * step vector, the line sums toward and away from the light, and the trilinear
+ * lookup.  Test infrastructure only, like everything in this file. */
+int orc_tv_lattice_compute(const orc_grid* g, const float Lg[3], float hl, orc_tv_lattice* L) {
+    if (!g || !Lg || !L || !(hl > 0.0f)) return 1;
+    for (int a = 0; a < 3; ++a) L->d[a] = (double)hl * (double)Lg[a];
+    L->ell = norm3(L->d);
+    if (!(L->ell > 0.0)) return 1;
+    for (int a = 0; a < 3; ++a) L->dhat[a] = L->d[a] / L->ell;
+    const double zh[3] = {0.0, 0.0, 1.0}, xh[3] = {1.0, 0.0, 0.0};
+    double c[3];
+    cross3(L->dhat, zh, c);
+    if (norm3(c) < 1e-6) cross3(L->dhat, xh, c);
+    const double nc = norm3(c);
+    for (int a = 0; a < 3; ++a) L->e1[a] = c[a] / nc;
+    cross3(L->dhat, L->e1, L->e2);
+    const double n[3] = {g->nx + 1.0, g->ny + 1.0, g->nz + 1.0};
+    double amin = 1e300, amax = -1e300, bmin = 1e300, bmax = -1e300, kmin = 1e300, kmax = -1e300;
+    for (int corner = 0; corner < 8; ++corner) {
+        const double p[3] = {(corner & 1) ? n[0] : 0.0, (corner & 2) ? n[1] : 0.0, (corner & 4) ? n[2] : 0.0};
+        const double a = dot3(p, L->e1), b = dot3(p, L->e2), k = dot3(p, L->dhat) / L->ell;
+        if (a < amin) amin = a;
+        if (a > amax) amax = a;
+        if (b < bmin) bmin = b;
+        if (b > bmax) bmax = b;
+        if (k < kmin) kmin = k;
+        if (k > kmax) kmax = k;
+    }
+    L->a0 = (int64_t)floor(amin) - 1;
+    L->A = (int64_t)ceil(amax) - L->a0 + 2;
+    L->b0 = (int64_t)floor(bmin) - 1;
+    L->B = (int64_t)ceil(bmax) - L->b0 + 2;
+    L->k0 = (int64_t)floor(kmin) - 1;
+    L->K = (int64_t)ceil(kmax) - L->k0 + 2;
+    return 0;
+}
+
+int64_t orc_tv_index(const orc_tv_lattice* L, int64_t i, int64_t j, int64_t k) { return (j * L->K + k) * L->A + i; }
+
+int orc_tv_build(const orc_grid* g, const float* vals, orc_density_fn density_fn, void* density_ctx,
+                 const orc_tv_lattice* L, float hl, double kappa, double* tau_plus, double* tau_minus) {
+    if (!g || (!vals && !density_fn) || !L || !tau_plus || !tau_minus) return 1;
+    const dens_t dens = {g, vals, density_fn, density_ctx};
+    double* rho = (double*)malloc(sizeof(double) * (size_t)L->K);
+    if (!rho) return 1;
+    for (int64_t j = 0; j < L->B; ++j)
+        for (int64_t i = 0; i < L->A; ++i) {
+            for (int64_t k = 0; k < L->K; ++k) {          /* V3 */
+                float P[3];
+                for (int a = 0; a < 3; ++a)
+                    P[a] = (float)((double)(L->a0 + i) * L->e1[a] + (double)(L->b0 + j) * L->e2[a] +
+                                   (double)(L->k0 + k) * L->d[a]);
+                rho[k] = density(&dens, P);
+            }
+            double acc = 0.0;                              /* V4: tau- (k' < k) */
+            for (int64_t k = 0; k < L->K; ++k) {
+                tau_minus[orc_tv_index(L, i, j, k)] = kappa * (double)hl * acc;
+                acc += rho[k];
+            }
+            acc = 0.0;                                     /* V4: tau+ (k' > k) */
+            for (int64_t k = L->K - 1; k >= 0; --k) {
+                tau_plus[orc_tv_index(L, i, j, k)] = kappa * (double)hl * acc;
+                acc += rho[k];
+            }
+        }
+    free(rho);
+    return 0;
+}
+
+double orc_tv_lookup(const orc_tv_lattice* L, const double* tau, const float U[3]) {
+    const double u[3] = {U[0], U[1], U[2]};
+    const double f[3] = {dot3(u, L->e1) - (double)L->a0, dot3(u, L->e2) - (double)L->b0,
+                         dot3(u, L->dhat) / L->ell - (double)L->k0};
+    const int64_t lim[3] = {L->A - 2, L->B - 2, L->K - 2};
+    int64_t c[3];
+    double w[3];
+    for (int a = 0; a < 3; ++a) {
+        double fl = floor(f[a]);
+        if (fl < 0.0) fl = 0.0;
+        if (fl > (double)lim[a]) fl = (double)lim[a];
+        c[a] = (int64_t)fl;
+        w[a] = f[a] - fl;
+    }
+    double v = 0.0;
+    for (int corner = 0; corner < 8; ++corner) {
+        const int di = corner & 1, dj = (corner >> 1) & 1, dk = (corner >> 2) & 1;
+        const double wt = (di ? w[0] : 1.0 - w[0]) * (dj ? w[1] : 1.0 - w[1]) * (dk ? w[2] : 1.0 - w[2]);
+        v += wt * tau[orc_tv_index(L, c[0] + di, c[1] + dj, c[2] + dk)];
+    }
+    return v;
+}
+
+double orc_light_tau(const orc_grid* g, const float* vals, orc_density_fn density_fn, void* density_ctx,
+                     const float U[3], const float Lg[3], float hl, double kappa) {
+    const dens_t dens = {g, vals, density_fn, density_ctx};
+    uint32_t M = 0;
+    return -log(light_march(&dens, U, Lg, hl, kappa, &M));
+}
+
+/* C8's sample count M from U (no sampling): the leading in-support light samples. */
+static uint32_t light_count(const orc_grid* g, const float U[3], const float Lg[3], float hl) {
+    uint32_t j = 1;
+    for (;; ++j) {
+        float s = (float)j * hl;
+        float Y[3] = {fmaf(s, Lg[0], U[0]), fmaf(s, Lg[1], U[1]), fmaf(s, Lg[2], U[2])};
+        if (!inside_support(g, Y) || j > 100000000u) break;
+    }
+    return j - 1;
+}
+
 int orc_guiding_map(const orc_grid* g, const float* vals,
                     orc_density_fn density_fn, void* density_ctx,
                     const orc_camera* cam, const orc_light* lights, int32_t n_lights,
@@ -254,6 +366,26 @@ int orc_guiding_map(const orc_grid* g, const float* vals,
     const double kappa = (double)med->extinction, alpha = (double)med->albedo;
     const double g_hg = (double)med->hg_g;
     const dens_t dens = {g, vals, density_fn, density_ctx};
+    /* NEXT-4 (DESIGN.md §12 V1): every light but the guide set's front light uses its own
+     * transmittance volume; each is built here independently (the mirror lattice of an
+     * opposite light included). */
+    orc_tv_lattice tv_lat[4];
+    double* tv_tau[4] = {NULL, NULL, NULL, NULL};
+    double* tv_scratch = NULL;
+    int tv_on[4] = {0, 0, 0, 0};
+    if (m->light_model == 1) {
+        for (int l = 0; l < n_lights; ++l) {
+            if (light_mode == 1 && l == 0) continue;
+            if (orc_tv_lattice_compute(g, fc.Lg[l], hl, &tv_lat[l])) return 1;
+            const size_t cnt = (size_t)(tv_lat[l].A * tv_lat[l].B * tv_lat[l].K);
+            tv_tau[l] = (double*)malloc(sizeof(double) * cnt);
+            tv_scratch = (double*)realloc(tv_scratch, sizeof(double) * cnt);
+            if (!tv_tau[l] || !tv_scratch) return 1;
+            orc_tv_build(g, vals, density_fn, density_ctx, &tv_lat[l], hl, kappa, tv_tau[l], tv_scratch);
+            tv_on[l] = 1;
+        }
+        free(tv_scratch);
+    }
 
     for (int64_t q = 0; q < n_pix; ++q) {
         int64_t p = pix ? pix[q] : q;
@@ -333,7 +465,13 @@ int orc_guiding_map(const orc_grid* g, const float* vals,
                 /* C8 + C10: L_n = sum_l T^l P_l (rgb applied at the end), L += A_n L_n */
                 for (int l = 0; l < n_lights; ++l) {
                     uint32_t M = 0;
-                    double Tl = light_march(&dens, U, fc.Lg[l], hl, kappa, &M);
+                    double Tl;
+                    if (tv_on[l]) {                      /* NEXT-4 V5 lookup; V6: M still counted */
+                        Tl = exp(-orc_tv_lookup(&tv_lat[l], tv_tau[l], U));
+                        M = light_count(g, U, fc.Lg[l], hl);
+                    } else {
+                        Tl = light_march(&dens, U, fc.Lg[l], hl, kappa, &M);
+                    }
                     lsamp += M;
                     S[l] += A * Tl;
                 }
@@ -365,6 +503,7 @@ int orc_guiding_map(const orc_grid* g, const float* vals,
             out_margin[2 * q + 1] = term_margin;
         }
     }
+    for (int l = 0; l < 4; ++l) free(tv_tau[l]);
     return 0;
 }
 

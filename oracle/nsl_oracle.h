@@ -45,6 +45,7 @@ typedef struct {
     int32_t jitter;                   /* 0 off, 1 per-ray hash */
     uint64_t seed;
     float guide_axis[3];              /* world axis "z" of eq:approx; (0,0,0) -> (0,0,1) */
+    int32_t light_model;              /* 0 canonical march (C8), 1 transmittance volume */
 } orc_march;
 
 /* Frame constants of DESIGN.md C3 (fp64 evaluation, rounded once to fp32). */
@@ -90,6 +91,23 @@ int orc_guiding_map(const orc_grid* g, const float* vals,
                     uint32_t frame_id, int64_t n_pix, const int64_t* pix,
                     double* out_rgbt, float* out_depth, uint32_t* out_debug, double* out_margin,
                     const int32_t* forced_hit, const int32_t* forced_term, int32_t no_clip_n);
+
+/* NEXT-4 transmittance-volume light model (V2-V5). */
+typedef struct {
+    double d[3], dhat[3], ell, e1[3], e2[3];   /* V2 (fp64) */
+    int64_t a0, b0, k0, A, B, K;
+} orc_tv_lattice;
+/* V2 lattice of the light step vector d = hl * Lg (index units). */
+int orc_tv_lattice_compute(const orc_grid* g, const float Lg[3], float hl, orc_tv_lattice* out);
+/* V3/V4: tau_plus / tau_minus, A*B*K doubles each, index (j*K + k)*A + i... see orc_tv_index. */
+int orc_tv_build(const orc_grid* g, const float* vals, orc_density_fn density_fn, void* density_ctx,
+                 const orc_tv_lattice* lat, float hl, double kappa, double* tau_plus, double* tau_minus);
+int64_t orc_tv_index(const orc_tv_lattice* lat, int64_t i, int64_t j, int64_t k);
+/* V5 trilinear lookup of tau (either array) at index-space position U. */
+double orc_tv_lookup(const orc_tv_lattice* lat, const double* tau, const float U[3]);
+/* C8's optical depth kappa*hl*sum rho(U + j hl Lg) from U (the canonical light march). */
+double orc_light_tau(const orc_grid* g, const float* vals, orc_density_fn density_fn, void* density_ctx,
+                     const float U[3], const float Lg[3], float hl, double kappa);
 
 /* NEXT-1 six-way bake (B1-B6). */
 typedef struct {
