@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--config", default="C2")
     p.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
     p.add_argument("--layout", default="oct_f32", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32"])
+    p.add_argument("--light-model", default="march", choices=["march", "tv"],
+                   help="march: canonical C8 (the headline); tv: NEXT-4 transmittance volume (DESIGN.md §12)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--gather", action="store_true",
                    help="N>1: after the timed loop, time the NCCL gather of all guiding maps to rank 0")
@@ -213,6 +215,9 @@ def main():
     layout = nsl.LAYOUTS[args.layout]
     cfg = args.config
     w = rank_workload(cfg, rank, world, args.frames)
+    if args.light_model == "tv":
+        from dataclasses import replace
+        w = replace(w, march=replace(w.march, light_model=1))
     F, H, W = w.n_frames, w.height, w.width
     stream = torch.cuda.current_stream()
 
@@ -312,7 +317,7 @@ def main():
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f16" if layout == 2 else "f32", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[cfg], "frames_per_rank": F, "frames_total": F * world,
-                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": args.layout,
+                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": args.layout, "light_model": args.light_model,
                        "l2": "flushed (512 MiB write) between timed steps, outside the events",
                        "parallelism": f"frame-sharded x{world}, no data-path collective"},
             "samples_per_s": counts["canonical_samples"] * world * K / t_loop,

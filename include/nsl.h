@@ -134,7 +134,12 @@ typedef struct {
  * >= 0 (0 -> step); max_steps >= 0 (0 -> to the support exit); depth_tau >= 0
  * compared with sigma_s; t_min in [0,1) (0 = no early termination);
  * opacity_form NSL_OPACITY_*; jitter 0/1; guide_axis: the world "z" of
- * omega x z ((0,0,0) -> (0,0,1)); front_identity 0/1 allows the C9 shortcut. */
+ * omega x z ((0,0,0) -> (0,0,1)); front_identity 0/1 allows the C9 shortcut;
+ * light_model NSL_LIGHT_MARCH (C8, canonical) or NSL_LIGHT_TV (NEXT-4,
+ * per frame and light a swept optical-depth lattice, one
+ * interpolated lookup per occupied sample; frames are processed in groups
+ * whose lattices fit NSL_TV_BUDGET_MB of transient device memory). */
+enum { NSL_LIGHT_MARCH = 0, NSL_LIGHT_TV = 1 };
 typedef struct {
     float step, light_step;
     int32_t max_steps;
@@ -144,6 +149,7 @@ typedef struct {
     uint64_t seed;
     float guide_axis[3];
     int32_t front_identity;
+    int32_t light_model;
 } nsl_march;
 
 /* ------------------------------------------------------------------ the march (rows a2-a8)

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.environ.get("NSL_LIB") or os.path.join(_HERE, "lib", "libnsl.so")   # NSL_LIB: build variants
 CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu", "bake.cu",
-                                                  "runtime.cu")]
+                                                  "runtime.cu", "tv.cu")]
 HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_HERE, "csrc", "sampler.cuh"),
            os.path.join(_ROOT, "include", "nsl.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -29,6 +29,7 @@ LAYOUT_LINEAR_F32, LAYOUT_QUAD_F32, LAYOUT_CORNER_F16, LAYOUT_OCT_F32 = 0, 1, 2,
 LAYOUT_DEFAULT = LAYOUT_OCT_F32
 LAYOUTS = {"linear_f32": 0, "quad_f32": 1, "corner_f16": 2, "oct_f32": 3}
 LIGHTS_EXPLICIT, LIGHTS_GUIDE = 0, 1
+LIGHT_MARCH, LIGHT_TV = 0, 1
 
 
 class NslError(RuntimeError):
@@ -69,7 +70,7 @@ class MarchS(ctypes.Structure):
     _fields_ = [("step", ctypes.c_float), ("light_step", ctypes.c_float), ("max_steps", ctypes.c_int32),
                 ("depth_tau", ctypes.c_float), ("t_min", ctypes.c_float), ("opacity_form", ctypes.c_int32),
                 ("jitter", ctypes.c_int32), ("seed", ctypes.c_uint64), ("guide_axis", ctypes.c_float * 3),
-                ("front_identity", ctypes.c_int32)]
+                ("front_identity", ctypes.c_int32), ("light_model", ctypes.c_int32)]
 
 
 class FrameConstantsS(ctypes.Structure):
@@ -177,7 +178,8 @@ def medium_s(m) -> MediumS:
 
 def march_s(m) -> MarchS:
     return MarchS(m.step, m.light_step, m.max_steps, m.depth_tau, m.t_min, m.opacity_form, m.jitter,
-                  m.seed & 0xFFFFFFFFFFFFFFFF, _f3(m.guide_axis), getattr(m, "front_identity", 1))
+                  m.seed & 0xFFFFFFFFFFFFFFFF, _f3(m.guide_axis), getattr(m, "front_identity", 1),
+                  getattr(m, "light_model", 0))
 
 
 def _stream_handle(stream) -> int:

@@ -145,6 +145,8 @@ nsl_status check_common(const nsl_light* lights, int n_lights, int light_mode, c
     if (m->opacity_form < 0 || m->opacity_form > 2) return fail(NSL_ERR_INVALID_ARG, "bad opacity_form");
     if (m->jitter != 0 && m->jitter != 1) return fail(NSL_ERR_INVALID_ARG, "jitter must be 0 or 1");
     if (!finite3(m->guide_axis)) return fail(NSL_ERR_INVALID_ARG, "guide_axis must be finite");
+    if (m->light_model != NSL_LIGHT_MARCH && m->light_model != NSL_LIGHT_TV)
+        return fail(NSL_ERR_INVALID_ARG, "bad light_model %d", m->light_model);
     return NSL_OK;
 }
 
@@ -168,6 +170,7 @@ MarchConst make_const(int n_lights, int light_mode, const nsl_medium* med, const
     mc.axis[0] = m->guide_axis[0];
     mc.axis[1] = m->guide_axis[1];
     mc.axis[2] = m->guide_axis[2];
+    mc.light_model = m->light_model;
     return mc;
 }
 
@@ -350,7 +353,64 @@ struct Prepared {
     std::vector<FrameIn> frames;
     MarchConst mc;
     int F = 0, W = 0, H = 0, proj = 0, layout = 0, n_lights = 0;
+    // NEXT-4 transmittance volume (light_model == NSL_LIGHT_TV): lattice slots per frame, host
+    // bounds of the lattice dims (strides), frames per group under the memory budget
+    int tv_slots = 0, tv_Astr = 0, tv_Bstr = 0, tv_Kstr = 0, tv_group = 0;
+    size_t tv_params_bytes() const { return sizeof(TvParams) * (size_t)F * tv_slots; }
+    size_t tv_slot_elems() const { return (size_t)tv_Astr * tv_Bstr * tv_Kstr; }
+    size_t tv_buf_bytes() const { return sizeof(float2) * tv_slot_elems() * tv_slots * (size_t)tv_group; }
 };
+
+// Host bounds of the V2 lattice dims: the projection of the support box on
+// any unit vector is at most its diagonal, so A, B <= diag + 5 and K <= diag / ell + 5 with
+// ell = h_l / voxel_width (unit lights); +6 (and 1e-5 on ell) keeps every device value below.
+static void tv_geometry(const nsl_volume* const* vols, int n_vols, Prepared& P) {
+    P.tv_slots = 0;
+    if (P.mc.light_model != NSL_LIGHT_TV) return;
+    P.tv_slots = P.mc.light_mode == NSL_LIGHTS_GUIDE ? (P.n_lights > 1 ? 1 : 0) : P.n_lights;
+    if (!P.tv_slots) return;
+    double diag = 0.0, kext = 0.0;
+    for (int i = 0; i < n_vols; ++i) {
+        const nsl_grid_desc& g = vols[i]->g;
+        const double d = std::sqrt((g.nx + 1.0) * (g.nx + 1.0) + (g.ny + 1.0) * (g.ny + 1.0) + (g.nz + 1.0) * (g.nz + 1.0));
+        diag = d > diag ? d : diag;
+        const double k = d / ((double)P.mc.hl / (double)g.voxel_width * (1.0 - 1e-5));
+        kext = k > kext ? k : kext;
+    }
+    P.tv_Astr = P.tv_Bstr = (int)std::ceil(diag) + 6;
+    P.tv_Kstr = (int)std::ceil(kext) + 6;
+    double budget_mb = 1024.0;
+    if (const char* e = getenv("NSL_TV_BUDGET_MB")) budget_mb = atof(e);
+    const double per_frame = (double)sizeof(float2) * P.tv_slot_elems() * P.tv_slots;
+    const double g = std::floor(budget_mb * 1048576.0 / per_frame);
+    P.tv_group = g < 1.0 ? 1 : (g > P.F ? P.F : (int)g);
+}
+
+// The march of a prepared batch: one launch, or (light_model TV) the lattice setup, then per
+// frame group the sweep and the march of that group.  tvp/tvbuf: P.tv_params_bytes() and
+// P.tv_buf_bytes() of device workspace (unused otherwise).
+static cudaError_t run_march(const Prepared& P, const FrameParams* params, const uint32_t* order, uint8_t* cull,
+                             TvParams* tvp, float2* tvbuf, float* out_rgbt, float* out_depth, uint32_t* out_debug,
+                             unsigned long long* counters, cudaStream_t s) {
+    float4* rgbt = reinterpret_cast<float4*>(out_rgbt);
+    if (!P.tv_slots)
+        return launch_march(params, P.mc, P.F, P.W, P.H, P.proj, P.layout, rgbt, out_depth, out_debug, counters, order,
+                            cull, nullptr, s);
+    cudaError_t e = launch_tv_setup(params, P.F, P.tv_slots, P.mc, tvp, s);
+    const size_t npf = (size_t)P.W * P.H;
+    const size_t tiles = march_cull_bytes(1, P.W, P.H);
+    for (int g0 = 0; e == cudaSuccess && g0 < P.F; g0 += P.tv_group) {
+        const int n = P.F - g0 < P.tv_group ? P.F - g0 : P.tv_group;
+        const TvParams* gp = tvp + (size_t)g0 * P.tv_slots;
+        e = launch_tv_sweep(params + g0, gp, n, P.tv_slots, P.tv_Astr, P.tv_Bstr, P.tv_Kstr, P.mc, P.layout, tvbuf, s);
+        if (e != cudaSuccess) break;
+        const TvArgs ta{gp, tvbuf, P.tv_slots, P.tv_Astr, P.tv_Kstr, (int64_t)P.tv_slot_elems()};
+        e = launch_march(params + g0, P.mc, n, P.W, P.H, P.proj, P.layout, rgbt + (size_t)g0 * npf,
+                         out_depth + (size_t)g0 * npf, out_debug ? out_debug + (size_t)g0 * npf * 6 : nullptr, counters,
+                         order, cull ? cull + (size_t)g0 * tiles : nullptr, &ta, s);
+    }
+    return e;
+}
 
 static nsl_status prepare(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
                           const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
@@ -388,6 +448,7 @@ static nsl_status prepare(const nsl_volume* const* vols, int32_t n_vols, const i
         fi.frame_id = frame_ids[f];
     }
     P.mc = make_const(n_lights, light_mode, med, m);
+    tv_geometry(vols, n_vols, P);
     return NSL_OK;
 }
 
@@ -410,8 +471,14 @@ static nsl_status batch_impl(const nsl_volume* const* vols, int32_t n_vols, cons
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
     if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, tile_order(P.W, P.H), s, ws)) return st;
-    cudaError_t e = launch_march(ws.params, P.mc, P.F, P.W, P.H, P.proj, P.layout, reinterpret_cast<float4*>(out_rgbt),
-                                 out_depth, out_debug, counters, ws.order, ws.cull, s);
+    void* tvws = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (P.tv_slots) e = cudaMallocAsync(&tvws, align_up(P.tv_params_bytes(), 256) + P.tv_buf_bytes(), s);
+    if (e == cudaSuccess)
+        e = run_march(P, ws.params, ws.order, ws.cull, static_cast<TvParams*>(tvws),
+                      reinterpret_cast<float2*>(static_cast<char*>(tvws) + align_up(P.tv_params_bytes(), 256)),
+                      out_rgbt, out_depth, out_debug, counters, s);
+    if (tvws) cudaFreeAsync(tvws, s);
     cudaError_t e2 = cudaFreeAsync(ws.base, s);
     if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
     if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(frame tables)");
@@ -542,6 +609,8 @@ struct nsl_plan {
     FrameParams* params = nullptr;
     uint32_t* order = nullptr;
     uint8_t* cull = nullptr;
+    TvParams* tvp = nullptr;     // NEXT-4 workspace (light_model TV)
+    float2* tvbuf = nullptr;
 };
 
 nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
@@ -560,8 +629,9 @@ nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const 
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
     const size_t b_o = align_up(sizeof(uint32_t) * order.size(), 256);
     const size_t b_p = align_up(sizeof(FrameParams) * F, 256);
-    const size_t b_c = march_cull_bytes(F, p->P.W, p->P.H);
-    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_o + b_p + b_c);
+    const size_t b_c = align_up(march_cull_bytes(F, p->P.W, p->P.H), 256);
+    const size_t b_tp = align_up(p->P.tv_params_bytes(), 256);
+    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_o + b_p + b_c + b_tp + p->P.tv_buf_bytes());
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaMalloc(plan)");
@@ -571,6 +641,8 @@ nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const 
     p->order = reinterpret_cast<uint32_t*>(static_cast<char*>(p->dev) + b_in + b_l);
     p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_o);
     p->cull = reinterpret_cast<uint8_t*>(p->dev) + b_in + b_l + b_o + b_p;
+    p->tvp = reinterpret_cast<TvParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_o + b_p + b_c);
+    p->tvbuf = reinterpret_cast<float2*>(static_cast<char*>(p->dev) + b_in + b_l + b_o + b_p + b_c + b_tp);
     std::vector<char> host(b_in + b_l + b_o);
     memcpy(host.data(), p->P.frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
@@ -596,9 +668,8 @@ nsl_status nsl_plan_execute(const nsl_plan* p, float* out_rgbt, float* out_depth
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (counters) NSL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint64_t), s), "cudaMemsetAsync(counters)");
     NSL_CUDA(launch_frame_setup(p->in, p->lights, p->P.F, p->P.mc, p->params, s), "frame_setup_kernel launch");
-    NSL_CUDA(launch_march(p->params, p->P.mc, p->P.F, p->P.W, p->P.H, p->P.proj, p->P.layout,
-                          reinterpret_cast<float4*>(out_rgbt), out_depth, out_debug,
-                          reinterpret_cast<unsigned long long*>(counters), p->order, p->cull, s),
+    NSL_CUDA(run_march(p->P, p->params, p->order, p->cull, p->tvp, p->tvbuf, out_rgbt, out_depth, out_debug,
+                       reinterpret_cast<unsigned long long*>(counters), s),
              "march_kernel launch");
     return NSL_OK;
 }

@@ -57,13 +57,37 @@ __global__ void tile_cull_kernel(const FrameParams* __restrict__ fps, int F, int
     cull[idx] = bits;
 }
 
-template <int LAYOUT, int PROJ, int MODE>
+// NEXT-4 V5: trilinear lookup of (tau+, tau-) at index-space position (x, y, z) in the
+// lattice of slot t (fractions from the clamped cell, as in the oracle).
+__device__ __forceinline__ float2 tv_lookup(const TvParams& t, const float2* __restrict__ base, int Astr, int Kstr,
+                                            float x, float y, float z) {
+    const float al = fmaf(z, t.e1[2], fmaf(y, t.e1[1], x * t.e1[0])) - t.a0;
+    const float be = fmaf(z, t.e2[2], fmaf(y, t.e2[1], x * t.e2[0])) - t.b0;
+    const float ga = fmaf(z, t.dk[2], fmaf(y, t.dk[1], x * t.dk[0])) - t.k0;
+    const float fi = fminf(fmaxf(floorf(al), 0.0f), (float)(t.A - 2));
+    const float fj = fminf(fmaxf(floorf(be), 0.0f), (float)(t.B - 2));
+    const float fk = fminf(fmaxf(floorf(ga), 0.0f), (float)(t.K - 2));
+    const float wi = al - fi, wj = be - fj, wk = ga - fk;
+    const float2* p = base + ((int64_t)fj * Kstr + (int64_t)fk) * Astr + (int64_t)fi;
+    const int64_t sj = (int64_t)Kstr * Astr;
+    const float2 c000 = __ldg(p), c100 = __ldg(p + 1), c010 = __ldg(p + Astr), c110 = __ldg(p + Astr + 1);
+    const float2 c001 = __ldg(p + sj), c101 = __ldg(p + sj + 1), c011 = __ldg(p + sj + Astr),
+                 c111 = __ldg(p + sj + Astr + 1);
+    float2 r;
+    r.x = lerpf(lerpf(lerpf(c000.x, c100.x, wi), lerpf(c010.x, c110.x, wi), wk),
+                lerpf(lerpf(c001.x, c101.x, wi), lerpf(c011.x, c111.x, wi), wk), wj);
+    r.y = lerpf(lerpf(lerpf(c000.y, c100.y, wi), lerpf(c010.y, c110.y, wi), wk),
+                lerpf(lerpf(c001.y, c101.y, wi), lerpf(c011.y, c111.y, wi), wk), wj);
+    return r;
+}
+
+template <int LAYOUT, int PROJ, int MODE, bool TV>
 __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H,
                                                          const uint32_t* __restrict__ tile_order,
-                                                         const uint8_t* __restrict__ cull, int tiles_x) {
+                                                         const uint8_t* __restrict__ cull, int tiles_x, TvArgs tv) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
     // grid (frame, tile rank): frames fastest in launch order; tiles centre-out
     // (tile_order) so the heavy tiles of every frame start first and the tail of
@@ -218,7 +242,12 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
                 else if (mc.form == NSL_OPACITY_RIEMANN) A = mc.alpha * Tp * s;
                 else A = Tp * sig_s;
                 const float kl = mc.hl * mc.kappa;
-                if (paired) {                              // C8: top/bottom in one loop
+                const bool guide = mc.light_mode == NSL_LIGHTS_GUIDE;
+                float2 tv0 = make_float2(0.0f, 0.0f);      // NEXT-4: the guide pair's (tau+, tau-)
+                if (TV && guide && mc.n_lights > 1)
+                    tv0 = tv_lookup(tv.params[f * tv.slots], tv.buf + (int64_t)f * tv.slots * tv.slot_elems,
+                                    tv.Astr, tv.Kstr, x, y, z);
+                if (!TV && paired) {                       // C8: top/bottom in one loop
                     int Ma, Mb, ma, mb;
                     if (DEBUG || COUNT) {
                         Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
@@ -246,12 +275,20 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
                 }
 #pragma unroll
                 for (int l = 0; l < 4; ++l) {             // C8 + C10
-                    if (l < mc.n_lights && !(paired && (l == 1 || l == 2))) {
+                    if (l < mc.n_lights && !(!TV && paired && (l == 1 || l == 2))) {
                         float Tl;
                         const float lx = sp.Lg[l][0], ly = sp.Lg[l][1], lz = sp.Lg[l][2];
                         if (l == 0 && front_fast) {
                             Tl = Tp;                      // C9: T^front_n = T_{n-1}
                             if (COUNT) lsamp += (uint32_t)light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
+                        } else if (TV && !(guide && l == 0)) {   // NEXT-4 V5 (V6: M still counted)
+                            const float tau = guide ? (l == 1 ? tv0.x : tv0.y)
+                                                    : tv_lookup(tv.params[f * tv.slots + l],
+                                                                tv.buf + ((int64_t)f * tv.slots + l) * tv.slot_elems,
+                                                                tv.Astr, tv.Kstr, x, y, z).x;
+                            Tl = __expf(-tau);
+                            if (DEBUG || COUNT)
+                                lsamp += (uint32_t)light_count(v, x, y, z, lx, ly, lz, mc.hl, sp.lim[l], sp.ilh[l]);
                         } else {
                             int M, mm;
                             if (DEBUG || COUNT) {
@@ -334,7 +371,7 @@ __global__ void jitter_debug_kernel(MarchConst mc, uint32_t frame, int n, uint32
 template <int LAYOUT, int PROJ, int MODE>
 cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
                        uint32_t* debug, unsigned long long* counters, const uint32_t* tile_order, uint8_t* cull,
-                       cudaStream_t s) {
+                       const TvArgs* tv, cudaStream_t s) {
     const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH, tiles = tiles_x * tiles_y;
     if (tiles > 65535) return cudaErrorInvalidConfiguration;
     if (PROJ == 0) {
@@ -343,24 +380,30 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
                                    tiles, cull);
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(march_kernel<LAYOUT, PROJ, MODE>, dim3((unsigned)F, (unsigned)tiles), dim3(kThreads), 0, s, fp,
-                      mc, rgbt, depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x);
+    const dim3 grid((unsigned)F, (unsigned)tiles);
+    if (tv)
+        return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth,
+                          debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, *tv);
+    return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth, debug,
+                      counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
 }
 
 template <int LAYOUT, int PROJ>
 cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
-                      uint32_t* debug, unsigned long long* counters, const uint32_t* to, uint8_t* cull, cudaStream_t s) {
-    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
-    if (counters) return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
-    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
+                      uint32_t* debug, unsigned long long* counters, const uint32_t* to, uint8_t* cull,
+                      const TvArgs* tv, cudaStream_t s) {
+    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
+    if (counters)
+        return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
+    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
 }
 
 template <int LAYOUT>
 cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, float4* rgbt,
                      float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* to, uint8_t* cull,
-                     cudaStream_t s) {
-    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s)
-                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, s);
+                     const TvArgs* tv, cudaStream_t s) {
+    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s)
+                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
 }
 
 }  // namespace
@@ -374,12 +417,12 @@ size_t march_cull_bytes(int F, int W, int H) {
 
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection, int layout,
                          float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
-                         const uint32_t* tile_order, uint8_t* cull, cudaStream_t s) {
+                         const uint32_t* tile_order, uint8_t* cull, const TvArgs* tv, cudaStream_t s) {
     switch (layout) {
-        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
-        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
-        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
-        case kOctF32: return launch_l<kOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, s);
+        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
+        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
+        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
+        case kOctF32: return launch_l<kOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
     }
     return cudaErrorInvalidValue;
 }

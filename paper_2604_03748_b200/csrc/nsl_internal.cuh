@@ -85,7 +85,31 @@ struct MarchConst {
     uint32_t seed_lo, seed_hi;
     int32_t front_identity;
     float axis[3];
+    int32_t light_model;       // NSL_LIGHT_MARCH | NSL_LIGHT_TV
 };
+
+// NEXT-4 transmittance volume: per (frame, lattice slot) constants of the
+// light step vector's lattice (V2, fp64 -> fp32) and the sweep window (the occupied box's
+// lattice range +-2: lookups at occupied samples never leave it).  Lattice values are float2
+// (tau+, tau-) at index (j * Kstr + k) * Astr + i of the slot's block of a group buffer.
+struct TvParams {
+    float e1[3], e2[3], d[3], dk[3];   // dk = dhat / ell
+    float a0, b0, k0, kh;              // lattice offsets (exact small integers), kappa * h_l
+    int32_t A, B, K;                   // lattice dims (V2)
+    int32_t i_lo, i_hi, j_lo, j_hi, k_lo, k_hi;
+    int32_t pad[3];
+};
+static_assert(sizeof(TvParams) % 16 == 0, "TvParams must be 16-B multiple");
+struct TvArgs {                        // march kernel argument (light_model == NSL_LIGHT_TV)
+    const TvParams* params;            // [F][slots] (group base)
+    const float2* buf;                 // group lattice buffer
+    int32_t slots, Astr, Kstr;
+    int64_t slot_elems;                // Astr * Bstr * Kstr
+};
+cudaError_t launch_tv_setup(const FrameParams* fps, int F, int slots, const MarchConst& mc, TvParams* out,
+                            cudaStream_t s);
+cudaError_t launch_tv_sweep(const FrameParams* fps, const TvParams* tvp, int F, int slots, int Astr, int Bstr,
+                            int Kstr, const MarchConst& mc, int layout, float2* buf, cudaStream_t s);
 
 // NEXT-1 six-way bake: per-frame light constants and call constants.
 struct BakeFrame {
@@ -169,9 +193,10 @@ cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F
                                FrameParams* out, cudaStream_t s);
 // mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path.
 // cull: march_cull_bytes(F, W, H) bytes of device workspace (orthographic views: per-tile cull flags).
+// tv: NULL (light_model 0) or the group's transmittance-volume arguments.
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection,
                          int layout, float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
-                         const uint32_t* tile_order, uint8_t* cull, cudaStream_t s);
+                         const uint32_t* tile_order, uint8_t* cull, const TvArgs* tv, cudaStream_t s);
 size_t march_cull_bytes(int F, int W, int H);
 int march_tile_w();
 int march_tile_h();

@@ -1,0 +1,92 @@
+"""GPU parity of the NEXT-4 transmittance-volume light model against the oracle
+run with the same light model: values within max(1e-4 |o|, 1e-5), depth and every debug
+counter bit-exact (V6: the bookkeeping is light-model independent)."""
+import os
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import nsl_inputs as I
+from parity import compare_frame
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nsl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    import paper_2604_03748_b200 as nsl
+    nsl.lib()
+    return nsl
+
+
+def tv(w):
+    return replace(w, march=replace(w.march, light_model=1))
+
+
+def run(nsl, w, layout=3, debug=True):
+    import torch
+    rgbt, depth, dbg = nsl.run_workload(w, layout=layout, debug=debug)
+    torch.cuda.synchronize()
+    return rgbt.cpu().numpy(), depth.cpu().numpy(), None if dbg is None else dbg.cpu().numpy()
+
+
+@pytest.mark.parametrize("debug", [True, False])
+@pytest.mark.parametrize("kw", [{}, {"perspective": True}, {"single_light": True}])
+def test_tv_parity_C1(nsl, debug, kw):
+    w = tv(I.make_workload("C1", **kw))
+    g, gd, gdbg = run(nsl, w, debug=debug)
+    compare_frame(w, 0, g[0], gd[0], gdbg[0] if gdbg is not None else None)
+
+
+def test_tv_differs_from_march_only_in_light_transmittance(nsl):
+    w = I.make_workload("C1")
+    a = run(nsl, w)
+    b = run(nsl, tv(w))
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])        # D and every counter
+    assert np.array_equal(a[0][..., 3], b[0][..., 3])                         # T
+    d = np.abs(a[0][..., :3] - b[0][..., :3])
+    assert 0 < d.max() < 0.1 * np.abs(a[0][..., :3]).max()
+
+
+@pytest.mark.parametrize("layout", [1, 3])
+def test_tv_parity_C2_subsampled(nsl, layout):
+    w = tv(I.make_workload("C2", frames=[0, 21, 40]))
+    g, gd, gdbg = run(nsl, w, layout=layout)
+    pix = np.arange(0, 512 * 512, 37)
+    for f in range(3):
+        compare_frame(w, f, g[f], gd[f], gdbg[f], pixels=pix)
+
+
+def test_tv_frame_groups_are_bitwise_invariant(nsl, monkeypatch):
+    """A tiny memory budget forces one frame per group: results equal the single-group run."""
+    w = tv(I.make_workload("C2", frames=[3, 9, 15, 27, 33]))
+    full = run(nsl, w, debug=False)
+    monkeypatch.setenv("NSL_TV_BUDGET_MB", "1")
+    grouped = run(nsl, w, debug=False)
+    for x, y in zip(full, grouped):
+        assert (x is None and y is None) or np.array_equal(x, y)
+
+
+def test_tv_plan_equals_batch(nsl):
+    import torch
+    w = tv(I.make_workload("C2", frames=[7, 8]))
+    ref = run(nsl, w, debug=False)
+    vols = nsl.upload_workload_volumes(w, 3)
+    plan = nsl.make_plan(w, vols)
+    rgbt, depth, _ = nsl.alloc_outputs(w.n_frames, w.height, w.width)
+    plan.execute(rgbt, depth)
+    torch.cuda.synchronize()
+    assert np.array_equal(rgbt.cpu().numpy(), ref[0]) and np.array_equal(depth.cpu().numpy(), ref[1])
+
+
+def test_tv_explicit_lights_C3_subsampled(nsl):
+    """C3 (carved 256^3, one explicit moving light): the lattice is the light's own."""
+    w = tv(I.make_workload("C3", frames=[0, 30]))
+    g, gd, gdbg = run(nsl, w)
+    pix = np.arange(0, 1024 * 1024, 997)
+    for f in range(2):
+        compare_frame(w, f, g[f], gd[f], gdbg[f], pixels=pix)
