@@ -106,6 +106,7 @@ __global__ void tv_setup_kernel(const FrameParams* __restrict__ fps, int F, int 
     out[idx] = t;
 }
 
+constexpr int kSweepSmemK = 64;   // windows of at most 64 points per line stage in shared memory
 template <int LAYOUT>
 __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __restrict__ fps,
                                                        const TvParams* __restrict__ tvp, int slots, int Astr,
@@ -133,23 +134,45 @@ __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __rest
     for (int a = 0; a < 3; ++a) base[a] = __fmaf_rn(bf, t.e2[a], __fmul_rn(af, t.e1[a]));
     float2* col = buf + (int64_t)fs * slot_elems + (int64_t)j * Kstr * Astr + i;
     uint32_t unused = 0;
-    float acc = 0.0f;                   // V4 tau-: exclusive prefix toward -d
-    for (int k = t.k_lo; k <= t.k_hi; ++k) {
+    auto sample_k = [&](int k) {
         const float kf = t.k0 + (float)k;
         const float x = __fmaf_rn(kf, t.d[0], base[0]), y = __fmaf_rn(kf, t.d[1], base[1]),
                     z = __fmaf_rn(kf, t.d[2], base[2]);
-        const float rho = inside(v, x, y, z) ? sample<LAYOUT, false>(v, x, y, z, unused) : 0.0f;
-        const float sk = t.kh * rho;
-        col[(int64_t)k * Astr] = make_float2(sk, acc);
-        acc += sk;
+        return t.kh * (inside(v, x, y, z) ? sample<LAYOUT, false>(v, x, y, z, unused) : 0.0f);
+    };
+    if (t.k_hi - t.k_lo < kSweepSmemK) {
+        // the line's kappa h rho_k staged in shared memory (a column per thread, conflict-free),
+        // then one backward walk writes each lattice point once: tau+ is the exclusive suffix,
+        // tau- = total - (tau+ + s_k) (absolute rounding ~ a few ulp of the line total)
+        extern __shared__ float sk_s[];
+        float* sk = sk_s + threadIdx.x;
+        float tot = 0.0f;
+        for (int k = t.k_lo; k <= t.k_hi; ++k) {
+            const float sv = sample_k(k);
+            sk[(k - t.k_lo) * blockDim.x] = sv;
+            tot += sv;
+        }
+        float suf = 0.0f;
+        for (int k = t.k_hi; k >= t.k_lo; --k) {
+            const float sv = sk[(k - t.k_lo) * blockDim.x];
+            col[(int64_t)k * Astr] = make_float2(suf, fmaxf(tot - (suf + sv), 0.0f));
+            suf += sv;
+        }
+        return;
+    }
+    float acc = 0.0f;                   // V4 tau-: exclusive prefix toward -d
+    for (int k = t.k_lo; k <= t.k_hi; ++k) {
+        const float sv = sample_k(k);
+        col[(int64_t)k * Astr] = make_float2(sv, acc);
+        acc += sv;
     }
     acc = 0.0f;                         // V4 tau+: exclusive suffix toward +d
     for (int k = t.k_hi; k >= t.k_lo; --k) {
         float2 e = col[(int64_t)k * Astr];
-        const float sk = e.x;
+        const float sv = e.x;
         e.x = acc;
         col[(int64_t)k * Astr] = e;
-        acc += sk;
+        acc += sv;
     }
 }
 
@@ -167,11 +190,12 @@ cudaError_t launch_tv_sweep(const FrameParams* fps, const TvParams* tvp, int F, 
     (void)mc;
     const dim3 grid((unsigned)(((int64_t)Astr * Bstr + 127) / 128), (unsigned)(F * slots));
     const int64_t slot_elems = (int64_t)Astr * Bstr * Kstr;
+    const size_t smem = (size_t)kSweepSmemK * 128 * sizeof(float);
     switch (layout) {
-        case kLinearF32: tv_sweep_kernel<kLinearF32><<<grid, 128, 0, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
-        case kQuadF32: tv_sweep_kernel<kQuadF32><<<grid, 128, 0, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
-        case kCornerF16: tv_sweep_kernel<kCornerF16><<<grid, 128, 0, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
-        case kOctF32: tv_sweep_kernel<kOctF32><<<grid, 128, 0, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
+        case kLinearF32: tv_sweep_kernel<kLinearF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
+        case kQuadF32: tv_sweep_kernel<kQuadF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
+        case kCornerF16: tv_sweep_kernel<kCornerF16><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
+        case kOctF32: tv_sweep_kernel<kOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
