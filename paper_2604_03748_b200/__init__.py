@@ -37,12 +37,31 @@ class NslError(RuntimeError):
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libnsl.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    """Compile libnsl.so for sm_100a in-tree (nvcc cross-compiles without a GPU): one nvcc
+    per translation unit in parallel (objects under lib/obj/), then one shared-library link."""
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
     newest = max(os.path.getmtime(p) for p in CSRC + HEADERS)
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
-        cmd = ["nvcc", *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", LIB_PATH, *CSRC]
-        subprocess.check_call(cmd)
+        objdir = os.path.join(os.path.dirname(LIB_PATH), "obj")
+        os.makedirs(objdir, exist_ok=True)
+        cflags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+        objs = [os.path.join(objdir, os.path.basename(c)[:-3] + ".o") for c in CSRC]
+
+        def compile_one(src_obj):
+            src, obj = src_obj
+            cmd = ["nvcc", *cflags, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", obj, src]
+            return subprocess.run(cmd, capture_output=True, text=True)
+
+        with ThreadPoolExecutor(max_workers=len(CSRC)) as ex:
+            results = list(ex.map(compile_one, zip(CSRC, objs)))
+        for r in results:
+            if verbose or r.returncode:
+                print(r.stdout + r.stderr, end="")
+            if r.returncode:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                               "-o", LIB_PATH, *objs])
     return LIB_PATH
 
 
