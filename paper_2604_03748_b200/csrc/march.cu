@@ -253,15 +253,13 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
                         Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
                         Mb = light_count(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2]);
                         float ra[3], rb[3];
-                        march_region(sp, v, 1, z, ra);
-                        march_region(sp, v, 2, z, rb);
+                        pair_regions(sp, v, z, ra, rb);
                         ma = min(Ma, box_count(x, y, z, ra, sp.ilh[1]));
                         mb = min(Mb, box_count(x, y, z, rb, sp.ilh[2]));
                     } else {
                         Ma = Mb = 0;
                         float ra[3], rb[3];
-                        march_region(sp, v, 1, z, ra);
-                        march_region(sp, v, 2, z, rb);
+                        pair_regions(sp, v, z, ra, rb);
                         ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.ilh[1], ra);
                         mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.ilh[2], rb);
                     }
