@@ -550,7 +550,9 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     cudaStream_t side = nullptr;
     std::vector<cudaEvent_t> evs;
     const size_t npf = (size_t)cams[0].width * cams[0].height;
-    const int nchunks = F < 8 ? F : 8, per = (F + nchunks - 1) / nchunks;
+    int want = 8;                                 // chunks (NSL_HOST_CHUNKS overrides)
+    if (const char* ev = getenv("NSL_HOST_CHUNKS")) want = atoi(ev) > 0 ? atoi(ev) : 8;
+    const int nchunks = F < want ? F : want, per = (F + nchunks - 1) / nchunks;
     if (st == NSL_OK) {
         e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
         if (e != cudaSuccess) st = cuda_fail(e, "cudaStreamCreate(side)");
