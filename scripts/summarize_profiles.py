@@ -41,14 +41,16 @@ for r in rows[hi + 1:]:
 tot = sum(sum(v) for v in agg.values())
 out = [f"# ncu launch list of `python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline` (B200, {tag})",
        "# gpu__time_duration.sum with --clock-control none: cold-cache, serialised; compare SHARES, not absolutes.",
-       "# march_kernel<.., 2> is the one instrumented (counted) launch; at::FillFunctor<uchar> is the L2 flush.", ""]
+       "# march_kernel<layout, proj, 2, tv> is the one instrumented (counted) launch; at::FillFunctor<uchar> is the L2 flush.", ""]
 step = 0.0
 for k, v in agg.items():
     out.append(f"{len(v):3d} launches  mean {sum(v) / len(v):9.2f} us  share-of-all {100 * sum(v) / tot:5.1f}%  {k}")
-    if k.startswith("nsl") and not k.endswith(", 2>"):
+    counted = "march_kernel" in k and k.split("<")[-1].split(",")[2].strip() == "2"
+    if k.startswith("nsl") and not counted:
         step += sum(v) / len(v)
-mk = [sum(v) / len(v) for k, v in agg.items() if "march_kernel" in k and k.endswith(", 0>")]
-out += ["", f"one bench step (layout + occupancy + frame_setup + march means): {step:.1f} us; "
+mk = [sum(v) / len(v) for k, v in agg.items()
+      if "march_kernel" in k and k.split("<")[-1].split(",")[2].strip() == "0"]
+out += ["", f"one bench step (volume build + finalize + frame_setup + cull + march means): {step:.1f} us; "
             f"march_kernel share of the step: {100 * mk[0] / step:.1f}%" if mk else ""]
 open(os.path.join(P, f"{round_tag}_launches_summary.txt"), "w").write("\n".join(out) + "\n")
 print("\n".join(out))
