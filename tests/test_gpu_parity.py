@@ -132,6 +132,26 @@ def test_parity_C2(nsl, debug):
         compare_frame(w, f, g[f], gd[f], None if gdbg is None else gdbg[f])
 
 
+def test_parity_C2_bench_launch_configuration(nsl):
+    """Exactly what bench.py times: all 60 C2 frames, OCT layout, device-resident raw grid,
+    caller-owned storage, volume re-upload + plan execute (FAST); every frame sampled 1/97."""
+    import torch
+    w = I.make_workload("C2")
+    raw = torch.from_numpy(w.volume(0)).cuda()
+    storage = torch.empty(nsl.volume_bytes(w.grid, 3), dtype=torch.uint8, device="cuda")
+    vols = [nsl.Volume(w.grid, raw, 3, storage=storage)]
+    plan = nsl.make_plan(w, vols)
+    outs = nsl.alloc_outputs(w.n_frames, w.height, w.width)
+    for _ in range(2):                                   # second step re-builds the volume in place
+        vols = [nsl.Volume(w.grid, raw, 3, storage=storage)]
+        plan.execute(outs[0], outs[1])
+    torch.cuda.synchronize()
+    g, gd = outs[0].cpu().numpy(), outs[1].cpu().numpy()
+    pix = np.arange(0, w.height * w.width, 97)
+    for f in range(w.n_frames):
+        compare_frame(w, f, g[f], gd[f], None, pixels=(pix + 13 * f) % (w.height * w.width))
+
+
 def test_parity_C2_density_sweep(nsl):
     for kappa in (16.0, 64.0):
         w = I.make_workload("C2", frames=[12], kappa=kappa)
