@@ -131,12 +131,15 @@ __global__ void __launch_bounds__(32 * kSetupWarps) relight_setup_kernel(const R
 }
 
 constexpr int kRelightThreads = 256;
-constexpr int kRelightPPT = 4;              // pixels per thread (loads issued together)
 
-// One CTA = kRelightThreads*kRelightPPT consecutive pixels of one frame; the frame's
-// constants are staged to shared memory once.  Maps/depth are streamed (evict-first),
-// the output is written with streaming stores; only the shadow maps stay in cache.
-__global__ void __launch_bounds__(kRelightThreads) relight_kernel(const RelightFrame* __restrict__ frames,
+// One CTA = kRelightThreads*PPT consecutive pixels of one frame; the frame's constants are
+// staged to shared memory once.  Maps/depth are streamed (evict-first), the output is written
+// with streaming stores; only the shadow maps stay in cache.  Two configurations (measured,
+// DESIGN.md §11): without shadow maps 4 pixels per thread (all loads issued together: 0.94 of
+// the HBM copy peak); with shadow maps the depth -> shadow-texel chain is two dependent
+// round trips, so 1 pixel per thread at full occupancy hides it better (+9 %).
+template <int PPT, int MINB>
+__global__ void __launch_bounds__(kRelightThreads, MINB) relight_kernel(const RelightFrame* __restrict__ frames,
                                                                   RelightConst rc, int blocks_per_frame,
                                                                   const float4* __restrict__ maps,
                                                                   const float* __restrict__ depth,
@@ -152,11 +155,11 @@ __global__ void __launch_bounds__(kRelightThreads) relight_kernel(const RelightF
     __syncthreads();
     const int npf = rc.W * rc.H;
     const size_t fbase = (size_t)f * npf;
-    const int p0 = chunk * (kRelightThreads * kRelightPPT) + threadIdx.x;
-    float4 m0[kRelightPPT], m1[kRelightPPT];
-    float D[kRelightPPT];
+    const int p0 = chunk * (kRelightThreads * PPT) + threadIdx.x;
+    float4 m0[PPT], m1[PPT];
+    float D[PPT];
 #pragma unroll
-    for (int k = 0; k < kRelightPPT; ++k) {
+    for (int k = 0; k < PPT; ++k) {
         const int pix = p0 + k * kRelightThreads;
         if (pix < npf) {
             const size_t q = fbase + pix;
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(kRelightThreads) relight_kernel(const RelightF
     }
     const int ns = fs.ns;
 #pragma unroll
-    for (int k = 0; k < kRelightPPT; ++k) {
+    for (int k = 0; k < PPT; ++k) {
         const int pix = p0 + k * kRelightThreads;
         if (pix >= npf) break;
         const float ch[8] = {m0[k].x, m0[k].y, m0[k].z, m0[k].w, m1[k].x, m1[k].y, m1[k].z, m1[k].w};
@@ -228,10 +231,13 @@ cudaError_t launch_relight(const RelightIn* in, int F, int n_lights, RelightFram
     relight_setup_kernel<<<(F + kSetupWarps - 1) / kSetupWarps, 32 * kSetupWarps, 0, s>>>(in, F, n_lights, rc, frames);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const long long per = kRelightThreads * kRelightPPT;
+    const long long per = kRelightThreads * (rc.any_shadow ? 1 : 4);
     const long long bpf = ((long long)rc.W * rc.H + per - 1) / per;
     if (bpf * F >= (1LL << 31)) return cudaErrorInvalidConfiguration;
-    relight_kernel<<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
+    if (rc.any_shadow)
+        relight_kernel<1, 8><<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
+    else
+        relight_kernel<4, 1><<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
     return cudaGetLastError();
 }
 
