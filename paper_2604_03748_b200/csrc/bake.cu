@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kBakeThreads) bake_kernel(const FrameParams* _
     v.sx1 = sp.supp[0];
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
+    v.mask_words = sp.slab_off;
 
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t gath = 0;

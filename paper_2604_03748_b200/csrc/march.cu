@@ -68,6 +68,9 @@ __device__ __forceinline__ float2 tv_lookup(const TvParams& t, const float2* __r
     const float fj = fminf(fmaxf(floorf(be), 0.0f), (float)(t.B - 2));
     const float fk = fminf(fmaxf(floorf(ga), 0.0f), (float)(t.K - 2));
     const float wi = al - fi, wj = be - fj, wk = ga - fk;
+    // V5 lookups at occupied samples stay inside the swept window
+    NSL_ASSERT(fi >= (float)t.i_lo && fi + 1.0f <= (float)t.i_hi && fj >= (float)t.j_lo &&
+               fj + 1.0f <= (float)t.j_hi && fk >= (float)t.k_lo && fk + 1.0f <= (float)t.k_hi);
     const float2* p = base + ((int64_t)fj * Kstr + (int64_t)fk) * Astr + (int64_t)fi;
     const int64_t sj = (int64_t)Kstr * Astr;
     const float2 c000 = __ldg(p), c100 = __ldg(p + 1), c010 = __ldg(p + Astr), c110 = __ldg(p + Astr + 1);
@@ -126,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
     v.sx1 = sp.supp[0];
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
+    v.mask_words = sp.slab_off;
     if (!COUNT && !valid) return;
 
     uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0, c_tp = 0, c_tl = 0;

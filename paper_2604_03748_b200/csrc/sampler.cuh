@@ -5,6 +5,18 @@
 #pragma once
 #include <cuda_fp16.h>
 
+// NSL_CHECK=1 builds a checked library (scripts/gpu_checked.sh): device asserts on every
+// volume/mask/lattice index the kernels compute (there is no compute-sanitizer on the pool).
+#ifndef NSL_CHECK
+#define NSL_CHECK 0
+#endif
+#if NSL_CHECK
+#include <cassert>
+#define NSL_ASSERT(c) assert(c)
+#else
+#define NSL_ASSERT(c) ((void)0)
+#endif
+
 #include "nsl_internal.cuh"
 
 namespace nsl {
@@ -35,6 +47,7 @@ struct Vol {
     int sy, sz;
     int shift, nbx, nby;
     float sx1, sy1, sz1;          // support upper bounds n+1
+    int mask_words;               // NSL_CHECK only: occupancy mask words
 };
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return __fmaf_rn(t, b - a, a); }
@@ -58,6 +71,8 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
     const int ix = __float_as_int(rx) - 0x4B400000, iy = __float_as_int(ry) - 0x4B400000,
               iz = __float_as_int(rz) - 0x4B400000;
     const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
+    NSL_ASSERT(ix >= 0 && iy >= 0 && iz >= 0 && (float)ix < v.sx1 && (float)iy < v.sy1 && (float)iz < v.sz1);
+    NSL_ASSERT(b >= 0 && (b >> 5) < v.mask_words);
     const uint32_t word = __ldg(v.occ + (b >> 5));
     if (!((word >> (b & 31)) & 1u)) return 0.0f;
     if (COUNT) ++gathers;
