@@ -138,8 +138,12 @@ __device__ __forceinline__ void bake_region(const FrameParams& sp, const BakeFra
     }
 }
 
+#ifndef NSL_BAKE_MINB
+#define NSL_BAKE_MINB 12  // min resident CTAs per SM (register cap 40: 48 warps/SM); measured 1 -> 14.3, 8 -> 11.1,
+                          // 12 -> 10.1, 14/16 -> 12.6 ms per C2 frame (spills)
+#endif
 template <int LAYOUT, int PROJ>
-__global__ void __launch_bounds__(kBakeThreads) bake_kernel(const FrameParams* __restrict__ fps,
+__global__ void __launch_bounds__(kBakeThreads, NSL_BAKE_MINB) bake_kernel(const FrameParams* __restrict__ fps,
                                                           const BakeFrame* __restrict__ bfs, const BakeConst bc,
                                                           float4* __restrict__ out, int W, int H, int tiles_x) {
     const int f = blockIdx.y;
