@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
             inv[1] = sp.invD[1];
             inv[2] = sp.invD[2];
 #pragma unroll
-            for (int l = 0; l < 4; ++l) P[l] = sp.P[l];
+            for (int l = 0; l < 4; ++l) P[l] = 0.0f;     // ortho: per-frame phase, read at the end
         } else {
             const float d0 = __fmaf_rn(fpy, sp.Ey[0], __fmaf_rn(fpx, sp.Ex[0], sp.F0[0]));
             const float d1 = __fmaf_rn(fpy, sp.Ey[1], __fmaf_rn(fpx, sp.Ex[1], sp.F0[1]));
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
             if (l < mc.n_lights) {
-                const float w = P[l] * S[l];
+                const float w = (PROJ == 0 ? sp.P[l] : P[l]) * S[l];
                 L0 += sp.rgb[l][0] * w;
                 L1 += sp.rgb[l][1] * w;
                 L2 += sp.rgb[l][2] * w;
