@@ -110,7 +110,8 @@ constexpr int kSweepSmemK = 64;   // windows of at most 64 points per line stage
 template <int LAYOUT>
 __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __restrict__ fps,
                                                        const TvParams* __restrict__ tvp, int slots, int Astr,
-                                                       int Kstr, int64_t slot_elems, float2* __restrict__ buf) {
+                                                       int Kstr, int64_t slot_elems, int smem_k,
+                                                       float2* __restrict__ buf) {
     const int fs = blockIdx.y, f = fs / slots;
     const TvParams& t = tvp[fs];
     const int line = blockIdx.x * blockDim.x + threadIdx.x;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __rest
                     z = __fmaf_rn(kf, t.d[2], base[2]);
         return t.kh * (inside(v, x, y, z) ? sample<LAYOUT, false>(v, x, y, z, unused) : 0.0f);
     };
-    if (t.k_hi - t.k_lo < kSweepSmemK) {
+    if (t.k_hi - t.k_lo < smem_k) {
         // the line's kappa h rho_k staged in shared memory (a column per thread, conflict-free),
         // then one backward walk writes each lattice point once: tau+ is the exclusive suffix,
         // tau- = total - (tau+ + s_k) (absolute rounding ~ a few ulp of the line total)
@@ -191,12 +192,14 @@ cudaError_t launch_tv_sweep(const FrameParams* fps, const TvParams* tvp, int F, 
     (void)mc;
     const dim3 grid((unsigned)(((int64_t)Astr * Bstr + 127) / 128), (unsigned)(F * slots));
     const int64_t slot_elems = (int64_t)Astr * Bstr * Kstr;
-    const size_t smem = (size_t)kSweepSmemK * 128 * sizeof(float);
+    // stage up to min(Kstr, 64) points per line: no more shared memory than the longest window
+    const int smem_k = Kstr < kSweepSmemK ? Kstr : kSweepSmemK;
+    const size_t smem = (size_t)smem_k * 128 * sizeof(float);
     switch (layout) {
-        case kLinearF32: tv_sweep_kernel<kLinearF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
-        case kQuadF32: tv_sweep_kernel<kQuadF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
-        case kCornerF16: tv_sweep_kernel<kCornerF16><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
-        case kOctF32: tv_sweep_kernel<kOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, buf); break;
+        case kLinearF32: tv_sweep_kernel<kLinearF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
+        case kQuadF32: tv_sweep_kernel<kQuadF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
+        case kCornerF16: tv_sweep_kernel<kCornerF16><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
+        case kOctF32: tv_sweep_kernel<kOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
