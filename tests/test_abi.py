@@ -172,3 +172,17 @@ def test_binding_has_no_fallback(monkeypatch, nsl):
     monkeypatch.setattr(nsl, "LIB_PATH", "/nonexistent/libnsl.so")
     with pytest.raises(nsl.NslError):
         nsl.lib()
+
+
+def test_c_example_compiles_as_c99(tmp_path):
+    """The boundary is plain C: examples/guiding_map_c.c builds with gcc -std=c99 -Wall -Werror
+    against include/nsl.h and links against libnsl.so (no CUDA headers, no Python)."""
+    import subprocess
+    import paper_2604_03748_b200 as nsl
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(nsl.build())
+    exe = tmp_path / "gm"
+    subprocess.check_call(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "guiding_map_c.c"), "-L", libdir, "-lnsl",
+                           f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)])
+    assert exe.exists()
