@@ -36,46 +36,54 @@ __device__ __forceinline__ double hg64(double g, double c) {
     return dd(ds(1.0, dm(g, g)), dm(dm(4.0, 3.141592653589793), dm(d, __dsqrt_rn(d))));
 }
 
-__global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_light* __restrict__ lights, int F,
-                                   MarchConst mc, FrameParams* __restrict__ out) {
+// One warp per frame: every lane evaluates the camera basis (and the guide set's t), lane a < 3
+// the per-axis constants of axis a, lane l < 4 the constants of light l, so the fp64 divide /
+// sqrt chains run side by side instead of one after another; each lane writes its own fields
+// with exactly the operations (and order) of C3/C3b/C10, so every value is unchanged.
+constexpr int kSetupWarps = 4;
+__global__ void __launch_bounds__(32 * kSetupWarps) frame_setup_kernel(const FrameIn* __restrict__ in,
+                                                                      const nsl_light* __restrict__ lights, int F,
+                                                                      MarchConst mc, FrameParams* __restrict__ out) {
     pdl_trigger();                     // the march (PDL) may launch now; it waits for this grid
-    int fi = blockIdx.x * blockDim.x + threadIdx.x;
+    const int fi = blockIdx.x * kSetupWarps + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (fi >= F) {
         pdl_wait();
         return;
     }
     const FrameIn& fr = in[fi];
     const nsl_camera& cam = fr.cam;
-    FrameParams p;
-    // ---- volume
-    p.data = fr.vol.data;
-    p.layout = fr.vol.layout;
-    p.nx = fr.vol.nx;
-    p.ny = fr.vol.ny;
-    p.nz = fr.vol.nz;
-    if (p.layout == kLinearF32) {
-        p.sy = p.nx + 2;
-        p.sz = (p.nx + 2) * (p.ny + 2);
-    } else {
-        p.sy = p.nx + 1;
-        p.sz = (p.nx + 1) * (p.ny + 1);
+    FrameParams& p = out[fi];
+    const int nx = fr.vol.nx, ny = fr.vol.ny, nz = fr.vol.nz;
+    const float supp[3] = {(float)(nx + 1), (float)(ny + 1), (float)(nz + 1)};
+    if (lane == 0) {                   // ---- volume and scalar fields
+        p.data = fr.vol.data;
+        p.layout = fr.vol.layout;
+        p.nx = nx;
+        p.ny = ny;
+        p.nz = nz;
+        if (p.layout == kLinearF32) {
+            p.sy = nx + 2;
+            p.sz = (nx + 2) * (ny + 2);
+        } else {
+            p.sy = nx + 1;
+            p.sz = (nx + 1) * (ny + 1);
+        }
+        for (int q = 0; q < 3; ++q) p.supp[q] = supp[q];
+        p.projection = cam.projection;
+        p.W = cam.width;
+        p.H = cam.height;
+        p.frame_id = fr.frame_id;
+        p.occ = fr.vol.occ;
+        p.occ_shift = fr.vol.og.shift;
+        p.occ_nbx = fr.vol.og.nbx;
+        p.occ_nby = fr.vol.og.nby;
+        p.occ_words = fr.vol.og.words_total;   // mask + slab boxes
+        p.slab_off = fr.vol.og.words;
+        p.occ_nbz = fr.vol.og.nbz;
+        p.pad2[0] = p.pad2[1] = p.pad2[2] = 0;
     }
-    p.supp[0] = (float)(p.nx + 1);
-    p.supp[1] = (float)(p.ny + 1);
-    p.supp[2] = (float)(p.nz + 1);
-    p.projection = cam.projection;
-    p.W = cam.width;
-    p.H = cam.height;
-    p.frame_id = fr.frame_id;
-    p.occ = fr.vol.occ;
-    p.occ_shift = fr.vol.og.shift;
-    p.occ_nbx = fr.vol.og.nbx;
-    p.occ_nby = fr.vol.og.nby;
-    p.occ_words = fr.vol.og.words_total;   // mask + slab boxes are staged together
-    p.slab_off = fr.vol.og.words;
-    p.occ_nbz = fr.vol.og.nbz;
 
-    // ---- camera basis (C3)
+    // ---- camera basis (C3), every lane
     const double dx = (double)fr.vol.dx;
     double Fw[3] = {cam.forward[0], cam.forward[1], cam.forward[2]};
     double Up[3] = {cam.up[0], cam.up[1], cam.up[2]};
@@ -92,13 +100,16 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
     const double ax = dd(dm(ay, W), H);
     const double cx = ds(dd(1.0, W), 1.0), cy = ds(1.0, dd(1.0, H));
     const double ex = dd(2.0, W), ey = dd(-2.0, H);
-    p.inv_dx = (float)dd(1.0, dx);
-    for (int a = 0; a < 3; ++a) {
+    if (lane == 0) p.inv_dx = (float)dd(1.0, dx);
+    float Dg = 0.0f;
+    if (lane < 3) {                    // ---- axis a = lane
+        const int a = lane;
         const double P = (double)cam.position[a], o = (double)fr.vol.origin[a];
         double w = da(P, dm(dm(cx, ax), r[a]));
         w = da(w, dm(dm(cy, ay), u[a]));
         p.B[a] = (float)da(dd(ds(w, o), dx), 0.5);
-        p.Dg[a] = (float)dd(f[a], dx);
+        Dg = (float)dd(f[a], dx);
+        p.Dg[a] = Dg;
         p.Oe[a] = (float)da(dd(ds(P, o), dx), 0.5);
         p.F0[a] = (float)da(da(f[a], dm(dm(cx, ax), r[a])), dm(dm(cy, ay), u[a]));
         p.fwd[a] = (float)f[a];
@@ -109,102 +120,113 @@ __global__ void frame_setup_kernel(const FrameIn* __restrict__ in, const nsl_lig
             p.Ex[a] = (float)dm(dm(ex, ax), r[a]);
             p.Ey[a] = (float)dm(dm(ey, ay), u[a]);
         }
+        // estimate helper (never decides an index on its own)
+        p.invD[a] = Dg != 0.0f ? 1.0f / Dg : 0.0f;
     }
 
-    // ---- lights (C3b): explicit, or the surrogate set of eq:approx
-    double Ln[4][3] = {};
+    // ---- light l = lane (C3b): explicit, or the surrogate set of eq:approx
+    const int l = lane;
+    const bool on = l < mc.n_lights;
+    double Ln[3] = {0.0, 0.0, 0.0};
     const nsl_light* L = lights + (size_t)fi * mc.n_lights;
-    if (mc.light_mode == NSL_LIGHTS_GUIDE) {
-        double om[3] = {-f[0], -f[1], -f[2]};
-        double A[3] = {mc.axis[0], mc.axis[1], mc.axis[2]};
-        if (A[0] == 0.0 && A[1] == 0.0 && A[2] == 0.0) A[2] = 1.0;
-        double nA = norm3(A);
-        double an[3] = {dd(A[0], nA), dd(A[1], nA), dd(A[2], nA)};
-        double s[3];
-        cross3(om, an, s);
-        double ns = norm3(s);
-        if (ns < 1e-6) {
-            const double xh[3] = {1.0, 0.0, 0.0};
-            cross3(om, xh, s);
-            ns = norm3(s);
-        }
-        double t[3] = {dd(s[0], ns), dd(s[1], ns), dd(s[2], ns)};
-        for (int q = 0; q < 3; ++q) {
-            Ln[0][q] = om[q];
-            Ln[1][q] = t[q];
-            Ln[2][q] = -t[q];
-        }
-    } else {
-        for (int l = 0; l < mc.n_lights; ++l) {
+    if (l < 4 && on) {
+        if (mc.light_mode == NSL_LIGHTS_GUIDE) {
+            double om[3] = {-f[0], -f[1], -f[2]};
+            if (l == 0) {
+                for (int q = 0; q < 3; ++q) Ln[q] = om[q];
+            } else {
+                double A[3] = {mc.axis[0], mc.axis[1], mc.axis[2]};
+                if (A[0] == 0.0 && A[1] == 0.0 && A[2] == 0.0) A[2] = 1.0;
+                double nA = norm3(A);
+                double an[3] = {dd(A[0], nA), dd(A[1], nA), dd(A[2], nA)};
+                double sv[3];
+                cross3(om, an, sv);
+                double ns = norm3(sv);
+                if (ns < 1e-6) {
+                    const double xh[3] = {1.0, 0.0, 0.0};
+                    cross3(om, xh, sv);
+                    ns = norm3(sv);
+                }
+                for (int q = 0; q < 3; ++q) {
+                    const double t = dd(sv[q], ns);
+                    Ln[q] = l == 1 ? t : -t;
+                }
+            }
+        } else {
             double v[3] = {L[l].to_light[0], L[l].to_light[1], L[l].to_light[2]};
             double nl = norm3(v);
-            for (int q = 0; q < 3; ++q) Ln[l][q] = dd(v[q], nl);
+            for (int q = 0; q < 3; ++q) Ln[q] = dd(v[q], nl);
         }
     }
-    for (int l = 0; l < 4; ++l) {
-        const bool on = l < mc.n_lights;
+    float Lg[3] = {0.0f, 0.0f, 0.0f};
+    if (l < 4) {
         for (int q = 0; q < 3; ++q) {
-            p.Ln[l][q] = on ? (float)Ln[l][q] : 0.0f;
-            p.Lg[l][q] = on ? (float)dd(Ln[l][q], dx) : 0.0f;
+            Lg[q] = on ? (float)dd(Ln[q], dx) : 0.0f;
+            p.Ln[l][q] = on ? (float)Ln[q] : 0.0f;
+            p.Lg[l][q] = Lg[q];
             p.rgb[l][q] = on ? L[l].rgb[q] : 0.0f;
         }
         // cos theta = to_light . dir (C10); per frame for ortho (dir = f)
-        p.P[l] = on ? (float)hg64((double)mc.g, dot3(Ln[l], f)) : 0.0f;
-    }
-    // ---- C9 preconditions: front light is exactly -D_g, orthographic, h_l == h
-    bool ok = mc.front_identity && mc.light_mode == NSL_LIGHTS_GUIDE && cam.projection == 0 && mc.hl == mc.h;
-    for (int q = 0; q < 3; ++q) ok = ok && (p.Lg[0][q] == -p.Dg[q]);
-    p.front_ok = ok ? 1 : 0;
-    // ---- estimate helpers (never decide an index on their own: every use is
-    //      followed by exact prescribed-op checks in march.cu)
-    for (int q = 0; q < 3; ++q) p.invD[q] = p.Dg[q] != 0.0f ? 1.0f / p.Dg[q] : 0.0f;
-    for (int l = 0; l < 4; ++l)
-        for (int q = 0; q < 3; ++q) {
-            const float L = p.Lg[l][q];
-            p.lim[l][q] = L > 0.0f ? p.supp[q] : (L < 0.0f ? 0.0f : 3.0e38f);
-            p.ilh[l][q] = L != 0.0f ? 1.0f / (L * mc.hl) : 1.0f;
+        p.P[l] = on ? (float)hg64((double)mc.g, dot3(Ln, f)) : 0.0f;
+        for (int q = 0; q < 3; ++q) {  // estimate helpers
+            p.lim[l][q] = Lg[q] > 0.0f ? supp[q] : (Lg[q] < 0.0f ? 0.0f : 3.0e38f);
+            p.ilh[l][q] = Lg[q] != 0.0f ? 1.0f / (Lg[q] * mc.hl) : 1.0f;
         }
-    bool pair = mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3;
-    for (int q = 0; q < 3; ++q) pair = pair && (p.Lg[2][q] == -p.Lg[1][q]);
-    p.pair12 = pair ? 1 : 0;
-    // occupied box in padded-index positions: cells [bmin*B, (bmax+1)*B) -> U in [lo, hi), clipped to the support
+    }
+    // ---- cross-lane predicates: C9 (front light exactly -D_g), the opposite guide pair, L_z == 0
+    float Dga[3], Lg1[3], Lg2[3], Lg0[3];
+    for (int q = 0; q < 3; ++q) {
+        Dga[q] = __shfl_sync(0xffffffffu, Dg, q);
+        Lg0[q] = __shfl_sync(0xffffffffu, Lg[q], 0);
+        Lg1[q] = __shfl_sync(0xffffffffu, Lg[q], 1);
+        Lg2[q] = __shfl_sync(0xffffffffu, Lg[q], 2);
+    }
+    const unsigned lz = __ballot_sync(0xffffffffu, l < 4 && on && Lg[2] == 0.0f);
+    if (lane == 0) {
+        bool ok = mc.front_identity && mc.light_mode == NSL_LIGHTS_GUIDE && cam.projection == 0 && mc.hl == mc.h;
+        for (int q = 0; q < 3; ++q) ok = ok && (Lg0[q] == -Dga[q]);
+        p.front_ok = ok ? 1 : 0;
+        bool pair = mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3;
+        for (int q = 0; q < 3; ++q) pair = pair && (Lg2[q] == -Lg1[q]);
+        p.pair12 = pair ? 1 : 0;
+        p.lz0 = (int32_t)(lz & 0xfu);   // horizontal light: marches stay in one z slab
+    }
+    // ---- occupied box in padded-index positions: cells [bmin*B, (bmax+1)*B) -> U in [lo, hi),
+    //      clipped to the support
     pdl_wait();                        // launched with PDL after the volume build: the AABB is its output
+    float alo[3], ahi[3];
     if (fr.vol.aabb) {
         const int B = 1 << fr.vol.og.shift;
         for (int q = 0; q < 3; ++q) {
             const int bmin = fr.vol.aabb[q], bmax = fr.vol.aabb[3 + q];
             if (bmin > bmax) {                      // empty volume: a point box
-                p.alo[q] = 0.0f;
-                p.ahi[q] = 0.0f;
+                alo[q] = 0.0f;
+                ahi[q] = 0.0f;
             } else {
-                p.alo[q] = (float)(bmin * B);
-                p.ahi[q] = fminf((float)((bmax + 1) * B), p.supp[q]);
+                alo[q] = (float)(bmin * B);
+                ahi[q] = fminf((float)((bmax + 1) * B), supp[q]);
             }
         }
     } else {
         for (int q = 0; q < 3; ++q) {
-            p.alo[q] = 0.0f;
-            p.ahi[q] = p.supp[q];
+            alo[q] = 0.0f;
+            ahi[q] = supp[q];
         }
     }
-    for (int l = 0; l < 4; ++l)
-        for (int q = 0; q < 3; ++q) {
-            const float L = p.Lg[l][q];
-            p.alim[l][q] = L > 0.0f ? p.ahi[q] : (L < 0.0f ? p.alo[q] : 3.0e38f);
-        }
-    p.lz0 = 0;
-    for (int l = 0; l < 4; ++l)
-        if (l < mc.n_lights && p.Lg[l][2] == 0.0f) p.lz0 |= 1 << l;   // horizontal light: marches stay in one z slab
-    out[fi] = p;
+    if (lane < 3) {
+        p.alo[lane] = alo[lane];
+        p.ahi[lane] = ahi[lane];
+    }
+    if (l < 4)
+        for (int q = 0; q < 3; ++q) p.alim[l][q] = Lg[q] > 0.0f ? ahi[q] : (Lg[q] < 0.0f ? alo[q] : 3.0e38f);
 }
 
 }  // namespace
 
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s) {
-    int threads = 64;
-    int blocks = (F + threads - 1) / threads;
-    return launch_pdl(frame_setup_kernel, dim3(blocks), dim3(threads), 0, s, in, lights, F, mc, out);
+    const int blocks = (F + kSetupWarps - 1) / kSetupWarps;
+    return launch_pdl(frame_setup_kernel, dim3(blocks), dim3(32 * kSetupWarps), 0, s, in, lights, F, mc, out);
 }
 
 }  // namespace nsl
