@@ -90,3 +90,14 @@ def test_tv_explicit_lights_C3_subsampled(nsl):
     pix = np.arange(0, 1024 * 1024, 997)
     for f in range(2):
         compare_frame(w, f, g[f], gd[f], gdbg[f], pixels=pix)
+
+
+def test_tv_parity_C4_C5_subsampled(nsl):
+    """The animated 256^3 plume (C4, a fresh volume per frame) and the 512^3 / 2048^2 stress
+    config (C5, groups of one frame under the default budget): sampled pixels vs the oracle."""
+    for cfg, frames, step in (("C4", [0, 120], 613), ("C5", [0, 700], 4099)):
+        w = tv(I.make_workload(cfg, frames=frames))
+        g, gd, _ = run(nsl, w, debug=False)
+        pix = np.arange(0, w.height * w.width, step)
+        for f in range(len(frames)):
+            compare_frame(w, f, g[f], gd[f], None, pixels=pix)
