@@ -116,6 +116,8 @@ __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __rest
     const TvParams& t = tvp[fs];
     const int line = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = line % Astr, j = line / Astr;
+    // the host's stride bounds (capi tv_geometry) hold every device-computed lattice
+    NSL_ASSERT(t.A <= Astr && t.K <= Kstr && (int64_t)Astr * t.B * Kstr <= slot_elems);
     if (i < t.i_lo || i > t.i_hi || j < t.j_lo || j > t.j_hi) return;
     const FrameParams& sp = fps[f];
     Vol v;

@@ -180,9 +180,10 @@ def test_c_example_compiles_as_c99(tmp_path):
     import subprocess
     import paper_2604_03748_b200 as nsl
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    libdir = os.path.dirname(nsl.build())
+    lib = nsl.build()                      # the library in use (NSL_LIB may point at a build variant)
+    libdir = os.path.dirname(lib)
     exe = tmp_path / "gm"
     subprocess.check_call(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
-                           os.path.join(root, "examples", "guiding_map_c.c"), "-L", libdir, "-lnsl",
+                           os.path.join(root, "examples", "guiding_map_c.c"), lib,
                            f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)])
     assert exe.exists()
