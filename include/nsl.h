@@ -285,6 +285,14 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
                                 const uint32_t* frame_ids, int32_t F,
                                 float* host_rgbt, float* host_depth, nsl_stream stream);
 
+/* The surrogate light set of eq:approx (C3b) for a camera:
+ * out[0] front = omega = -forward, out[1] top = normalize(omega x axis), out[2] bottom =
+ * -top (axis NULL -> world z; fallback x^ when omega is parallel to axis), as the fp32 unit
+ * vectors the march uses in NSL_LIGHTS_GUIDE mode (computed by the same device code), each
+ * with radiance rgb (NULL -> white).  Host outputs; synchronises `stream`. */
+nsl_status nsl_guide_lights(const nsl_camera* cam, const float axis[3], const float rgb[3], nsl_light out[3],
+                            nsl_stream stream);
+
 /* ------------------------------------------------------------------ debug / verification
  * Frame constants of DESIGN.md C3/C3b/C10 as the device computes them
  * (fp64 evaluation rounded once to fp32), for bitwise comparison with the

@@ -103,7 +103,7 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_batch_counted",
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
-           "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight"]
+           "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights"]
 
 
 class BakeS(ctypes.Structure):
@@ -149,6 +149,7 @@ def lib():
     L.nsl_debug_jitter.argtypes = [P(MarchS), u32, i32, vp, vp, vp]
     L.nsl_sixway_bake.argtypes = [P(vp), i32, P(i32), P(CameraS), P(MediumS), P(BakeS), P(u32), i32, vp, vp, vp]
     L.nsl_debug_bake_lights.argtypes = [P(GridDesc), P(CameraS), vp, vp, vp]
+    L.nsl_guide_lights.argtypes = [P(CameraS), vp, vp, P(LightS), vp]
     L.nsl_relight.argtypes = [P(CameraS), i32, vp, vp, P(LightS), i32, P(ctypes.c_float), P(ctypes.c_float),
                               vp, vp, ctypes.c_float, vp, vp]
     for name in EXPORTS[2:]:
@@ -411,6 +412,18 @@ class RelightCall:
 
     def __call__(self, stream=None):
         _check(lib().nsl_relight(*self.args, _stream_handle(stream)), "nsl_relight")
+
+
+def guide_lights(cam, axis=None, rgb=None, stream=None):
+    """The surrogate light set of eq:approx (front, top, bottom) for a camera, as the device
+    computes it: a list of three (to_light, rgb) tuples."""
+    out = (LightS * 3)()
+    ax = None if axis is None else _f3(axis)
+    col = None if rgb is None else _f3(rgb)
+    _check(lib().nsl_guide_lights(ctypes.byref(camera_s(cam)), None if ax is None else ctypes.addressof(ax),
+                                  None if col is None else ctypes.addressof(col), out, _stream_handle(stream)),
+           "nsl_guide_lights")
+    return [(tuple(out[l].to_light), tuple(out[l].rgb)) for l in range(3)]
 
 
 def run_bake(w, bake, layout: int = LAYOUT_DEFAULT, vols=None, out=None, stream=None):

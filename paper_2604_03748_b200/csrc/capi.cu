@@ -887,6 +887,37 @@ nsl_status nsl_debug_frame_constants(const nsl_grid_desc* g, const nsl_camera* c
     return NSL_OK;
 }
 
+nsl_status nsl_guide_lights(const nsl_camera* cam, const float axis[3], const float rgb[3], nsl_light out[3],
+                            nsl_stream stream) {
+    g_err.clear();
+    if (!cam || !out) return fail(NSL_ERR_INVALID_ARG, "NULL camera/out");
+    if (axis && !finite3(axis)) return fail(NSL_ERR_INVALID_ARG, "axis must be finite");
+    if (rgb && (!finite3(rgb) || rgb[0] < 0.0f || rgb[1] < 0.0f || rgb[2] < 0.0f))
+        return fail(NSL_ERR_INVALID_ARG, "rgb must be finite and >= 0");
+    const nsl_grid_desc g = {1, 1, 1, {0.0f, 0.0f, 0.0f}, 1.0f};
+    const nsl_medium med = {1.0f, 1.0f, 0.0f};
+    nsl_march m;
+    memset(&m, 0, sizeof m);
+    m.step = 1.0f;
+    m.t_min = 1e-4f;
+    m.guide_axis[0] = axis ? axis[0] : 0.0f;
+    m.guide_axis[1] = axis ? axis[1] : 0.0f;
+    m.guide_axis[2] = axis ? axis[2] : 1.0f;
+    nsl_light in[3];
+    for (int l = 0; l < 3; ++l)
+        for (int a = 0; a < 3; ++a) {
+            in[l].to_light[a] = a == 0 ? 1.0f : 0.0f;      // ignored in guide mode
+            in[l].rgb[a] = rgb ? rgb[a] : 1.0f;
+        }
+    nsl_frame_constants fc;
+    if (nsl_status st = nsl_debug_frame_constants(&g, cam, in, 3, NSL_LIGHTS_GUIDE, &med, &m, &fc, stream)) return st;
+    for (int l = 0; l < 3; ++l) {
+        memcpy(out[l].to_light, fc.Ln[l], sizeof out[l].to_light);
+        memcpy(out[l].rgb, in[l].rgb, sizeof out[l].rgb);
+    }
+    return NSL_OK;
+}
+
 nsl_status nsl_debug_jitter(const nsl_march* m, uint32_t frame_id, int32_t n, uint32_t* out_hash, float* out_delta,
                             nsl_stream stream) {
     g_err.clear();

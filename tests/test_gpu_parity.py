@@ -51,6 +51,22 @@ def test_frame_constants_bitwise(nsl, cfg, kw):
             assert a["front_identity_ok"] == 1
 
 
+def test_guide_lights_match_the_oracle(nsl):
+    """nsl_guide_lights returns the march's fp32 guide set (front = -forward, top/bottom =
+    +-normalize(omega x z)) bit for bit like the oracle's C3b, horizontal for a z-up axis."""
+    for yaw in (0.0, 37.0, 123.0, 271.0):
+        cam = I.orbit_camera(yaw, 64, 64)
+        got = nsl.guide_lights(cam, rgb=(0.5, 0.25, 1.0))
+        w = I.make_workload("C1")
+        ref = oracle.frame_constants(w.grid, cam, [I.Light((1.0, 0.0, 0.0), (1.0, 1.0, 1.0))] * 3, I.LIGHTS_GUIDE,
+                                     w.medium, w.march)
+        for l in range(3):
+            assert np.array_equal(bits(got[l][0]), bits(ref["Ln"][l]))
+            assert got[l][1] == (0.5, 0.25, 1.0)
+        assert got[1][0][2] == 0.0 and got[2][0][2] == 0.0
+        assert abs(float(np.dot(got[0][0], got[1][0]))) < 1e-6
+
+
 def test_frame_constants_random_cameras(nsl):
     rng = np.random.default_rng(11)
     for trial in range(40):
