@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--impl", default="nsl", choices=["nsl", "reference"])
     p.add_argument("--config", default="C2")
     p.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
-    p.add_argument("--layout", default="oct_f32", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32"])
+    p.add_argument("--layout", default="oct_f32", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32", "brick_oct_f32"])
     p.add_argument("--light-model", default="march", choices=["march", "tv"],
                    help="march: canonical C8 (the headline); tv: NEXT-4 transmittance volume (DESIGN.md §12)")
     p.add_argument("--no-e2e", action="store_true")

@@ -66,12 +66,16 @@ typedef struct {
  *               fp16 (1 x 16-B gather/sample); values rounded RNE to fp16
  *  OCT_F32    : per padded cell (i,j,k), i<=nx, j<=ny, k<=nz, the QUAD float4 of
  *               planes k and k+1 side by side (32 B: one 256-bit gather/sample),
- *               exact fp32 values; storage must be 32-B aligned  */
+ *               exact fp32 values; storage must be 32-B aligned
+ *  BRICK_OCT_F32: the OCT elements in 4x4x4-cell bricks (2 KB each, x fastest inside
+ *               a brick): one 256-bit gather/sample, 3-D locality per 128-B line;
+ *               storage must be 32-B aligned (measured against OCT: DESIGN.md §6)  */
 typedef enum {
     NSL_LAYOUT_LINEAR_F32 = 0,
     NSL_LAYOUT_QUAD_F32 = 1,
     NSL_LAYOUT_CORNER_F16 = 2,
     NSL_LAYOUT_OCT_F32 = 3,
+    NSL_LAYOUT_BRICK_OCT_F32 = 4,
     NSL_LAYOUT_DEFAULT = 3
 } nsl_layout;
 

@@ -25,9 +25,9 @@ HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_HERE, 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
 
-LAYOUT_LINEAR_F32, LAYOUT_QUAD_F32, LAYOUT_CORNER_F16, LAYOUT_OCT_F32 = 0, 1, 2, 3
+LAYOUT_LINEAR_F32, LAYOUT_QUAD_F32, LAYOUT_CORNER_F16, LAYOUT_OCT_F32, LAYOUT_BRICK_OCT_F32 = 0, 1, 2, 3, 4
 LAYOUT_DEFAULT = LAYOUT_OCT_F32
-LAYOUTS = {"linear_f32": 0, "quad_f32": 1, "corner_f16": 2, "oct_f32": 3}
+LAYOUTS = {"linear_f32": 0, "quad_f32": 1, "corner_f16": 2, "oct_f32": 3, "brick_oct_f32": 4}
 LIGHTS_EXPLICIT, LIGHTS_GUIDE = 0, 1
 LIGHT_MARCH, LIGHT_TV = 0, 1
 

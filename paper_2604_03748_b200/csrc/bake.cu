@@ -320,6 +320,7 @@ cudaError_t launch_bake(const FrameParams* fp, const BakeFrame* bf, const BakeCo
         case kQuadF32: return launch_bake_l<kQuadF32>(fp, bf, bc, F, W, H, projection, out, s);
         case kCornerF16: return launch_bake_l<kCornerF16>(fp, bf, bc, F, W, H, projection, out, s);
         case kOctF32: return launch_bake_l<kOctF32>(fp, bf, bc, F, W, H, projection, out, s);
+        case kBrickOctF32: return launch_bake_l<kBrickOctF32>(fp, bf, bc, F, W, H, projection, out, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -83,7 +83,8 @@ nsl_status check_grid(const nsl_grid_desc* g) {
 }
 
 nsl_status check_layout(int layout) {
-    if (layout != kLinearF32 && layout != kQuadF32 && layout != kCornerF16 && layout != kOctF32)
+    if (layout != kLinearF32 && layout != kQuadF32 && layout != kCornerF16 && layout != kOctF32 &&
+        layout != kBrickOctF32)
         return fail(NSL_ERR_INVALID_ARG, "unknown layout %d", layout);
     return NSL_OK;
 }
@@ -289,8 +290,9 @@ static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* densit
     if (nsl_status st = check_grid(g)) return st;
     if (nsl_status st = check_layout(layout)) return st;
     if (!density || !device_storage || !out) return fail(NSL_ERR_INVALID_ARG, "NULL density/storage/out");
-    if (reinterpret_cast<uintptr_t>(device_storage) % (layout == kOctF32 ? 32 : 16))
-        return fail(NSL_ERR_INVALID_ARG, "storage must be %d-B aligned", layout == kOctF32 ? 32 : 16);
+    const int align = layout == kOctF32 || layout == kBrickOctF32 ? 32 : 16;
+    if (reinterpret_cast<uintptr_t>(device_storage) % align)
+        return fail(NSL_ERR_INVALID_ARG, "storage must be %d-B aligned", align);
     const size_t need = nsl_volume_bytes(g, layout);
     if (storage_bytes < need) return fail(NSL_ERR_INVALID_ARG, "storage_bytes %zu < required %zu", storage_bytes, need);
     const size_t n = (size_t)g->nx * g->ny * g->nz;

@@ -425,6 +425,7 @@ cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int
         case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
         case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
         case kOctF32: return launch_l<kOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
+        case kBrickOctF32: return launch_l<kBrickOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
     }
     return cudaErrorInvalidValue;
 }

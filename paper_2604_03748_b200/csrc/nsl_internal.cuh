@@ -184,6 +184,7 @@ constexpr int kLinearF32 = NSL_LAYOUT_LINEAR_F32;
 constexpr int kQuadF32 = NSL_LAYOUT_QUAD_F32;
 constexpr int kCornerF16 = NSL_LAYOUT_CORNER_F16;
 constexpr int kOctF32 = NSL_LAYOUT_OCT_F32;
+constexpr int kBrickOctF32 = NSL_LAYOUT_BRICK_OCT_F32;
 
 // Launch helpers implemented in the .cu files.
 // layout + occupancy + AABB + invalid-voxel count from the raw grid (two launches, no memsets)

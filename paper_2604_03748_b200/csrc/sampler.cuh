@@ -78,7 +78,10 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
     if (COUNT) ++gathers;
     const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias)),
                 fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
-    const int e = ix + iy * v.sy + iz * v.sz;
+    const int e = LAYOUT == kBrickOctF32
+                      ? (((iz >> 2) * v.sz + (iy >> 2) * v.sy + (ix >> 2)) << 6) | ((iz & 3) << 4) | ((iy & 3) << 2) |
+                            (ix & 3)
+                      : ix + iy * v.sy + iz * v.sz;
     if (LAYOUT == kLinearF32) {
         const float* p = static_cast<const float*>(v.data) + e;
         const float c000 = __ldg(p), c100 = __ldg(p + 1);
@@ -94,7 +97,7 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
         const float x00 = __fmaf_rn(fx, q0.y, q0.x), x10 = __fmaf_rn(fx, q0.w, q0.z);
         const float x01 = __fmaf_rn(fx, q1.y, q1.x), x11 = __fmaf_rn(fx, q1.w, q1.z);
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
-    } else if (LAYOUT == kOctF32) {
+    } else if (LAYOUT == kOctF32 || LAYOUT == kBrickOctF32) {
         // one 256-bit gather: (c000, c100 - c000, c010, c110 - c010 | the same for plane k+1)
         float a0, a1, a2, a3, b0, b1, b2, b3;
         asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"

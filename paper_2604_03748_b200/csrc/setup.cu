@@ -64,6 +64,9 @@ __global__ void __launch_bounds__(32 * kSetupWarps) frame_setup_kernel(const Fra
         if (p.layout == kLinearF32) {
             p.sy = nx + 2;
             p.sz = (nx + 2) * (ny + 2);
+        } else if (p.layout == kBrickOctF32) {     // strides in bricks of 4^3 cells
+            p.sy = (nx + 4) / 4;
+            p.sz = ((nx + 4) / 4) * ((ny + 4) / 4);
         } else {
             p.sy = nx + 1;
             p.sz = (nx + 1) * (ny + 1);

@@ -202,6 +202,7 @@ cudaError_t launch_tv_sweep(const FrameParams* fps, const TvParams* tvp, int F, 
         case kQuadF32: tv_sweep_kernel<kQuadF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
         case kCornerF16: tv_sweep_kernel<kCornerF16><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
         case kOctF32: tv_sweep_kernel<kOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
+        case kBrickOctF32: tv_sweep_kernel<kBrickOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -19,6 +19,7 @@ size_t layout_elems(int layout, int nx, int ny, int nz) {
         case kQuadF32: return (size_t)(nx + 1) * (ny + 1) * (nz + 2);
         case kCornerF16: return (size_t)(nx + 1) * (ny + 1) * (nz + 1);
         case kOctF32: return (size_t)(nx + 1) * (ny + 1) * (nz + 1);
+        case kBrickOctF32: return (size_t)((nx + 4) / 4) * ((ny + 4) / 4) * ((nz + 4) / 4) * 64;
     }
     return 0;
 }
@@ -29,6 +30,7 @@ size_t layout_elem_bytes(int layout) {
         case kQuadF32: return 16;
         case kCornerF16: return 16;
         case kOctF32: return 32;
+        case kBrickOctF32: return 32;
     }
     return 0;
 }
@@ -144,6 +146,30 @@ __device__ __forceinline__ void layout_oct_cta(const Raw& r, float* __restrict__
             for (int t = 0; t < 4; ++t) q[t] = n[t];
         }
     }
+}
+
+// BRICK_OCT: element e = brick * 64 + (i & 3) + 4 (j & 3) + 16 (k & 3), brick = ((k >> 2) nby_b +
+// (j >> 2)) nbx_b + (i >> 2); one thread per element (coalesced 256-bit stores), cells beyond
+// (n_x, n_y, n_z) in the last bricks hold zeros (never sampled).
+__device__ __forceinline__ void layout_brick_oct_cta(const Raw& r, float* __restrict__ out, int pb) {
+    const int nbx = (r.nx + 4) / 4, nby = (r.ny + 4) / 4, nbz = (r.nz + 4) / 4;
+    const int64_t e = (int64_t)pb * 256 + threadIdx.x;
+    if (e >= (int64_t)nbx * nby * nbz * 64) return;
+    const int off = (int)(e & 63);
+    const int64_t b = e >> 6;
+    const int bx = (int)(b % nbx), by = (int)((b / nbx) % nby), bz = (int)(b / ((int64_t)nbx * nby));
+    const int i = bx * 4 + (off & 3), j = by * 4 + ((off >> 2) & 3), k = bz * 4 + (off >> 4);
+    float c[8];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const float c0 = r.at(i, j, k + t), c1 = r.at(i + 1, j, k + t);
+        const float c2 = r.at(i, j + 1, k + t), c3 = r.at(i + 1, j + 1, k + t);
+        c[4 * t + 0] = c0;
+        c[4 * t + 1] = __fsub_rn(c1, c0);
+        c[4 * t + 2] = c2;
+        c[4 * t + 3] = __fsub_rn(c3, c2);
+    }
+    st256(out + 8 * e, c);
 }
 
 // ---------------------------------------------------------------- occupancy role
@@ -272,6 +298,7 @@ __global__ void __launch_bounds__(256, 6) volume_build_kernel(Raw r, void* __res
     if (LAYOUT == kQuadF32) layout_quad_cta(r, static_cast<float4*>(out), pb, kb, kstep);
     if (LAYOUT == kCornerF16) layout_corner_f16_cta(r, static_cast<uint4*>(out), pb, kb, kstep);
     if (LAYOUT == kOctF32) layout_oct_cta(r, static_cast<float*>(out), pb, kb, kstep);
+    if (LAYOUT == kBrickOctF32) layout_brick_oct_cta(r, static_cast<float*>(out), pb);
 }
 
 // The occupancy region [mask: words][slab_min: nbz x (bx, by)][slab_max: nbz x (bx, by)], the
@@ -391,10 +418,13 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
     Raw r{raw, v.nx, v.ny, v.nz};
     const int plane = v.layout == kLinearF32 ? (v.nx + 2) * (v.ny + 2) : (v.nx + 1) * (v.ny + 1);
     const int planes = v.layout == kCornerF16 || v.layout == kOctF32 ? v.nz + 1 : v.nz + 2;
-    const int plane_blocks = (plane + 255) / 256;
-    int kstep = v.layout == kQuadF32  ? (planes + kQuadPlanes - 1) / kQuadPlanes
-                : v.layout == kOctF32 ? (planes + kOctRun - 1) / kOctRun
-                                      : planes;
+    const int plane_blocks = v.layout == kBrickOctF32
+                                 ? (int)((layout_elems(kBrickOctF32, v.nx, v.ny, v.nz) + 255) / 256)
+                                 : (plane + 255) / 256;
+    int kstep = v.layout == kQuadF32       ? (planes + kQuadPlanes - 1) / kQuadPlanes
+                : v.layout == kOctF32      ? (planes + kOctRun - 1) / kOctRun
+                : v.layout == kBrickOctF32 ? 1
+                                           : planes;
     const long max_layout_ctas = 2000000000L - v.og.rows;
     if ((long)plane_blocks * kstep > max_layout_ctas) kstep = (int)(max_layout_ctas / plane_blocks);
     const unsigned grid = (unsigned)(v.og.rows + (long)plane_blocks * kstep);
@@ -415,6 +445,10 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
             break;
         case kOctF32:
             volume_build_kernel<kOctF32><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
+                                                                          occ_stride);
+            break;
+        case kBrickOctF32:
+            volume_build_kernel<kBrickOctF32><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
                                                                           occ_stride);
             break;
         default:

@@ -133,7 +133,7 @@ def test_parity_C1_corner_f16(nsl):
 def test_layouts_agree_bitwise(nsl):
     w = I.make_workload("C2", frames=[3])
     a = run(nsl, w, layout=0)
-    for lay in (1, 3):
+    for lay in (1, 3, 4):
         b = run(nsl, w, layout=lay)
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
@@ -270,7 +270,7 @@ def test_device_upload_reports_invalid_values(nsl):
     d = torch.ones((8, 8, 8), device="cuda")
     d[1, 2, 3] = float("nan")
     d[4, 4, 4] = -2.0
-    for layout in (0, 1, 2, 3):
+    for layout in (0, 1, 2, 3, 4):
         v = nsl.Volume(g, d, layout)
         assert v.check() == 2
     v = nsl.Volume(g, torch.ones((8, 8, 8), device="cuda"), 1)
