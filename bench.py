@@ -197,6 +197,24 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def launches_per_step(w, args) -> int:
+    """Kernels of one timed step: volume_build + occ_finalize per distinct volume, then
+    frame_setup, tile_cull and march_kernel; the TV light model adds tv_setup and, per frame
+    group (NSL_TV_BUDGET_MB, the library's host bound), tv_sweep + tile_cull + march_kernel."""
+    n = 2 * len(w.volume_specs) + 1
+    if args.light_model != "tv":
+        return n + 2
+    g = w.grid
+    diag = math.sqrt((g.nx + 1) ** 2 + (g.ny + 1) ** 2 + (g.nz + 1) ** 2)
+    hl = w.march.light_step if w.march.light_step > 0 else w.march.step
+    astr = math.ceil(diag) + 6
+    kstr = math.ceil(diag / (hl / g.voxel_width * (1 - 1e-5))) + 6
+    slots = 1 if w.light_mode == 1 else len(w.lights[0])
+    per_frame = 8 * astr * astr * kstr * slots
+    group = max(1, min(w.n_frames, int(float(os.environ.get("NSL_TV_BUDGET_MB", "1024")) * 1048576 // per_frame)))
+    return n + 1 + 3 * math.ceil(w.n_frames / group)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -323,7 +341,8 @@ def main():
             "samples_per_s": counts["canonical_samples"] * world * K / t_loop,
             "ms_per_frame": ms_step / F, "frames_per_s": F * world * K / t_loop,
             "march_ms_per_step": statistics.mean(march_ms), "layout_ms_per_step": statistics.mean(layout_ms),
-            "counts_per_rank_step": counts, "gpu_launches": 4 * K, "clocks": clk, "roofline": roof}
+            "counts_per_rank_step": counts, "gpu_launches": launches_per_step(w, args) * K, "clocks": clk,
+            "roofline": roof}
 
     # optional result gather to rank 0 (the only collective of the design; not in the timed step)
     if world > 1 and args.gather:
