@@ -347,6 +347,10 @@ def test_random_tiny_cases(nsl):
         w = _case(grid, vals, cam, lights, mode, med, m, frame_id=int(rng.integers(0, 1000)))
         g, gd, gdbg = run(nsl, w)
         compare_frame(w, 0, g[0], gd[0], gdbg[0])
+        if trial % 2 == 0:             # the same case under the NEXT-4 light model
+            wt = replace(w, march=replace(m, light_model=1))
+            g, gd, gdbg = run(nsl, wt, layout=3)
+            compare_frame(wt, 0, g[0], gd[0], gdbg[0])
 
 
 def test_plan_equals_batch_and_counts(nsl):
