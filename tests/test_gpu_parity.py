@@ -376,3 +376,32 @@ def test_plan_equals_batch_and_counts(nsl):
     assert c["light_samples"] == d[:, 5].sum()
     assert c["occupied_samples"] == d[:, 4].sum()
     assert 0 < c["gathers"] <= c["tested_primary"] + c["tested_light"] <= c["canonical_samples"]
+
+
+def test_plan_execute_is_cuda_graph_capturable(nsl):
+    """The timed path (volume re-build + plan execute: 5 PDL-chained kernels, no host sync, no
+    memcpy) captures into a CUDA graph; replays give the eager results bit for bit."""
+    import torch
+    w = I.make_workload("C2", frames=[0, 17, 41])
+    raw = torch.from_numpy(w.volume(0)).cuda()
+    storage = torch.empty(nsl.volume_bytes(w.grid, 3), dtype=torch.uint8, device="cuda")
+    vols = [nsl.Volume(w.grid, raw, 3, storage=storage)]
+    plan = nsl.make_plan(w, vols)
+    outs = nsl.alloc_outputs(w.n_frames, w.height, w.width)
+    plan.execute(outs[0], outs[1])
+    torch.cuda.synchronize()
+    ref = (outs[0].clone(), outs[1].clone())
+    outs[0].zero_()
+    outs[1].zero_()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    keep = []
+    with torch.cuda.graph(g, stream=s):
+        keep.append(nsl.Volume(w.grid, raw, 3, storage=storage, stream=s))
+        plan.execute(outs[0], outs[1], stream=s)
+    for _ in range(3):
+        outs[0].zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], ref[0]) and torch.equal(outs[1], ref[1])
