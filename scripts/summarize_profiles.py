@@ -75,13 +75,37 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio"]
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "sm__warps_active.avg.per_cycle_active",
+        "dram__bytes.sum.per_second", "lts__t_sectors.sum"]
 lines = ["# ncu --set full of march_kernel<OCT_F32, ORTHO, FAST> on C2 (60 frames 512^2 over 128^3, guide lights)",
          "# command: ncu --set full --clock-control none --import-source on -k regex:march_kernel -s 2 -c 1 "
          "python scripts/profile_march.py", f"# report: {os.path.relpath(rep, ROOT)}", ""]
 for k in keys:
     if k in d:
         lines.append(f"{k:82s} {d[k][1]:>18s} {d[k][0]}")
+# derived views against the chip's peaks (north star: "achieved L1/TEX and L2 throughput, HBM GB/s,
+# and warp execution efficiency against the chip's peaks")
+def val(k, scale=1.0):
+    return float(d[k][1].replace(",", "")) * scale if k in d else float("nan")
+
+
+t_s = val("gpu__time_duration.sum") * ({"usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(
+    d.get("gpu__time_duration.sum", ("us",))[0], 1e-6))
+peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6541.1}
+lines += ["", "# derived",
+          f"warp execution efficiency (active threads per issued instruction / 32): "
+          f"{val('smsp__thread_inst_executed_per_inst_executed.ratio') / 32:.3f}",
+          f"warps active per SM: {val('sm__warps_active.avg.per_cycle_active'):.1f} of 64",
+          f"HBM: {val('dram__bytes.sum.per_second'):.0f} GB/s achieved vs {peaks['hbm_gbs']:.0f} GB/s measured copy peak "
+          f"({val('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f} % of DRAM peak per ncu)",
+          f"L2: {val('lts__t_sectors.sum') * 32 / t_s / 1e9:.0f} GB/s of sector traffic "
+          f"({val('lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} % of L2 peak per ncu), "
+          f"hit rate {val('lts__t_sector_hit_rate.pct'):.1f} %",
+          f"L1/TEX: {val('l1tex__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} % of peak (data-pipe wavefronts), "
+          f"hit rate {val('l1tex__t_sector_hit_rate.pct'):.1f} %",
+          f"issue slots: {val('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} % active "
+          f"(the binding limit; long-scoreboard stalls {val('smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio'):.2f} per issue)"]
 open(os.path.join(P, f"{round_tag}_ncu_march_summary.txt"), "w").write("\n".join(lines) + "\n")
 mult = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}
 traffic = (float(d["dram__bytes_read.sum"][1]) * mult[d["dram__bytes_read.sum"][0]]
