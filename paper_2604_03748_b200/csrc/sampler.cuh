@@ -39,6 +39,9 @@ static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (3
 #define NSL_MINB 5   // min resident CTAs per SM requested from ptxas (register cap = 65536 / (256 * NSL_MINB));
                      // 5 (<= 51 registers, 40 warps/SM) measured fastest on C2 (profiles/r1_sweep.txt)
 #endif
+#ifndef NSL_VOL_EVF
+#define NSL_VOL_EVF 1   // OCT gathers marked L1::evict_first (the mask and frame constants stay): -0.3 %
+#endif
 constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
@@ -100,9 +103,15 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
     } else if (LAYOUT == kOctF32 || LAYOUT == kBrickOctF32) {
         // one 256-bit gather: (c000, c100 - c000, c010, c110 - c010 | the same for plane k+1)
         float a0, a1, a2, a3, b0, b1, b2, b3;
+#if NSL_VOL_EVF
+        asm("ld.global.nc.L1::evict_first.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
+            : "l"(static_cast<const float*>(v.data) + 8 * (size_t)e));
+#else
         asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
             : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
             : "l"(static_cast<const float*>(v.data) + 8 * (size_t)e));
+#endif
         const float x00 = __fmaf_rn(fx, a1, a0), x10 = __fmaf_rn(fx, a3, a2);
         const float x01 = __fmaf_rn(fx, b1, b0), x11 = __fmaf_rn(fx, b3, b2);
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
