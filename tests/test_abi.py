@@ -147,6 +147,7 @@ def test_march_argument_validation(nsl):
         (dict(march=replace(w.march, depth_tau=-1.0)), "depth_tau"),
         (dict(march=replace(w.march, max_steps=-2)), "max_steps"),
         (dict(march=replace(w.march, jitter=2)), "jitter"),
+        (dict(march=replace(w.march, light_model=7)), "light_model"),
         (dict(lights=[[I.Light((1, 0, 0), (1, 1, 1))] * 4], mode=I.LIGHTS_GUIDE), "at most 3"),
         (dict(lights=[[I.Light((2, 0, 0), (1, 1, 1))]], mode=I.LIGHTS_EXPLICIT), "not unit"),
         (dict(lights=[[I.Light((1, 0, 0), (-1, 1, 1))]], mode=I.LIGHTS_EXPLICIT), "rgb"),
@@ -156,6 +157,37 @@ def test_march_argument_validation(nsl):
     for over, needle in cases:
         rc, msg = _batch_rc(nsl, w, **over)
         assert rc == 1, (over, msg)
+        assert needle in msg, (needle, msg)
+
+
+def test_relight_and_guide_lights_validation(nsl):
+    """NEXT-2/3 and the guide-light helper reject bad arguments on the host, before any CUDA call."""
+    L = nsl.lib()
+    cam = nsl.camera_s(I.Camera(I.ORTHO, (0.5, 0.5, 2.0), (0.0, 0.0, -1.0), (0.0, 1.0, 0.0), 1.0, 4, 4))
+    f3 = ctypes.c_float * 3
+    ok = nsl.lights_s([[I.Light((1.0, 0.0, 0.0), (1, 1, 1))]])
+    five = nsl.lights_s([[I.Light((1.0, 0.0, 0.0), (1, 1, 1))] * 5])
+    bad = nsl.lights_s([[I.Light((2.0, 0.0, 0.0), (1, 1, 1))]])
+    nan_axis = f3(0, 0, float("nan"))
+    cases = [
+        (lambda: L.nsl_relight(ctypes.byref(cam), 1, 4096, None, five, 5, f3(0, 0, 0), f3(0, 0, 0), None, None,
+                               2e-3, 4096, None), "n_lights"),
+        (lambda: L.nsl_relight(ctypes.byref(cam), 1, 4096, None, bad, 1, f3(0, 0, 0), f3(0, 0, 0), None, None,
+                               2e-3, 4096, None), "not unit"),
+        (lambda: L.nsl_relight(ctypes.byref(cam), 1, 4100, None, ok, 1, f3(0, 0, 0), f3(0, 0, 0), None, None,
+                               2e-3, 4096, None), "aligned"),
+        (lambda: L.nsl_relight(ctypes.byref(cam), 1, 4096, None, ok, 1, f3(0, 0, 0), f3(0, 0, 0), None, None,
+                               -1.0, 4096, None), "bias"),
+        (lambda: L.nsl_relight(ctypes.byref(cam), 0, 4096, None, ok, 1, f3(0, 0, 0), f3(0, 0, 0), None, None,
+                               2e-3, 4096, None), "F"),
+        (lambda: L.nsl_guide_lights(None, None, None, None, None), "NULL"),
+        (lambda: L.nsl_guide_lights(ctypes.byref(cam), ctypes.addressof(nan_axis), None, (nsl.LightS * 3)(), None),
+         "axis"),
+    ]
+    for call, needle in cases:
+        rc = call()
+        msg = L.nsl_last_error().decode()
+        assert rc == 1, (needle, msg)
         assert needle in msg, (needle, msg)
 
 
