@@ -142,7 +142,7 @@ typedef struct {
  * light_model NSL_LIGHT_MARCH (C8, canonical) or NSL_LIGHT_TV (NEXT-4,
  * per frame and light a swept optical-depth lattice, one
  * interpolated lookup per occupied sample; frames are processed in groups
- * whose lattices fit NSL_TV_BUDGET_MB of transient device memory). */
+ * whose lattices fit NSL_TV_BUDGET_MB (default 4096) of transient device memory). */
 enum { NSL_LIGHT_MARCH = 0, NSL_LIGHT_TV = 1 };
 typedef struct {
     float step, light_step;
