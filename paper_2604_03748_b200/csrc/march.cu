@@ -84,8 +84,10 @@ __device__ __forceinline__ float2 tv_lookup(const TvParams& t, const float2* __r
     return r;
 }
 
-template <int LAYOUT, int PROJ, int MODE, bool TV>
-__global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
+// G3: the guide set of three lights (front + the exactly opposite top/bottom pair, pair12 by
+// construction): the explicit-light paths are compiled out, so the kernel carries less state.
+template <int LAYOUT, int PROJ, int MODE, bool TV, bool G3>
+__global__ void __launch_bounds__(kThreads, (G3 ? NSL_MINB_G3 : NSL_MINB) * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H,
@@ -222,7 +224,8 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
         uint32_t n_occ = 0, lsamp = 0;
         // C9 precondition per ray: step 1 lies outside the support (i.e. n_lo >= 2)
         const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && m_lo <= m_hi && !r.in(v, 1);
-        const bool paired = sp.pair12 != 0;
+        const bool paired = G3 || sp.pair12 != 0;
+        const int n_lights = G3 ? 3 : mc.n_lights;
         float nf = (float)m_lo;
         for (int n = m_lo; n <= m_hi; ++n, nf += 1.0f) {
             float t, x, y, z;
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
                 }
 #pragma unroll
                 for (int l = 0; l < 4; ++l) {             // C8 + C10
-                    if (l < mc.n_lights && !(!TV && paired && (l == 1 || l == 2))) {
+                    if (l < n_lights && !(!TV && paired && (l == 1 || l == 2))) {
                         float Tl;
                         const float lx = sp.Lg[l][0], ly = sp.Lg[l][1], lz = sp.Lg[l][2];
                         if (l == 0 && front_fast) {
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, NSL_MINB * 256 / kThreads) march_ker
         float L0 = 0.0f, L1 = 0.0f, L2 = 0.0f;
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            if (l < mc.n_lights) {
+            if (l < n_lights) {
                 const float w = (PROJ == 0 ? sp.P[l] : P[l]) * S[l];
                 L0 += sp.rgb[l][0] * w;
                 L1 += sp.rgb[l][1] * w;
@@ -384,10 +387,13 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
     }
     const dim3 grid((unsigned)F, (unsigned)tiles);
     if (tv)
-        return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth,
-                          debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, *tv);
-    return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth, debug,
-                      counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
+        return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, false>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
+                          depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, *tv);
+    if (NSL_G3 && MODE == kFast && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
+        return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, NSL_G3 != 0>, grid, dim3(kThreads), 0, s, fp, mc,
+                          rgbt, depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
+    return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, false>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth,
+                      debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
 }
 
 template <int LAYOUT, int PROJ>

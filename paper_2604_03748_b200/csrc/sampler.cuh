@@ -42,6 +42,12 @@ static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (3
 #ifndef NSL_VOL_EVF
 #define NSL_VOL_EVF 1   // OCT gathers marked L1::evict_first (the mask and frame constants stay): -0.3 %
 #endif
+#ifndef NSL_G3
+#define NSL_G3 1    // FAST guide-set (3 lights) launches use the march specialised for it
+#endif
+#ifndef NSL_MINB_G3
+#define NSL_MINB_G3 6   // its register cap (40: 48 warps/SM)
+#endif
 constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
