@@ -106,6 +106,12 @@ __global__ void tv_setup_kernel(const FrameParams* __restrict__ fps, int F, int 
     out[idx] = t;
 }
 
+#ifndef NSL_SWEEP_2PASS
+#define NSL_SWEEP_2PASS 1
+#endif
+#ifndef NSL_SWEEP_NOSMEM
+#define NSL_SWEEP_NOSMEM 1
+#endif
 constexpr int kSweepSmemK = 64;   // windows of at most 64 points per line stage in shared memory
 template <int LAYOUT>
 __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __restrict__ fps,
@@ -164,6 +170,18 @@ __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __rest
         }
         return;
     }
+#if NSL_SWEEP_2PASS
+    // longer windows: the line total first, then the backward walk re-samples each point
+    // (the same values, so the result equals the staged path's) and writes it once
+    float tot = 0.0f;
+    for (int k = t.k_lo; k <= t.k_hi; ++k) tot += sample_k(k);
+    float suf = 0.0f;
+    for (int k = t.k_hi; k >= t.k_lo; --k) {
+        const float sv = sample_k(k);
+        col[(int64_t)k * Astr] = make_float2(suf, fmaxf(tot - (suf + sv), 0.0f));
+        suf += sv;
+    }
+#else
     float acc = 0.0f;                   // V4 tau-: exclusive prefix toward -d
     for (int k = t.k_lo; k <= t.k_hi; ++k) {
         const float sv = sample_k(k);
@@ -178,6 +196,7 @@ __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __rest
         col[(int64_t)k * Astr] = e;
         acc += sv;
     }
+#endif
 }
 
 }  // namespace
@@ -195,7 +214,8 @@ cudaError_t launch_tv_sweep(const FrameParams* fps, const TvParams* tvp, int F, 
     const dim3 grid((unsigned)(((int64_t)Astr * Bstr + 127) / 128), (unsigned)(F * slots));
     const int64_t slot_elems = (int64_t)Astr * Bstr * Kstr;
     // stage up to min(Kstr, 64) points per line: no more shared memory than the longest window
-    const int smem_k = Kstr < kSweepSmemK ? Kstr : kSweepSmemK;
+    int smem_k = Kstr < kSweepSmemK ? Kstr : kSweepSmemK;
+    if (NSL_SWEEP_2PASS && Kstr > kSweepSmemK * NSL_SWEEP_NOSMEM) smem_k = 0;   // every window may be long
     const size_t smem = (size_t)smem_k * 128 * sizeof(float);
     switch (layout) {
         case kLinearF32: tv_sweep_kernel<kLinearF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;

@@ -42,6 +42,16 @@ def test_tv_parity_C1(nsl, debug, kw):
     compare_frame(w, 0, g[0], gd[0], gdbg[0] if gdbg is not None else None)
 
 
+@pytest.mark.parametrize("debug", [True, False])
+def test_tv_long_windows_C1(nsl, debug):
+    """h_l = h / 8: lattice lines longer than the sweep's shared-memory stage (64 points),
+    so the sweep takes its long-window path."""
+    w = tv(I.make_workload("C1"))
+    w = replace(w, march=replace(w.march, light_step=w.march.step / 8))
+    g, gd, gdbg = run(nsl, w, debug=debug)
+    compare_frame(w, 0, g[0], gd[0], gdbg[0] if gdbg is not None else None)
+
+
 def test_tv_differs_from_march_only_in_light_transmittance(nsl):
     w = I.make_workload("C1")
     a = run(nsl, w)
