@@ -84,10 +84,11 @@ __device__ __forceinline__ float2 tv_lookup(const TvParams& t, const float2* __r
     return r;
 }
 
-// G3: the guide set of three lights (front + the exactly opposite top/bottom pair, pair12 by
-// construction): the explicit-light paths are compiled out, so the kernel carries less state.
-template <int LAYOUT, int PROJ, int MODE, bool TV, bool G3>
-__global__ void __launch_bounds__(kThreads, (G3 ? NSL_MINB_G3 : NSL_MINB) * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
+// NL: the light set fixed at compile time, so the paths it cannot take are compiled out and
+// the kernel carries less state: 3 = the guide set (front + the exactly opposite top/bottom
+// pair, pair12 by construction), 1 = one light (march or C9), 0 = any set (runtime).
+template <int LAYOUT, int PROJ, int MODE, bool TV, int NL>
+__global__ void __launch_bounds__(kThreads, (NL == 3 ? NSL_MINB_G3 : NL == 1 ? NSL_MINB_L1 : NSL_MINB) * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H,
@@ -224,8 +225,8 @@ __global__ void __launch_bounds__(kThreads, (G3 ? NSL_MINB_G3 : NSL_MINB) * 256 
         uint32_t n_occ = 0, lsamp = 0;
         // C9 precondition per ray: step 1 lies outside the support (i.e. n_lo >= 2)
         const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && m_lo <= m_hi && !r.in(v, 1);
-        const bool paired = G3 || sp.pair12 != 0;
-        const int n_lights = G3 ? 3 : mc.n_lights;
+        const bool paired = NL == 3 || (NL == 0 && sp.pair12 != 0);
+        const int n_lights = NL ? NL : mc.n_lights;
         float nf = (float)m_lo;
         for (int n = m_lo; n <= m_hi; ++n, nf += 1.0f) {
             float t, x, y, z;
@@ -386,13 +387,24 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
         if (e != cudaSuccess) return e;
     }
     const dim3 grid((unsigned)F, (unsigned)tiles);
-    if (tv)
-        return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, false>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
+    if (tv) {
+        if constexpr (MODE == kFast) {   // (the guide-set kernel with TV lookups spills: C2 +11 %)
+            if (NSL_TV_NL && mc.n_lights == 1)
+                return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 1>, grid, dim3(kThreads), 0, s, fp, mc,
+                                  rgbt, depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, *tv);
+        }
+        return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 0>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
                           depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, *tv);
-    if (NSL_G3 && MODE == kFast && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
-        return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, NSL_G3 != 0>, grid, dim3(kThreads), 0, s, fp, mc,
-                          rgbt, depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
-    return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, false>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth,
+    }
+    if constexpr (MODE == kFast) {
+        if (NSL_G3 && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
+            return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 3>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
+                              depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
+        if (NSL_L1 && mc.n_lights == 1)
+            return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 1>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
+                              depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
+    }
+    return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 0>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth,
                       debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
 }
 

@@ -45,6 +45,15 @@ static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (3
 #ifndef NSL_G3
 #define NSL_G3 1    // FAST guide-set (3 lights) launches use the march specialised for it
 #endif
+#ifndef NSL_L1                  // march specialised for a single light
+#define NSL_L1 1
+#endif
+#ifndef NSL_TV_NL               // the single-light kernel for the TV light model too
+#define NSL_TV_NL 1
+#endif
+#ifndef NSL_MINB_L1
+#define NSL_MINB_L1 6   // its register cap
+#endif
 #ifndef NSL_MINB_G3
 #define NSL_MINB_G3 6   // its register cap (40: 48 warps/SM)
 #endif

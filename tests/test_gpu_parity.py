@@ -115,9 +115,12 @@ def test_parity_C1(nsl, layout, kw):
     assert rep["samples"] > 50000
 
 
-def test_parity_C1_nondebug_front_identity(nsl):
-    """The timed path (no debug counters, C9 front-light shortcut) meets the value bar too."""
-    w = I.make_workload("C1")
+@pytest.mark.parametrize("kw", [{}, {"single_light": True}, {"perspective": True},
+                                {"perspective": True, "single_light": True}])
+def test_parity_C1_nondebug_front_identity(nsl, kw):
+    """The timed path (no debug counters; the guide-set kernel with the C9 front-light
+    shortcut, the single-light kernel, the generic one for perspective guide sets)."""
+    w = I.make_workload("C1", **kw)
     g, gd, _ = run(nsl, w, debug=False)
     compare_frame(w, 0, g[0], gd[0], None)
 
@@ -175,11 +178,12 @@ def test_parity_C2_density_sweep(nsl):
         compare_frame(w, 0, g[0], gd[0], gdbg[0])
 
 
-def test_parity_C3(nsl):
+@pytest.mark.parametrize("debug", [True, False])
+def test_parity_C3(nsl, debug):
     w = I.make_workload("C3", frames=[0, 30])
-    g, gd, gdbg = run(nsl, w)
+    g, gd, gdbg = run(nsl, w, debug=debug)
     for f in range(2):
-        compare_frame(w, f, g[f], gd[f], gdbg[f])
+        compare_frame(w, f, g[f], gd[f], None if gdbg is None else gdbg[f])
 
 
 def _subsample(H, W, step):
