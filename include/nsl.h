@@ -289,6 +289,28 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
                                 const uint32_t* frame_ids, int32_t F,
                                 float* host_rgbt, float* host_depth, nsl_stream stream);
 
+/* Animated volumes (SURVEY §8(a) rows a1 + a9, config C4; the simulator's
+ * density is "streamed directly into the guiding map generation", one grid per frame).
+ * Frame f's density densities[f] (DEVICE pointer, x-fastest nx*ny*nz fp32, like
+ * nsl_volume_upload with density_on_device = 1) is laid out into storage[f] (caller-owned
+ * device memory of storage_bytes >= nsl_volume_bytes(g, layout), aligned as for
+ * nsl_volume_upload; one buffer per frame, not shared between frames) and marched with
+ * cams[f] and lights[f*n_lights ...].  densities and storage are HOST arrays of F device
+ * pointers.  Frames run in chunks of `chunk` frames (0 -> 3): the layouts of chunk c+1 build
+ * on an internal side stream while chunk c marches on `stream` (the HBM-bound build hides
+ * under the latency-bound march).  Results are bitwise those of nsl_volume_upload of every
+ * frame followed by nsl_guiding_map_batch; outputs as nsl_guiding_map_batch (device, F*H*W*4
+ * and F*H*W floats).  Asynchronous: all work is ordered on `stream` on return, unless
+ * n_invalid (host pointer) is non-NULL, in which case the call synchronises `stream` and
+ * stores the number of non-finite or negative density values over all frames (counted by
+ * the build kernels; the maps of such frames are unspecified). */
+nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* densities, int32_t layout,
+                                    void* const* storage, size_t storage_bytes, const nsl_camera* cams,
+                                    const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                                    const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids,
+                                    int32_t F, int32_t chunk, float* out_rgbt, float* out_depth,
+                                    uint64_t* n_invalid, nsl_stream stream);
+
 /* The surrogate light set of eq:approx (C3b) for a camera:
  * out[0] front = omega = -forward, out[1] top = normalize(omega x axis), out[2] bottom =
  * -top (axis NULL -> world z; fallback x^ when omega is parallel to axis), as the fp32 unit

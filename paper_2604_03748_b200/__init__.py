@@ -103,7 +103,8 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_volume_release", "nsl_guiding_map", "nsl_guiding_map_batch", "nsl_guiding_map_batch_counted",
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
-           "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights"]
+           "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
+           "nsl_guiding_map_animated"]
 
 
 class BakeS(ctypes.Structure):
@@ -144,6 +145,9 @@ def lib():
     L.nsl_plan_destroy.argtypes = [vp]
     L.nsl_guiding_map_host.argtypes = [P(GridDesc), vp, i32, P(CameraS), P(LightS), i32, i32, P(MediumS),
                                        P(MarchS), P(u32), i32, vp, vp, vp]
+    L.nsl_guiding_map_animated.argtypes = [P(GridDesc), P(vp), i32, P(vp), ctypes.c_size_t, P(CameraS), P(LightS),
+                                           i32, i32, P(MediumS), P(MarchS), P(u32), i32, i32, vp, vp,
+                                           P(ctypes.c_uint64), vp]
     L.nsl_debug_frame_constants.argtypes = [P(GridDesc), P(CameraS), P(LightS), i32, i32, P(MediumS),
                                             P(MarchS), P(FrameConstantsS), vp]
     L.nsl_debug_jitter.argtypes = [P(MarchS), u32, i32, vp, vp, vp]
@@ -447,6 +451,48 @@ def guiding_map_host(grid, host_density, layout, cams, lights, light_mode, mediu
                                       lights_s(lights), len(lights[0]), light_mode, ctypes.byref(medium_s(medium)),
                                       ctypes.byref(march_s(march)), fid, F, host_rgbt.data_ptr(),
                                       host_depth.data_ptr(), _stream_handle(stream)), "nsl_guiding_map_host")
+
+
+class Animated:
+    """nsl_guiding_map_animated (rows a1 + a9, C4) with the host arguments marshalled once:
+    frame f's device density densities[f] is laid out into storages[f] and marched with
+    cams[f]; the layouts of the next chunk of frames build on a side stream while the current
+    chunk marches.  Calling it re-runs the whole step (e.g. after the simulator refreshed the
+    densities in place)."""
+
+    def __init__(self, grid, densities, layout, storages, cams, lights, light_mode, medium, march, frame_ids,
+                 chunk: int = 0):
+        F = len(cams)
+        assert len(densities) == F and len(storages) == F
+        for d in densities:
+            assert d.is_cuda and d.is_contiguous()
+        self._keep = (list(densities), list(storages))
+        self.F, self.layout, self.chunk, self.n_l, self.light_mode = F, layout, chunk, len(lights[0]), light_mode
+        self.nbytes = min(t.numel() for t in storages)
+        self.g = grid_desc(grid)
+        self.dp = (ctypes.c_void_p * F)(*[d.data_ptr() for d in densities])
+        self.sp = (ctypes.c_void_p * F)(*[t.data_ptr() for t in storages])
+        self.cs = (CameraS * F)(*[camera_s(c) for c in cams])
+        self.ls = lights_s(lights)
+        self.med, self.mar = medium_s(medium), march_s(march)
+        self.fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+
+    def __call__(self, out_rgbt, out_depth, check: bool = False, stream=None) -> Optional[int]:
+        """check=True synchronises and returns the number of invalid density values over all frames."""
+        n = ctypes.c_uint64()
+        _check(lib().nsl_guiding_map_animated(ctypes.byref(self.g), self.dp, self.layout, self.sp, self.nbytes,
+                                              self.cs, self.ls, self.n_l, self.light_mode, ctypes.byref(self.med),
+                                              ctypes.byref(self.mar), self.fid, self.F, self.chunk,
+                                              _ptr(out_rgbt), _ptr(out_depth), ctypes.byref(n) if check else None,
+                                              _stream_handle(stream)), "nsl_guiding_map_animated")
+        return n.value if check else None
+
+
+def guiding_map_animated(grid, densities, layout, storages, cams, lights, light_mode, medium, march, frame_ids,
+                         out_rgbt, out_depth, chunk: int = 0, check: bool = False, stream=None) -> Optional[int]:
+    """One-shot form of Animated (marshals the host arguments on every call)."""
+    return Animated(grid, densities, layout, storages, cams, lights, light_mode, medium, march, frame_ids,
+                    chunk)(out_rgbt, out_depth, check=check, stream=stream)
 
 
 def debug_frame_constants(grid, cam, lights, light_mode, medium, march, stream=None) -> dict:

@@ -236,8 +236,9 @@ std::vector<uint32_t> tile_order(int W, int H) {
     return out;
 }
 
-nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
-                        const MarchConst& mc, const std::vector<uint32_t>& order, cudaStream_t s, Workspace& ws) {
+// The frame tables (FrameIn, lights, tile order) uploaded into a fresh stream-ordered workspace.
+nsl_status upload_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
+                         const std::vector<uint32_t>& order, cudaStream_t s, Workspace& ws) {
     const int F = (int)frames.size();
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
@@ -256,7 +257,13 @@ nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lig
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
     if (!order.empty()) memcpy(host.data() + b_in + b_l, order.data(), sizeof(uint32_t) * order.size());
     NSL_CUDA(cudaMemcpyAsync(ws.base, host.data(), host.size(), cudaMemcpyHostToDevice, s), "frame table upload");
-    NSL_CUDA(launch_frame_setup(ws.in, ws.lights, F, mc, ws.params, s), "frame_setup_kernel launch");
+    return NSL_OK;
+}
+
+nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
+                        const MarchConst& mc, const std::vector<uint32_t>& order, cudaStream_t s, Workspace& ws) {
+    if (nsl_status st = upload_frames(frames, lights, n_lights, order, s, ws)) return st;
+    NSL_CUDA(launch_frame_setup(ws.in, ws.lights, (int)frames.size(), mc, ws.params, s), "frame_setup_kernel launch");
     return NSL_OK;
 }
 
@@ -276,6 +283,36 @@ static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* densit
                                      int32_t layout, void* device_storage, size_t storage_bytes, nsl_stream stream,
                                      nsl_volume** out, bool validate_host);
 
+// Host-only part of an upload: argument checks and the handle (no device work).
+static nsl_status volume_handle(const nsl_grid_desc* g, int32_t layout, void* device_storage, size_t storage_bytes,
+                                nsl_volume** out) {
+    if (nsl_status st = check_grid(g)) return st;
+    if (nsl_status st = check_layout(layout)) return st;
+    if (!device_storage) return fail(NSL_ERR_INVALID_ARG, "NULL storage");
+    const int align = layout == kOctF32 || layout == kBrickOctF32 ? 32 : 16;
+    if (reinterpret_cast<uintptr_t>(device_storage) % align)
+        return fail(NSL_ERR_INVALID_ARG, "storage must be %d-B aligned", align);
+    const size_t need = nsl_volume_bytes(g, layout);
+    if (storage_bytes < need) return fail(NSL_ERR_INVALID_ARG, "storage_bytes %zu < required %zu", storage_bytes, need);
+    nsl_volume* v = new nsl_volume;
+    v->g = *g;
+    v->layout = layout;
+    v->data = device_storage;
+    v->invalid = reinterpret_cast<unsigned long long*>(static_cast<char*>(device_storage) + tail_offset(g, layout));
+    v->occ = reinterpret_cast<uint32_t*>(static_cast<char*>(device_storage) + mask_offset(g, layout));
+    v->og = occ_geom(g->nx, g->ny, g->nz);
+    v->aabb = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(v->invalid) + 16);
+    *out = v;
+    return NSL_OK;
+}
+
+// Device part: the layout + occupancy build of a device-resident raw grid into v's storage.
+static cudaError_t enqueue_build(const nsl_volume* v, const float* raw, cudaStream_t s) {
+    return launch_volume_build(
+        raw, desc_of(v), v->data,
+        reinterpret_cast<uint32_t*>(static_cast<char*>(v->data) + scratch_offset(&v->g, v->layout)), v->invalid, s);
+}
+
 nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32_t density_on_device, int32_t layout,
                              void* device_storage, size_t storage_bytes, nsl_stream stream, nsl_volume** out) {
     return volume_upload_impl(g, density, density_on_device, layout, device_storage, storage_bytes, stream, out, true);
@@ -287,30 +324,18 @@ static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* densit
                                      int32_t layout, void* device_storage, size_t storage_bytes, nsl_stream stream,
                                      nsl_volume** out, bool validate_host) {
     g_err.clear();
-    if (nsl_status st = check_grid(g)) return st;
-    if (nsl_status st = check_layout(layout)) return st;
-    if (!density || !device_storage || !out) return fail(NSL_ERR_INVALID_ARG, "NULL density/storage/out");
-    const int align = layout == kOctF32 || layout == kBrickOctF32 ? 32 : 16;
-    if (reinterpret_cast<uintptr_t>(device_storage) % align)
-        return fail(NSL_ERR_INVALID_ARG, "storage must be %d-B aligned", align);
-    const size_t need = nsl_volume_bytes(g, layout);
-    if (storage_bytes < need) return fail(NSL_ERR_INVALID_ARG, "storage_bytes %zu < required %zu", storage_bytes, need);
+    if (!density || !out) return fail(NSL_ERR_INVALID_ARG, "NULL density/out");
+    nsl_volume* v = nullptr;
+    if (nsl_status st = volume_handle(g, layout, device_storage, storage_bytes, &v)) return st;
     const size_t n = (size_t)g->nx * g->ny * g->nz;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto bail = [&](nsl_status st) { delete v; return st; };
     if (!density_on_device && validate_host) {
         for (size_t i = 0; i < n; ++i)
             if (!(density[i] >= 0.0f) || !std::isfinite(density[i]))
-                return fail(NSL_ERR_INVALID_ARG, "density[%zu] = %g is not finite and >= 0", i, (double)density[i]);
+                return bail(fail(NSL_ERR_INVALID_ARG, "density[%zu] = %g is not finite and >= 0", i,
+                                 (double)density[i]));
     }
-    nsl_volume* v = new nsl_volume;
-    v->g = *g;
-    v->layout = layout;
-    v->data = device_storage;
-    v->invalid = reinterpret_cast<unsigned long long*>(static_cast<char*>(device_storage) + tail_offset(g, layout));
-    v->occ = reinterpret_cast<uint32_t*>(static_cast<char*>(device_storage) + mask_offset(g, layout));
-    v->og = occ_geom(g->nx, g->ny, g->nz);
-    v->aabb = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(v->invalid) + 16);
-    auto bail = [&](nsl_status st) { delete v; return st; };
     cudaError_t e = cudaSuccess;
     const float* raw = density;
     void* staging = nullptr;
@@ -322,9 +347,7 @@ static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* densit
         if (e != cudaSuccess) return bail(cuda_fail(e, "density upload"));
         raw = static_cast<const float*>(staging);
     }
-    e = launch_volume_build(raw, desc_of(v), device_storage,
-                            reinterpret_cast<uint32_t*>(static_cast<char*>(device_storage) + scratch_offset(g, layout)),
-                            v->invalid, s);
+    e = enqueue_build(v, raw, s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "volume build launch"));
     if (staging) {
         e = cudaFreeAsync(staging, s);
@@ -603,6 +626,116 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     if (es != cudaSuccess) return cuda_fail(es, "cudaStreamSynchronize");
     if (n_invalid) return fail(NSL_ERR_INVALID_ARG, "density has %llu non-finite or negative values", n_invalid);
     return NSL_OK;
+}
+
+// Animated volumes: frame f's density is laid out into its own storage and marched with its
+// own camera.  Chunks of frames: the layouts of chunk c+1 build on a side stream while chunk c
+// marches on `stream`; an event per chunk orders its march after its builds, and `stream`
+// waits for the side stream at the end, so everything is ordered on `stream` on return.
+nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* densities, int32_t layout,
+                                    void* const* storage, size_t storage_bytes, const nsl_camera* cams,
+                                    const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                                    const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                                    int32_t chunk, float* out_rgbt, float* out_depth, uint64_t* n_invalid,
+                                    nsl_stream stream) {
+    g_err.clear();
+    if (nsl_status st = check_grid(g)) return st;
+    if (nsl_status st = check_layout(layout)) return st;
+    if (!densities || !storage || !cams) return fail(NSL_ERR_INVALID_ARG, "NULL densities/storage/cameras");
+    if (F < 1) return fail(NSL_ERR_INVALID_ARG, "F must be >= 1");
+    if (chunk < 0) return fail(NSL_ERR_INVALID_ARG, "chunk must be >= 0");
+    if (nsl_status st = check_outputs(out_rgbt, out_depth)) return st;
+    // every argument is checked (host only) before anything is enqueued
+    std::vector<nsl_volume*> vols((size_t)F, nullptr);
+    auto release_all = [&]() {
+        for (nsl_volume* v : vols) nsl_volume_release(v);
+    };
+    for (int f = 0; f < F; ++f) {
+        nsl_status st = densities[f] ? volume_handle(g, layout, storage[f], storage_bytes, &vols[f])
+                                     : fail(NSL_ERR_INVALID_ARG, "NULL density of frame %d", f);
+        if (st != NSL_OK) {
+            release_all();
+            return st;
+        }
+    }
+    std::vector<int32_t> fv((size_t)F);
+    for (int f = 0; f < F; ++f) fv[f] = f;
+    Prepared P;
+    const nsl_volume* const* vp = const_cast<const nsl_volume* const*>(vols.data());
+    if (nsl_status st = prepare(vp, F, fv.data(), cams, lights, n_lights, light_mode, med, m, frame_ids, F, P)) {
+        release_all();
+        return st;
+    }
+    const int per = chunk > 0 ? chunk : 3;       // measured on C4: 3 frames per chunk
+    const size_t npf = (size_t)cams[0].width * cams[0].height;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream), side = nullptr;
+    std::vector<cudaEvent_t> evs;
+    auto event_on = [&](cudaStream_t from, cudaStream_t to) -> cudaError_t {
+        cudaEvent_t ev = nullptr;
+        cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+        evs.push_back(ev);
+        e = cudaEventRecord(ev, from);
+        return e == cudaSuccess ? cudaStreamWaitEvent(to, ev, 0) : e;
+    };
+    nsl_status st = NSL_OK;
+    cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e != cudaSuccess) st = cuda_fail(e, "cudaStreamCreate(side)");
+    if (st == NSL_OK && (e = event_on(s, side)) != cudaSuccess)   // builds follow earlier work on `stream`
+        st = cuda_fail(e, "stream ordering");
+    // frame tables of all F frames in one upload; per chunk only frame setup + march
+    Workspace ws;
+    void* tvws = nullptr;
+    const size_t tiles = march_cull_bytes(1, P.W, P.H);
+    Prepared Pc = P;                             // a chunk's view of P (F = frames of the chunk)
+    Pc.tv_group = P.tv_group < per ? P.tv_group : per;
+    if (st == NSL_OK) st = upload_frames(P.frames, lights, n_lights, tile_order(P.W, P.H), s, ws);
+    if (st == NSL_OK && P.tv_slots) {
+        Pc.F = per;
+        e = cudaMallocAsync(&tvws, align_up(Pc.tv_params_bytes(), 256) + Pc.tv_buf_bytes(), s);
+        if (e != cudaSuccess) st = cuda_fail(e, "cudaMallocAsync(TV workspace)");
+    }
+    for (int f0 = 0; st == NSL_OK && f0 < F; f0 += per) {
+        const int n = F - f0 < per ? F - f0 : per;
+        for (int f = f0; e == cudaSuccess && f < f0 + n; ++f) e = enqueue_build(vols[f], densities[f], side);
+        if (e != cudaSuccess) {
+            st = cuda_fail(e, "volume build launch");
+            break;
+        }
+        if ((e = event_on(side, s)) != cudaSuccess) {
+            st = cuda_fail(e, "chunk ordering");
+            break;
+        }
+        Pc.F = n;
+        e = launch_frame_setup(ws.in + f0, ws.lights + (size_t)f0 * n_lights, n, P.mc, ws.params + f0, s);
+        if (e == cudaSuccess)
+            e = run_march(Pc, ws.params + f0, ws.order, ws.cull + (size_t)f0 * tiles, static_cast<TvParams*>(tvws),
+                          reinterpret_cast<float2*>(static_cast<char*>(tvws) + align_up(Pc.tv_params_bytes(), 256)),
+                          out_rgbt + (size_t)f0 * npf * 4, out_depth + (size_t)f0 * npf, nullptr, nullptr, s);
+        if (e != cudaSuccess) st = cuda_fail(e, "march launch");
+    }
+    if (tvws) cudaFreeAsync(tvws, s);
+    if (ws.base) cudaFreeAsync(ws.base, s);
+    if (side) {
+        e = event_on(side, s);                   // `stream` resumes after every build
+        if (e != cudaSuccess) cudaStreamSynchronize(side);
+    }
+    unsigned long long* counts = nullptr;
+    if (st == NSL_OK && n_invalid) {             // the build kernels' invalid-voxel counters
+        e = cudaMallocHost(&counts, sizeof(unsigned long long) * F);
+        for (int f = 0; e == cudaSuccess && f < F; ++f)
+            e = cudaMemcpyAsync(counts + f, vols[f]->invalid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_fail(e, "invalid-voxel counters");
+        uint64_t tot = 0;
+        for (int f = 0; st == NSL_OK && f < F; ++f) tot += counts[f];
+        *n_invalid = tot;
+    }
+    if (counts) cudaFreeHost(counts);
+    release_all();
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);   // released once they complete
+    if (side) cudaStreamDestroy(side);
+    return st;
 }
 
 struct nsl_plan {

@@ -2,7 +2,8 @@
 plus 60 frame marches.  Sequential: build everything, then march everything (what bench.py
 times).  Pipelined: frames in chunks, chunk c+1's volumes build on a second stream while chunk
 c marches (stream events order each chunk's march after its builds) - the HBM-bound builds hide
-under the latency-bound marches.  Device time per step, L2 flushed between steps.
+under the latency-bound marches.  Library: the same schedule inside one C-ABI call,
+nsl_guiding_map_animated.  Device time per step, L2 flushed between steps.
 
     python scripts/bench_pipeline.py [--config C4 --frames 60 --chunk 6 --steps 5]
 """
@@ -85,10 +86,25 @@ def timed(fn):
     return statistics.median(ts)
 
 
+dens = [raw[w.frame_vol[f]] for f in range(F)]
+stor_f = [storage[w.frame_vol[f]] for f in range(F)]
+
+
+anim = nsl.Animated(w.grid, dens, layout, stor_f, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                    w.frame_ids, chunk=a.chunk)
+
+
+def library():
+    anim(outs[0], outs[1], stream=sa)
+
+
 t_seq = timed(sequential)
 ref = (outs[0].clone(), outs[1].clone())
 t_pipe = timed(pipelined)
 same = bool(torch.equal(outs[0], ref[0]) and torch.equal(outs[1], ref[1]))
+t_lib = timed(library)
+same_lib = bool(torch.equal(outs[0], ref[0]) and torch.equal(outs[1], ref[1]))
 print(json.dumps({"config": a.config, "frames": F, "volumes": len(raw), "chunk": a.chunk,
                   "sequential_ms_per_step": t_seq, "pipelined_ms_per_step": t_pipe,
-                  "speedup": t_seq / t_pipe, "outputs_bitwise_equal": same}))
+                  "library_ms_per_step": t_lib, "speedup": t_seq / t_pipe, "library_speedup": t_seq / t_lib,
+                  "outputs_bitwise_equal": same and same_lib}))

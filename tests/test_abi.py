@@ -191,6 +191,42 @@ def test_relight_and_guide_lights_validation(nsl):
         assert needle in msg, (needle, msg)
 
 
+def test_animated_validation(nsl):
+    """nsl_guiding_map_animated checks every frame's storage, camera and light before enqueuing."""
+    from dataclasses import replace
+    L = nsl.lib()
+    w = I.make_workload("C1")
+    g = nsl.grid_desc(w.grid)
+    nb = nsl.volume_bytes(w.grid, 3)
+    F = 2
+    cams = (nsl.CameraS * F)(*[nsl.camera_s(w.cameras[0])] * F)
+    bad_cams = (nsl.CameraS * F)(nsl.camera_s(w.cameras[0]), nsl.camera_s(replace(w.cameras[0], width=0)))
+    ls = nsl.lights_s([w.lights[0]] * F)
+    med, mar = nsl.medium_s(w.medium), nsl.march_s(w.march)
+    fid = (ctypes.c_uint32 * F)(0, 1)
+    vp2 = ctypes.c_void_p * F
+
+    def call(dens=(4096, 4096), stor=(8192, 8192), nbytes=nb, cs=cams, f=F, chunk=0, rgbt=4096):
+        return L.nsl_guiding_map_animated(ctypes.byref(g), vp2(*dens), 3, vp2(*stor), nbytes, cs, ls,
+                                          len(w.lights[0]), w.light_mode, ctypes.byref(med), ctypes.byref(mar),
+                                          fid, f, chunk, rgbt, 4096, None, None)
+    cases = [
+        (dict(dens=(4096, 0)), "NULL density of frame 1"),
+        (dict(stor=(8192, 0)), "NULL storage"),
+        (dict(stor=(8192, 8200)), "aligned"),
+        (dict(nbytes=nb - 1), "storage_bytes"),
+        (dict(cs=bad_cams), "width"),
+        (dict(f=0), "F must be"),
+        (dict(chunk=-1), "chunk"),
+        (dict(rgbt=4100), "aligned"),
+    ]
+    for over, needle in cases:
+        rc = call(**over)
+        msg = L.nsl_last_error().decode()
+        assert rc == 1, (over, msg)
+        assert needle in msg, (needle, msg)
+
+
 def test_mixed_sizes_rejected(nsl):
     from dataclasses import replace
     w = I.make_workload("C2", frames=[0, 1])
