@@ -197,6 +197,34 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def sampler_ceiling(layout, counts, march_s):
+    import torch
+    import nsl_inputs as I
+    import paper_2604_03748_b200 as nsl
+    n = 16
+    rng = np.random.default_rng(7)
+    dens = torch.from_numpy((0.5 + 0.1 * rng.random((n, n, n))).astype(np.float32)).cuda()
+    vol = nsl.Volume(I.Grid(n, n, n, (0.0, 0.0, 0.0), 1.0 / n), dens, layout)
+    sink = torch.empty(148 * 16 * 4 * 128, dtype=torch.float32, device="cuda")
+    nsl.bench_l1_gather(vol, sink)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        samples = nsl.bench_l1_gather(vol, sink)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    peak = samples / statistics.median(ts)
+    gathers = counts["gathers"] / march_s
+    tested = (counts["tested_primary"] + counts["tested_light"]) / march_s
+    return {"samples_per_s": peak, "source": "nsl_bench_l1_gather, 16^3 fully occupied grid, same layout",
+            "executed_gathers_per_s": gathers, "frac_gathers": gathers / peak,
+            "tested_samples_per_s": tested, "frac_tested": tested / peak}
+
+
+
 def launches_per_step(w, args) -> int:
     """Kernels of one timed step: volume_build + occ_finalize per distinct volume, then
     frame_setup, tile_cull and march_kernel; the TV light model adds tv_setup and, per frame
@@ -330,6 +358,14 @@ def main():
             "executed_gather_gbs": counts["gathers"] * bytes_per_sample / march_s / 1e9,
             "algorithmic_output_bytes_per_launch": 20 * W * H * F,
             "hbm_peak_gbs": peaks.get("hbm_gbs")}
+    # the sampler's own ceiling (SURVEY 8(d) "Denominators"): the march's light-sample loop alone
+    # on a fully occupied, L1-resident 16^3 grid of the same layout (nsl_bench_l1_gather), measured
+    # here after the timed region; executed gathers and tested samples (occupancy tests, gathered
+    # or not) of the march per second against it
+    try:
+        roof["sampler_ceiling"] = sampler_ceiling(layout, counts, march_s)
+    except Exception as e:                      # reported, never fatal for the bench line
+        roof["sampler_ceiling"] = {"error": str(e)[:200]}
 
     line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

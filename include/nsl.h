@@ -319,6 +319,16 @@ nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* 
 nsl_status nsl_guide_lights(const nsl_camera* cam, const float axis[3], const float rgb[3], nsl_light out[3],
                             nsl_stream stream);
 
+/* Sampler microbenchmark (SURVEY §8(d) "Denominators"): the march's own light-sample loop
+ * (sampler.cuh light_sum: positions, occupancy test, one gather, trilinear) run by every
+ * thread of waves x (SMs x resident CTAs) CTAs of 128 threads over 16-sample lines inside
+ * [2, 15)^3 of `vol` (>= 16^3; meant for a small, fully occupied, L1-resident grid), reps
+ * times; warps on the march's 8 x 4 footprint at a 0.25-voxel pixel pitch.  sink: device,
+ * >= threads floats (written, keeps the work live).  *samples (host) = samples the launch
+ * takes; time it with events on `stream`.  Asynchronous. */
+nsl_status nsl_bench_l1_gather(const nsl_volume* vol, int32_t waves, int32_t reps, float* sink, size_t sink_floats,
+                               uint64_t* samples, nsl_stream stream);
+
 /* ------------------------------------------------------------------ debug / verification
  * Frame constants of DESIGN.md C3/C3b/C10 as the device computes them
  * (fp64 evaluation rounded once to fp32), for bitwise comparison with the

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.environ.get("NSL_LIB") or os.path.join(_HERE, "lib", "libnsl.so")   # NSL_LIB: build variants
 CSRC = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "volume.cu", "setup.cu", "march.cu", "bake.cu",
-                                                  "runtime.cu", "tv.cu")]
+                                                  "runtime.cu", "tv.cu", "microbench.cu")]
 HEADERS = [os.path.join(_HERE, "csrc", "nsl_internal.cuh"), os.path.join(_HERE, "csrc", "sampler.cuh"),
            os.path.join(_ROOT, "include", "nsl.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -104,7 +104,7 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
            "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
-           "nsl_guiding_map_animated"]
+           "nsl_guiding_map_animated", "nsl_bench_l1_gather"]
 
 
 class BakeS(ctypes.Structure):
@@ -148,6 +148,7 @@ def lib():
     L.nsl_guiding_map_animated.argtypes = [P(GridDesc), P(vp), i32, P(vp), ctypes.c_size_t, P(CameraS), P(LightS),
                                            i32, i32, P(MediumS), P(MarchS), P(u32), i32, i32, vp, vp,
                                            P(ctypes.c_uint64), vp]
+    L.nsl_bench_l1_gather.argtypes = [vp, i32, i32, vp, ctypes.c_size_t, P(ctypes.c_uint64), vp]
     L.nsl_debug_frame_constants.argtypes = [P(GridDesc), P(CameraS), P(LightS), i32, i32, P(MediumS),
                                             P(MarchS), P(FrameConstantsS), vp]
     L.nsl_debug_jitter.argtypes = [P(MarchS), u32, i32, vp, vp, vp]
@@ -493,6 +494,14 @@ def guiding_map_animated(grid, densities, layout, storages, cams, lights, light_
     """One-shot form of Animated (marshals the host arguments on every call)."""
     return Animated(grid, densities, layout, storages, cams, lights, light_mode, medium, march, frame_ids,
                     chunk)(out_rgbt, out_depth, check=check, stream=stream)
+
+
+def bench_l1_gather(vol: Volume, sink, waves: int = 4, reps: int = 64, stream=None) -> int:
+    """Enqueue the sampler microbenchmark on `vol` (nsl_bench_l1_gather); returns the samples it takes."""
+    n = ctypes.c_uint64()
+    _check(lib().nsl_bench_l1_gather(vol.handle, waves, reps, sink.data_ptr(), sink.numel(), ctypes.byref(n),
+                                     _stream_handle(stream)), "nsl_bench_l1_gather")
+    return n.value
 
 
 def debug_frame_constants(grid, cam, lights, light_mode, medium, march, stream=None) -> dict:

@@ -1053,6 +1053,39 @@ nsl_status nsl_guide_lights(const nsl_camera* cam, const float axis[3], const fl
     return NSL_OK;
 }
 
+nsl_status nsl_bench_l1_gather(const nsl_volume* vol, int32_t waves, int32_t reps, float* sink, size_t sink_floats,
+                               uint64_t* samples, nsl_stream stream) {
+    g_err.clear();
+    if (!vol || !sink || !samples) return fail(NSL_ERR_INVALID_ARG, "NULL volume/sink/samples");
+    if (waves < 1 || reps < 1) return fail(NSL_ERR_INVALID_ARG, "waves and reps must be >= 1");
+    const nsl_grid_desc& g = vol->g;
+    if (g.nx < 16 || g.ny < 16 || g.nz < 16) return fail(NSL_ERR_INVALID_ARG, "the volume must be at least 16^3");
+    int dev = 0, sms = 0;
+    NSL_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    NSL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    const int per_sm = l1_gather_max_blocks_per_sm(vol->layout);
+    const size_t blocks = (size_t)sms * (per_sm > 0 ? per_sm : 1) * waves;
+    const size_t threads = blocks * l1_gather_threads();
+    if (sink_floats < threads) return fail(NSL_ERR_INVALID_ARG, "sink needs %zu floats", threads);
+    FrameParams p;
+    memset(&p, 0, sizeof p);
+    p.data = vol->data;
+    p.layout = vol->layout;
+    layout_strides(vol->layout, g.nx, g.ny, p.sy, p.sz);
+    p.supp[0] = (float)(g.nx + 1);
+    p.supp[1] = (float)(g.ny + 1);
+    p.supp[2] = (float)(g.nz + 1);
+    p.occ = vol->occ;
+    p.occ_shift = vol->og.shift;
+    p.occ_nbx = vol->og.nbx;
+    p.occ_nby = vol->og.nby;
+    p.slab_off = vol->og.words;
+    NSL_CUDA(launch_l1_gather(p, (int)blocks, reps, sink, reinterpret_cast<cudaStream_t>(stream)),
+             "l1_gather_kernel launch");
+    *samples = (uint64_t)threads * reps * l1_gather_line();
+    return NSL_OK;
+}
+
 nsl_status nsl_debug_jitter(const nsl_march* m, uint32_t frame_id, int32_t n, uint32_t* out_hash, float* out_delta,
                             nsl_stream stream) {
     g_err.clear();

@@ -77,6 +77,20 @@ struct FrameParams {
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 
 // Parameters common to every frame of a call (kernel argument).
+// element strides (y, z) of a volume layout, in cells (bricks for BRICK_OCT_F32)
+__host__ __device__ inline void layout_strides(int layout, int nx, int ny, int32_t& sy, int32_t& sz) {
+    if (layout == NSL_LAYOUT_LINEAR_F32) {            // apron of 1 on each side
+        sy = nx + 2;
+        sz = (nx + 2) * (ny + 2);
+    } else if (layout == NSL_LAYOUT_BRICK_OCT_F32) {  // strides in bricks of 4^3 cells
+        sy = (nx + 4) / 4;
+        sz = ((nx + 4) / 4) * ((ny + 4) / 4);
+    } else {
+        sy = nx + 1;
+        sz = (nx + 1) * (ny + 1);
+    }
+}
+
 struct MarchConst {
     float h, hl, tau_d, t_min;
     float kappa, alpha, g;
@@ -190,6 +204,11 @@ constexpr int kBrickOctF32 = NSL_LAYOUT_BRICK_OCT_F32;
 // layout + occupancy + AABB + invalid-voxel count from the raw grid (two launches, no memsets)
 cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storage, uint32_t* scratch,
                                 unsigned long long* invalid, cudaStream_t s);
+// sampler microbenchmark (microbench.cu): volume fields of p only
+cudaError_t launch_l1_gather(const FrameParams& p, int blocks, int reps, float* sink, cudaStream_t s);
+int l1_gather_threads();
+int l1_gather_line();
+int l1_gather_max_blocks_per_sm(int layout);
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s);
 // mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path.

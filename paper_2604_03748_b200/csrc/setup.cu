@@ -61,16 +61,7 @@ __global__ void __launch_bounds__(32 * kSetupWarps) frame_setup_kernel(const Fra
         p.nx = nx;
         p.ny = ny;
         p.nz = nz;
-        if (p.layout == kLinearF32) {
-            p.sy = nx + 2;
-            p.sz = (nx + 2) * (ny + 2);
-        } else if (p.layout == kBrickOctF32) {     // strides in bricks of 4^3 cells
-            p.sy = (nx + 4) / 4;
-            p.sz = ((nx + 4) / 4) * ((ny + 4) / 4);
-        } else {
-            p.sy = nx + 1;
-            p.sz = (nx + 1) * (ny + 1);
-        }
+        layout_strides(p.layout, nx, ny, p.sy, p.sz);
         for (int q = 0; q < 3; ++q) p.supp[q] = supp[q];
         p.projection = cam.projection;
         p.W = cam.width;
