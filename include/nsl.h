@@ -296,9 +296,10 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
  * device memory of storage_bytes >= nsl_volume_bytes(g, layout), aligned as for
  * nsl_volume_upload; one buffer per frame, not shared between frames) and marched with
  * cams[f] and lights[f*n_lights ...].  densities and storage are HOST arrays of F device
- * pointers.  Frames run in chunks of `chunk` frames (0 -> 3): the layouts of chunk c+1 build
- * on an internal side stream while chunk c marches on `stream` (the HBM-bound build hides
- * under the latency-bound march).  Results are bitwise those of nsl_volume_upload of every
+ * pointers.  Frames run in chunks of `chunk` frames (0 -> 6): the layouts of chunk c+1 build
+ * on an internal side stream while chunk c marches on `stream` (results of early chunks are
+ * ready early; how much of the HBM-bound build hides under the march depends on the march's
+ * length).  Results are bitwise those of nsl_volume_upload of every
  * frame followed by nsl_guiding_map_batch; outputs as nsl_guiding_map_batch (device, F*H*W*4
  * and F*H*W floats).  Asynchronous: all work is ordered on `stream` on return, unless
  * n_invalid (host pointer) is non-NULL, in which case the call synchronises `stream` and

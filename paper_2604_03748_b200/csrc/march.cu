@@ -95,11 +95,14 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? NSL_MINB_G3 : NL == 1 ? N
                                                          const uint32_t* __restrict__ tile_order,
                                                          const uint8_t* __restrict__ cull, int tiles_x, TvArgs tv) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
-    // grid (frame, tile rank): frames fastest in launch order; tiles centre-out
-    // (tile_order) so the heavy tiles of every frame start first and the tail of
-    // the launch is made of cheap border tiles.
-    const int f = (int)blockIdx.x;
-    const uint32_t tile = __ldg(tile_order + blockIdx.y);
+    // grid (frame, tile rank): frames fastest in launch order, so the heavy tiles of every frame
+    // start first and the tail of the launch is made of cheap border tiles; or (frame_major, for
+    // volumes beyond L2 and per-frame volumes) (tile rank, frame): the CTAs in flight then cover
+    // one frame and share its volume's cache lines.  Tiles centre-out (tile_order) either way.
+    const bool fmaj = mc.frame_major != 0;
+    const int f = (int)(fmaj ? blockIdx.y : blockIdx.x);
+    const int ntiles = (int)(fmaj ? gridDim.x : gridDim.y);
+    const uint32_t tile = __ldg(tile_order + (fmaj ? blockIdx.x : blockIdx.y));
     const int tx = (int)(tile & 0xffffu), ty = (int)(tile >> 16);
     pdl_wait();                        // launched with PDL after frame_setup / tile_cull: their outputs
     const FrameParams& sp = fps[f];
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? NSL_MINB_G3 : NL == 1 ? N
     const bool valid = px < W && py < H;
     const size_t o = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
 
-    if (PROJ == 0 && (__ldg(cull + (size_t)f * gridDim.y + ty * tiles_x + tx) & (DEBUG || COUNT ? 2 : 1))) {
+    if (PROJ == 0 && (__ldg(cull + (size_t)f * ntiles + ty * tiles_x + tx) & (DEBUG || COUNT ? 2 : 1))) {
         if (valid) {                   // the empty map: L = 0, T = 1, D = 0, counters 0
             out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
             out_depth[o] = 0.0f;
@@ -386,7 +389,7 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
                                    tiles, cull);
         if (e != cudaSuccess) return e;
     }
-    const dim3 grid((unsigned)F, (unsigned)tiles);
+    const dim3 grid = mc.frame_major ? dim3((unsigned)tiles, (unsigned)F) : dim3((unsigned)F, (unsigned)tiles);
     if (tv) {
         if constexpr (MODE == kFast) {   // (the guide-set kernel with TV lookups spills: C2 +11 %)
             if (NSL_TV_NL && mc.n_lights == 1)

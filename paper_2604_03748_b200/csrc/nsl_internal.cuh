@@ -100,6 +100,7 @@ struct MarchConst {
     int32_t front_identity;
     float axis[3];
     int32_t light_model;       // NSL_LIGHT_MARCH | NSL_LIGHT_TV
+    int32_t frame_major;       // march grid order (march.cu): 0 frames fastest, 1 tiles fastest
 };
 
 // NEXT-4 transmittance volume: per (frame, lattice slot) constants of the
