@@ -209,6 +209,19 @@ def test_parity_C5_subsampled_full_size(nsl):
 
 
 # ------------------------------------------------------------------ batch / determinism / sharding / host API
+@pytest.mark.parametrize("cfg,frames", [("C2", [0, 7, 30]), ("C4", [0, 1, 120])])
+def test_march_grid_order_is_bitwise_invariant(nsl, monkeypatch, cfg, frames):
+    """Frames-fastest and tiles-fastest march grids (DESIGN.md §6 grid order) give identical maps,
+    debug counters included."""
+    w = I.make_workload(cfg, frames=frames)
+    outs = []
+    for fm in ("0", "1"):
+        monkeypatch.setenv("NSL_FRAME_MAJOR", fm)
+        outs.append(run(nsl, w, layout=3, debug=cfg == "C2"))
+    for x, y in zip(*outs):
+        assert (x is None and y is None) or np.array_equal(x, y)
+
+
 def test_batch_equals_single_frames_and_is_deterministic(nsl):
     import torch
     w = I.make_workload("C2", frames=[0, 1, 2, 3])
