@@ -217,18 +217,25 @@ struct Workspace {
     uint8_t* cull = nullptr;           // march_cull_bytes workspace (march calls only)
 };
 
-// March tile order: centre-out by the distance of the tile centre from the image
-// centre (the smoke of a billboard is centred, so heavy tiles start first and the
-// end of the launch is made of cheap border tiles).  Packed (tx | ty << 16).
+// March tile order: whole tile rows together, rows centre-out from the image centre and
+// tiles centre-out inside a row (the smoke of a billboard is centred, so heavy tiles start
+// first and the end of the launch is made of cheap border tiles).  Rows together: the
+// horizontal guide-pair light lines of a tile row stay in one z-slab of the volume, so the
+// CTAs in flight share that slab in L2 (C5, 4.3 GB volume: march -19 %; C3 -3.7 %; C2 -0.8 %
+// against plain centre-out by distance).  Packed (tx | ty << 16).
 std::vector<uint32_t> tile_order(int W, int H) {
     const int tw = march_tile_w(), th = march_tile_h();
     const int nx = (W + tw - 1) / tw, ny = (H + th - 1) / th;
     std::vector<std::pair<double, uint32_t>> v;
     v.reserve((size_t)nx * ny);
+    const char* mode = getenv("NSL_TILE_ORDER");      // "centre": plain centre-out (A/B)
+    const bool rows = !(mode && mode[0] == 'c');
     for (int ty = 0; ty < ny; ++ty)
         for (int tx = 0; tx < nx; ++tx) {
             const double dx = (tx + 0.5) * tw - 0.5 * W, dy = (ty + 0.5) * th - 0.5 * H;
-            v.push_back({dx * dx + dy * dy, (uint32_t)tx | ((uint32_t)ty << 16)});
+            // rows: whole tile rows together (rows centre-out, tiles centre-out inside a row)
+            const double key = rows ? std::fabs(dy) * 1e6 + std::fabs(dx) : dx * dx + dy * dy;
+            v.push_back({key, (uint32_t)tx | ((uint32_t)ty << 16)});
         }
     std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
     std::vector<uint32_t> out(v.size());
