@@ -13,6 +13,10 @@
 #include <stddef.h>
 #include <string.h>
 
+#ifndef M_PI /* strict ISO C modes do not define it (same value as glibc's) */
+#define M_PI 3.14159265358979323846
+#endif
+
 /* ---------------------------------------------------------------- C10 HG */
 /* Henyey-Greenstein phase ("Henyey-Greenstein phase function
  * with g=0"; formula SPEC S:59): (1-g^2) / (4 pi (1+g^2-2 g c)^(3/2)). */
