@@ -213,63 +213,34 @@ struct Workspace {
     FrameIn* in = nullptr;
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
-    uint32_t* order = nullptr;
     uint8_t* cull = nullptr;           // march_cull_bytes workspace (march calls only)
 };
 
-// March tile order: whole tile rows together, rows centre-out from the image centre and
-// tiles centre-out inside a row (the smoke of a billboard is centred, so heavy tiles start
-// first and the end of the launch is made of cheap border tiles).  Rows together: the
-// horizontal guide-pair light lines of a tile row stay in one z-slab of the volume, so the
-// CTAs in flight share that slab in L2 (C5, 4.3 GB volume: march -19 %; C3 -3.7 %; C2 -0.8 %
-// against plain centre-out by distance).  Packed (tx | ty << 16).
-std::vector<uint32_t> tile_order(int W, int H) {
-    const int tw = march_tile_w(), th = march_tile_h();
-    const int nx = (W + tw - 1) / tw, ny = (H + th - 1) / th;
-    std::vector<std::pair<double, uint32_t>> v;
-    v.reserve((size_t)nx * ny);
-    const char* mode = getenv("NSL_TILE_ORDER");      // "centre": plain centre-out (A/B)
-    const bool rows = !(mode && mode[0] == 'c');
-    for (int ty = 0; ty < ny; ++ty)
-        for (int tx = 0; tx < nx; ++tx) {
-            const double dx = (tx + 0.5) * tw - 0.5 * W, dy = (ty + 0.5) * th - 0.5 * H;
-            // rows: whole tile rows together (rows centre-out, tiles centre-out inside a row)
-            const double key = rows ? std::fabs(dy) * 1e6 + std::fabs(dx) : dx * dx + dy * dy;
-            v.push_back({key, (uint32_t)tx | ((uint32_t)ty << 16)});
-        }
-    std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    std::vector<uint32_t> out(v.size());
-    for (size_t i = 0; i < v.size(); ++i) out[i] = v[i].second;
-    return out;
-}
-
-// The frame tables (FrameIn, lights, tile order) uploaded into a fresh stream-ordered workspace.
-nsl_status upload_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
-                         const std::vector<uint32_t>& order, cudaStream_t s, Workspace& ws) {
+// The frame tables (FrameIn, lights) uploaded into a fresh stream-ordered workspace, plus the
+// march's tile cull flags when `march`.
+nsl_status upload_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights, bool march,
+                         cudaStream_t s, Workspace& ws) {
     const int F = (int)frames.size();
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
-    const size_t b_o = align_up(sizeof(uint32_t) * order.size(), 256);
     const size_t b_p = align_up(sizeof(FrameParams) * F, 256);
-    const size_t b_c = order.empty() ? 0 : march_cull_bytes(F, frames[0].cam.width, frames[0].cam.height);
+    const size_t b_c = march ? march_cull_bytes(F, frames[0].cam.width, frames[0].cam.height) : 0;
     retain_pool_once();
-    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_o + b_p + b_c, s), "cudaMallocAsync(frame tables)");
+    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_p + b_c, s), "cudaMallocAsync(frame tables)");
     ws.in = reinterpret_cast<FrameIn*>(ws.base);
     ws.lights = reinterpret_cast<nsl_light*>(static_cast<char*>(ws.base) + b_in);
-    ws.order = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.base) + b_in + b_l);
-    ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l + b_o);
-    ws.cull = b_c ? reinterpret_cast<uint8_t*>(ws.base) + b_in + b_l + b_o + b_p : nullptr;
-    std::vector<char> host(b_in + b_l + b_o);
+    ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l);
+    ws.cull = b_c ? reinterpret_cast<uint8_t*>(ws.base) + b_in + b_l + b_p : nullptr;
+    std::vector<char> host(b_in + b_l);
     memcpy(host.data(), frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
-    if (!order.empty()) memcpy(host.data() + b_in + b_l, order.data(), sizeof(uint32_t) * order.size());
     NSL_CUDA(cudaMemcpyAsync(ws.base, host.data(), host.size(), cudaMemcpyHostToDevice, s), "frame table upload");
     return NSL_OK;
 }
 
 nsl_status build_frames(const std::vector<FrameIn>& frames, const nsl_light* lights, int n_lights,
-                        const MarchConst& mc, const std::vector<uint32_t>& order, cudaStream_t s, Workspace& ws) {
-    if (nsl_status st = upload_frames(frames, lights, n_lights, order, s, ws)) return st;
+                        const MarchConst& mc, bool march, cudaStream_t s, Workspace& ws) {
+    if (nsl_status st = upload_frames(frames, lights, n_lights, march, s, ws)) return st;
     NSL_CUDA(launch_frame_setup(ws.in, ws.lights, (int)frames.size(), mc, ws.params, s), "frame_setup_kernel launch");
     return NSL_OK;
 }
@@ -434,12 +405,12 @@ static void tv_geometry(const nsl_volume* const* vols, int n_vols, Prepared& P) 
 // The march of a prepared batch: one launch, or (light_model TV) the lattice setup, then per
 // frame group the sweep and the march of that group.  tvp/tvbuf: P.tv_params_bytes() and
 // P.tv_buf_bytes() of device workspace (unused otherwise).
-static cudaError_t run_march(const Prepared& P, const FrameParams* params, const uint32_t* order, uint8_t* cull,
+static cudaError_t run_march(const Prepared& P, const FrameParams* params, uint8_t* cull,
                              TvParams* tvp, float2* tvbuf, float* out_rgbt, float* out_depth, uint32_t* out_debug,
                              unsigned long long* counters, cudaStream_t s) {
     float4* rgbt = reinterpret_cast<float4*>(out_rgbt);
     if (!P.tv_slots)
-        return launch_march(params, P.mc, P.F, P.W, P.H, P.proj, P.layout, rgbt, out_depth, out_debug, counters, order,
+        return launch_march(params, P.mc, P.F, P.W, P.H, P.proj, P.layout, rgbt, out_depth, out_debug, counters,
                             cull, nullptr, s);
     cudaError_t e = launch_tv_setup(params, P.F, P.tv_slots, P.mc, tvp, s);
     const size_t npf = (size_t)P.W * P.H;
@@ -452,7 +423,7 @@ static cudaError_t run_march(const Prepared& P, const FrameParams* params, const
         const TvArgs ta{gp, tvbuf, P.tv_slots, P.tv_Astr, P.tv_Kstr, (int64_t)P.tv_slot_elems()};
         e = launch_march(params + g0, P.mc, n, P.W, P.H, P.proj, P.layout, rgbt + (size_t)g0 * npf,
                          out_depth + (size_t)g0 * npf, out_debug ? out_debug + (size_t)g0 * npf * 6 : nullptr, counters,
-                         order, cull ? cull + (size_t)g0 * tiles : nullptr, &ta, s);
+                         cull ? cull + (size_t)g0 * tiles : nullptr, &ta, s);
     }
     return e;
 }
@@ -516,12 +487,12 @@ static nsl_status batch_impl(const nsl_volume* const* vols, int32_t n_vols, cons
         return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
-    if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, tile_order(P.W, P.H), s, ws)) return st;
+    if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, true, s, ws)) return st;
     void* tvws = nullptr;
     cudaError_t e = cudaSuccess;
     if (P.tv_slots) e = cudaMallocAsync(&tvws, align_up(P.tv_params_bytes(), 256) + P.tv_buf_bytes(), s);
     if (e == cudaSuccess)
-        e = run_march(P, ws.params, ws.order, ws.cull, static_cast<TvParams*>(tvws),
+        e = run_march(P, ws.params, ws.cull, static_cast<TvParams*>(tvws),
                       reinterpret_cast<float2*>(static_cast<char*>(tvws) + align_up(P.tv_params_bytes(), 256)),
                       out_rgbt, out_depth, out_debug, counters, s);
     if (tvws) cudaFreeAsync(tvws, s);
@@ -710,7 +681,7 @@ nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* 
     const size_t tiles = march_cull_bytes(1, P.W, P.H);
     Prepared Pc = P;                             // a chunk's view of P (F = frames of the chunk)
     Pc.tv_group = P.tv_group < per ? P.tv_group : per;
-    if (st == NSL_OK) st = upload_frames(P.frames, lights, n_lights, tile_order(P.W, P.H), s, ws);
+    if (st == NSL_OK) st = upload_frames(P.frames, lights, n_lights, true, s, ws);
     if (st == NSL_OK && P.tv_slots) {
         Pc.F = per;
         e = cudaMallocAsync(&tvws, align_up(Pc.tv_params_bytes(), 256) + Pc.tv_buf_bytes(), s);
@@ -730,7 +701,7 @@ nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* 
         Pc.F = n;
         e = launch_frame_setup(ws.in + f0, ws.lights + (size_t)f0 * n_lights, n, P.mc, ws.params + f0, s);
         if (e == cudaSuccess)
-            e = run_march(Pc, ws.params + f0, ws.order, ws.cull + (size_t)f0 * tiles, static_cast<TvParams*>(tvws),
+            e = run_march(Pc, ws.params + f0, ws.cull + (size_t)f0 * tiles, static_cast<TvParams*>(tvws),
                           reinterpret_cast<float2*>(static_cast<char*>(tvws) + align_up(Pc.tv_params_bytes(), 256)),
                           out_rgbt + (size_t)f0 * npf * 4, out_depth + (size_t)f0 * npf, nullptr, nullptr, s);
         if (e != cudaSuccess) st = cuda_fail(e, "march launch");
@@ -765,7 +736,6 @@ struct nsl_plan {
     FrameIn* in = nullptr;
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
-    uint32_t* order = nullptr;
     uint8_t* cull = nullptr;
     TvParams* tvp = nullptr;     // NEXT-4 workspace (light_model TV)
     float2* tvbuf = nullptr;
@@ -782,29 +752,25 @@ nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const 
         delete p;
         return st;
     }
-    const std::vector<uint32_t> order = tile_order(p->P.W, p->P.H);
     const size_t b_in = align_up(sizeof(FrameIn) * F, 256);
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
-    const size_t b_o = align_up(sizeof(uint32_t) * order.size(), 256);
     const size_t b_p = align_up(sizeof(FrameParams) * F, 256);
     const size_t b_c = align_up(march_cull_bytes(F, p->P.W, p->P.H), 256);
     const size_t b_tp = align_up(p->P.tv_params_bytes(), 256);
-    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_o + b_p + b_c + b_tp + p->P.tv_buf_bytes());
+    cudaError_t e = cudaMalloc(&p->dev, b_in + b_l + b_p + b_c + b_tp + p->P.tv_buf_bytes());
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaMalloc(plan)");
     }
     p->in = reinterpret_cast<FrameIn*>(p->dev);
     p->lights = reinterpret_cast<nsl_light*>(static_cast<char*>(p->dev) + b_in);
-    p->order = reinterpret_cast<uint32_t*>(static_cast<char*>(p->dev) + b_in + b_l);
-    p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_o);
-    p->cull = reinterpret_cast<uint8_t*>(p->dev) + b_in + b_l + b_o + b_p;
-    p->tvp = reinterpret_cast<TvParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_o + b_p + b_c);
-    p->tvbuf = reinterpret_cast<float2*>(static_cast<char*>(p->dev) + b_in + b_l + b_o + b_p + b_c + b_tp);
-    std::vector<char> host(b_in + b_l + b_o);
+    p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l);
+    p->cull = reinterpret_cast<uint8_t*>(p->dev) + b_in + b_l + b_p;
+    p->tvp = reinterpret_cast<TvParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_p + b_c);
+    p->tvbuf = reinterpret_cast<float2*>(static_cast<char*>(p->dev) + b_in + b_l + b_p + b_c + b_tp);
+    std::vector<char> host(b_in + b_l);
     memcpy(host.data(), p->P.frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
-    memcpy(host.data() + b_in + b_l, order.data(), sizeof(uint32_t) * order.size());
     e = cudaMemcpyAsync(p->dev, host.data(), host.size(), cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) {
         cudaFree(p->dev);
@@ -826,7 +792,7 @@ nsl_status nsl_plan_execute(const nsl_plan* p, float* out_rgbt, float* out_depth
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (counters) NSL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint64_t), s), "cudaMemsetAsync(counters)");
     NSL_CUDA(launch_frame_setup(p->in, p->lights, p->P.F, p->P.mc, p->params, s), "frame_setup_kernel launch");
-    NSL_CUDA(run_march(p->P, p->params, p->order, p->cull, p->tvp, p->tvbuf, out_rgbt, out_depth, out_debug,
+    NSL_CUDA(run_march(p->P, p->params, p->cull, p->tvp, p->tvbuf, out_rgbt, out_depth, out_debug,
                        reinterpret_cast<unsigned long long*>(counters), s),
              "march_kernel launch");
     return NSL_OK;
@@ -874,7 +840,7 @@ nsl_status nsl_sixway_bake(const nsl_volume* const* vols, int32_t n_vols, const 
         return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
-    if (nsl_status st = build_frames(P.frames, dummy.data(), 1, P.mc, std::vector<uint32_t>(), s, ws)) return st;
+    if (nsl_status st = build_frames(P.frames, dummy.data(), 1, P.mc, false, s, ws)) return st;
     BakeFrame* bf = nullptr;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bf), sizeof(BakeFrame) * F, s);
     if (e == cudaSuccess) e = launch_bake_setup(ws.in, ws.params, F, b->light_step, med->hg_g, bf, s);
@@ -986,7 +952,7 @@ nsl_status nsl_debug_bake_lights(const nsl_grid_desc* g, const nsl_camera* cam, 
     const MarchConst mc = make_const(1, NSL_LIGHTS_EXPLICIT, &med, &m);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
-    if (nsl_status st = build_frames(frames, &dummy, 1, mc, std::vector<uint32_t>(), s, ws)) return st;
+    if (nsl_status st = build_frames(frames, &dummy, 1, mc, false, s, ws)) return st;
     BakeFrame* bf = nullptr;
     BakeFrame h;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bf), sizeof(BakeFrame), s);
@@ -1022,7 +988,7 @@ nsl_status nsl_debug_frame_constants(const nsl_grid_desc* g, const nsl_camera* c
     const MarchConst mc = make_const(n_lights, light_mode, med, m);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Workspace ws;
-    if (nsl_status st = build_frames(frames, lights, n_lights, mc, std::vector<uint32_t>(), s, ws)) return st;
+    if (nsl_status st = build_frames(frames, lights, n_lights, mc, false, s, ws)) return st;
     FrameParams p;
     cudaError_t e = cudaMemcpyAsync(&p, ws.params, sizeof p, cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(ws.base, s);

@@ -2,8 +2,9 @@
 // L394-407; C3-C12) for sm_100a.
 //
 // One thread per pixel; a warp marches a coherent 8x4 pixel tile, a CTA a
-// 16x8 tile (4 warps).  Grid (frame, tile rank): frames fastest, tiles in
-// centre-out order.  Sample positions use only explicitly rounded fp32
+// 16x8 tile (4 warps).  Grid (frame, tile column, tile row): frames fastest,
+// whole tile rows together, rows and columns centre-out (or tiles first when
+// the frames view different volumes).  Sample positions use only explicitly rounded fp32
 // operations (__fmaf_rn, __fmul_rn) so that every index decision is
 // bit-identical to the oracle (C14); values are fp32 with FMA
 // lerps.  The step range is clipped exactly (C5) and each light march's
@@ -87,23 +88,32 @@ __device__ __forceinline__ float2 tv_lookup(const TvParams& t, const float2* __r
 // NL: the light set fixed at compile time, so the paths it cannot take are compiled out and
 // the kernel carries less state: 3 = the guide set (front + the exactly opposite top/bottom
 // pair, pair12 by construction), 1 = one light (march or C9), 0 = any set (runtime).
+// k-th index of [0, n) in centre-out order (ties: the lower index first): n odd m, m-1, m+1,
+// m-2, ...; n even m-1, m, m-2, m+1, ... with m = n / 2.  A bijection of [0, n).
+__device__ __forceinline__ int centre_out(int k, int n) {
+    const int m = n >> 1, h = k >> 1;
+    if (n & 1) return (k & 1) ? m - 1 - h : m + h;
+    return (k & 1) ? m + h : m - 1 - h;
+}
+
 template <int LAYOUT, int PROJ, int MODE, bool TV, int NL>
 __global__ void __launch_bounds__(kThreads, (NL == 3 ? NSL_MINB_G3 : NL == 1 ? NSL_MINB_L1 : NSL_MINB) * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H,
-                                                         const uint32_t* __restrict__ tile_order,
                                                          const uint8_t* __restrict__ cull, int tiles_x, TvArgs tv) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
-    // grid (frame, tile rank): frames fastest in launch order, so the heavy tiles of every frame
-    // start first and the tail of the launch is made of cheap border tiles; or (frame_major, for
-    // volumes beyond L2 and per-frame volumes) (tile rank, frame): the CTAs in flight then cover
-    // one frame and share its volume's cache lines.  Tiles centre-out (tile_order) either way.
+    // 3-D grid (frame, tile column rank, tile row rank): frames fastest, then the tiles of one
+    // tile row, then rows -- rows and columns centre-out (centre_out), so whole tile rows run
+    // together (the horizontal light lines of a row stay in one z-slab of the volume) and the
+    // heavy centre tiles start first.  frame_major (frames of different volumes): (column, row,
+    // frame), the CTAs in flight then cover one frame and share its volume.  No order table:
+    // the tile follows from the block index without a dependent load.
     const bool fmaj = mc.frame_major != 0;
-    const int f = (int)(fmaj ? blockIdx.y : blockIdx.x);
-    const int ntiles = (int)(fmaj ? gridDim.x : gridDim.y);
-    const uint32_t tile = __ldg(tile_order + (fmaj ? blockIdx.x : blockIdx.y));
-    const int tx = (int)(tile & 0xffffu), ty = (int)(tile >> 16);
+    const int f = (int)(fmaj ? blockIdx.z : blockIdx.x);
+    const int tiles_y = (int)(fmaj ? gridDim.y : gridDim.z);
+    const int tx = centre_out((int)(fmaj ? blockIdx.x : blockIdx.y), tiles_x);
+    const int ty = centre_out((int)(fmaj ? blockIdx.y : blockIdx.z), tiles_y);
     pdl_wait();                        // launched with PDL after frame_setup / tile_cull: their outputs
     const FrameParams& sp = fps[f];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -112,18 +122,8 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? NSL_MINB_G3 : NL == 1 ? N
     const bool valid = px < W && py < H;
     const size_t o = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
 
-    if (PROJ == 0 && (__ldg(cull + (size_t)f * ntiles + ty * tiles_x + tx) & (DEBUG || COUNT ? 2 : 1))) {
-        if (valid) {                   // the empty map: L = 0, T = 1, D = 0, counters 0
-            out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
-            out_depth[o] = 0.0f;
-            if (DEBUG) {
-                uint32_t* dbg = out_debug + o * 6;
-                dbg[0] = dbg[1] = dbg[2] = dbg[3] = dbg[4] = dbg[5] = 0u;
-            }
-        }
-        return;                        // uniform over the CTA
-    }
-
+    // the cull flag and the volume fields are independent loads: issue them together
+    const uint8_t cflag = PROJ == 0 ? __ldg(cull + (size_t)f * (tiles_x * tiles_y) + ty * tiles_x + tx) : 0;
     Vol v;
     v.data = sp.data;
     v.sy = sp.sy;
@@ -136,6 +136,17 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? NSL_MINB_G3 : NL == 1 ? N
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
     v.mask_words = sp.slab_off;
+    if (PROJ == 0 && (cflag & (DEBUG || COUNT ? 2 : 1))) {
+        if (valid) {                   // the empty map: L = 0, T = 1, D = 0, counters 0
+            out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
+            out_depth[o] = 0.0f;
+            if (DEBUG) {
+                uint32_t* dbg = out_debug + o * 6;
+                dbg[0] = dbg[1] = dbg[2] = dbg[3] = dbg[4] = dbg[5] = 0u;
+            }
+        }
+        return;                        // uniform over the CTA
+    }
     if (!COUNT && !valid) return;
 
     uint32_t c_prim = 0, c_light = 0, c_gath = 0, c_occ = 0, c_tp = 0, c_tl = 0;
@@ -379,7 +390,7 @@ __global__ void jitter_debug_kernel(MarchConst mc, uint32_t frame, int n, uint32
 
 template <int LAYOUT, int PROJ, int MODE>
 cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
-                       uint32_t* debug, unsigned long long* counters, const uint32_t* tile_order, uint8_t* cull,
+                       uint32_t* debug, unsigned long long* counters, uint8_t* cull,
                        const TvArgs* tv, cudaStream_t s) {
     const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH, tiles = tiles_x * tiles_y;
     if (tiles > 65535) return cudaErrorInvalidConfiguration;
@@ -389,44 +400,45 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
                                    tiles, cull);
         if (e != cudaSuccess) return e;
     }
-    const dim3 grid = mc.frame_major ? dim3((unsigned)tiles, (unsigned)F) : dim3((unsigned)F, (unsigned)tiles);
+    const unsigned txn = (unsigned)tiles_x, tyn = (unsigned)tiles_y;
+    const dim3 grid = mc.frame_major ? dim3(txn, tyn, (unsigned)F) : dim3((unsigned)F, txn, tyn);
     if (tv) {
         if constexpr (MODE == kFast) {   // (the guide-set kernel with TV lookups spills: C2 +11 %)
             if (NSL_TV_NL && mc.n_lights == 1)
                 return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 1>, grid, dim3(kThreads), 0, s, fp, mc,
-                                  rgbt, depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, *tv);
+                                  rgbt, depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, *tv);
         }
         return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 0>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
-                          depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, *tv);
+                          depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, *tv);
     }
     if constexpr (MODE == kFast) {
         if (NSL_G3 && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
             return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 3>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
-                              depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
+                              depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, TvArgs{});
         if (NSL_L1 && mc.n_lights == 1)
             return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 1>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
-                              depth, debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
+                              depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, TvArgs{});
     }
     return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 0>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth,
-                      debug, counters, W, H, tile_order, (const uint8_t*)cull, tiles_x, TvArgs{});
+                      debug, counters, W, H, (const uint8_t*)cull, tiles_x, TvArgs{});
 }
 
 template <int LAYOUT, int PROJ>
 cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
-                      uint32_t* debug, unsigned long long* counters, const uint32_t* to, uint8_t* cull,
+                      uint32_t* debug, unsigned long long* counters, uint8_t* cull,
                       const TvArgs* tv, cudaStream_t s) {
-    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
+    if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s);
     if (counters)
-        return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
-    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
+        return launch_lpm<LAYOUT, PROJ, kCounted>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s);
+    return launch_lpm<LAYOUT, PROJ, kFast>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s);
 }
 
 template <int LAYOUT>
 cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, float4* rgbt,
-                     float* depth, uint32_t* debug, unsigned long long* counters, const uint32_t* to, uint8_t* cull,
+                     float* depth, uint32_t* debug, unsigned long long* counters, uint8_t* cull,
                      const TvArgs* tv, cudaStream_t s) {
-    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s)
-                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, rgbt, depth, debug, counters, to, cull, tv, s);
+    return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s)
+                     : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s);
 }
 
 }  // namespace
@@ -440,13 +452,13 @@ size_t march_cull_bytes(int F, int W, int H) {
 
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection, int layout,
                          float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
-                         const uint32_t* tile_order, uint8_t* cull, const TvArgs* tv, cudaStream_t s) {
+                         uint8_t* cull, const TvArgs* tv, cudaStream_t s) {
     switch (layout) {
-        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
-        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
-        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
-        case kOctF32: return launch_l<kOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
-        case kBrickOctF32: return launch_l<kBrickOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, tile_order, cull, tv, s);
+        case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
+        case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
+        case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
+        case kOctF32: return launch_l<kOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
+        case kBrickOctF32: return launch_l<kBrickOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -217,7 +217,7 @@ cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F
 // tv: NULL (light_model 0) or the group's transmittance-volume arguments.
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection,
                          int layout, float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
-                         const uint32_t* tile_order, uint8_t* cull, const TvArgs* tv, cudaStream_t s);
+                         uint8_t* cull, const TvArgs* tv, cudaStream_t s);
 size_t march_cull_bytes(int F, int W, int H);
 int march_tile_w();
 int march_tile_h();
