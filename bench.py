@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--gather", action="store_true",
                    help="N>1: after the timed loop, time the NCCL gather of all guiding maps to rank 0")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-sampler-ceiling", action="store_true",
+                   help="skip the sampler microbenchmark after the timed region (ncu launch lists)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     return p.parse_args()
 
@@ -363,7 +365,8 @@ def main():
     # here after the timed region; executed gathers and tested samples (occupancy tests, gathered
     # or not) of the march per second against it
     try:
-        roof["sampler_ceiling"] = sampler_ceiling(layout, counts, march_s)
+        if not args.no_sampler_ceiling:
+            roof["sampler_ceiling"] = sampler_ceiling(layout, counts, march_s)
     except Exception as e:                      # reported, never fatal for the bench line
         roof["sampler_ceiling"] = {"error": str(e)[:200]}
 

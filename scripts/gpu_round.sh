@@ -8,7 +8,7 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 300 python scripts/bench_relight.py > gpurun_out/bench_relight.json 2>&1; echo "relight rc=$?"
 timeout 300 python scripts/bench_bake.py > gpurun_out/bench_bake.json 2>&1; echo "bake rc=$?"
 timeout 600 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref.json 2>&1; echo "ref rc=$?"
-CMD="python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline --no-sampler-ceiling"
 timeout 300 $CMD > gpurun_out/launch_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/launch_ncu.log 2>&1; echo "launch-list rc=$?"
 timeout 300 python scripts/profile_march.py > gpurun_out/prof_plain.log 2>&1 && \

@@ -39,7 +39,7 @@ for r in rows[hi + 1:]:
     name = r[ki].split("(")[0].replace("void ", "")
     agg.setdefault(name, []).append(float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0))
 tot = sum(sum(v) for v in agg.values())
-out = [f"# ncu launch list of `python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline` (B200, {tag})",
+out = [f"# ncu launch list of `python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline --no-sampler-ceiling` (B200, {tag})",
        "# gpu__time_duration.sum with --clock-control none: cold-cache, serialised; compare SHARES, not absolutes.",
        "# march_kernel<layout, proj, 2, tv> is the one instrumented (counted) launch; at::FillFunctor<uchar> is the L2 flush.", ""]
 step = 0.0
