@@ -97,7 +97,7 @@ __device__ __forceinline__ int centre_out(int k, int n) {
 }
 
 template <int LAYOUT, int PROJ, int MODE, bool TV, int NL>
-__global__ void __launch_bounds__(kThreads, (NL == 3 ? NSL_MINB_G3 : NL == 1 ? NSL_MINB_L1 : NSL_MINB) * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
+__global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL_MINB_G3) : NL == 1 ? NSL_MINB_L1 : NSL_MINB) * 256 / kThreads) march_kernel(const FrameParams* __restrict__ fps, const MarchConst mc,
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H,
@@ -403,7 +403,10 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
     const unsigned txn = (unsigned)tiles_x, tyn = (unsigned)tiles_y;
     const dim3 grid = mc.frame_major ? dim3(txn, tyn, (unsigned)F) : dim3((unsigned)F, txn, tyn);
     if (tv) {
-        if constexpr (MODE == kFast) {   // (the guide-set kernel with TV lookups spills: C2 +11 %)
+        if constexpr (MODE == kFast) {
+            if (NSL_TV_G3 && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
+                return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 3>, grid, dim3(kThreads), 0, s, fp, mc,
+                                  rgbt, depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, *tv);
             if (NSL_TV_NL && mc.n_lights == 1)
                 return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 1>, grid, dim3(kThreads), 0, s, fp, mc,
                                   rgbt, depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, *tv);

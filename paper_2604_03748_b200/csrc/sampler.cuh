@@ -51,6 +51,12 @@ static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (3
 #ifndef NSL_TV_NL               // the single-light kernel for the TV light model too
 #define NSL_TV_NL 1
 #endif
+#ifndef NSL_TV_G3               // the guide-set kernel for the TV light model
+#define NSL_TV_G3 1
+#endif
+#ifndef NSL_MINB_G3TV
+#define NSL_MINB_G3TV 5 // its register cap (48)
+#endif
 #ifndef NSL_MINB_L1
 #define NSL_MINB_L1 6   // its register cap
 #endif
