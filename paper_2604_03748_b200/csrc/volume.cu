@@ -130,13 +130,27 @@ __device__ __forceinline__ void layout_oct_cta(const Raw& r, float* __restrict__
     const int e2 = pb * 256 + threadIdx.x;
     if (e2 >= plane) return;
     const int i = e2 % qx, j = e2 / qx;
+    // the x/y apron tests and row offsets are fixed per thread: padded corner a is real iff
+    // 1 <= a <= n; raw offset of padded (a, b, c) = ((c - 1) ny + b - 1) nx + a - 1
+    const bool x0 = i >= 1, x1 = i < r.nx, y0 = j >= 1, y1 = j < r.ny;
+    const bool c00 = x0 && y0, c10 = x1 && y0, c01 = x0 && y1, c11 = x1 && y1;
+    const int64_t zs = (int64_t)r.nx * r.ny, o00 = (int64_t)(j - 1) * r.nx + (i - 1);
+    auto quad = [&](int c, float (&d)[4]) {           // the 2x2 x/y corners of padded plane c
+        const bool pc = c >= 1 && c <= r.nz;
+        const float* b = r.v + (o00 + (int64_t)(c - 1) * zs);
+        d[0] = pc && c00 ? __ldg(b) : 0.0f;
+        d[1] = pc && c10 ? __ldg(b + 1) : 0.0f;
+        d[2] = pc && c01 ? __ldg(b + r.nx) : 0.0f;
+        d[3] = pc && c11 ? __ldg(b + r.nx + 1) : 0.0f;
+    };
     for (int k0 = kb * kOctRun; k0 < r.nz + 1; k0 += kstep * kOctRun) {
         const int k1 = min(k0 + kOctRun, r.nz + 1);
-        float q[4] = {r.at(i, j, k0), r.at(i + 1, j, k0), r.at(i, j + 1, k0), r.at(i + 1, j + 1, k0)};
+        float q[4];
+        quad(k0, q);
 #pragma unroll kOctUnroll
         for (int k = k0; k < k1; ++k) {
-            const float n[4] = {r.at(i, j, k + 1), r.at(i + 1, j, k + 1), r.at(i, j + 1, k + 1),
-                                r.at(i + 1, j + 1, k + 1)};
+            float n[4];
+            quad(k + 1, n);
             // (c000, c100 - c000, c010, c110 - c010 | the same for plane k+1): the differences are
             // rounded exactly as the sampler's lerp rounds them (bit-identical to LINEAR)
             const float c[8] = {q[0], __fsub_rn(q[1], q[0]), q[2], __fsub_rn(q[3], q[2]),
