@@ -227,6 +227,16 @@ def test_animated_validation(nsl):
         assert needle in msg, (needle, msg)
 
 
+def test_bench_l1_gather_validation(nsl):
+    L = nsl.lib()
+    n = ctypes.c_uint64()
+    for args, needle in [((None, 1, 1, 4096, 1 << 20), "NULL"), ((4096, 0, 1, 4096, 1 << 20), "waves")]:
+        vol, waves, reps, sink, nf = args
+        rc = L.nsl_bench_l1_gather(vol, waves, reps, sink, nf, ctypes.byref(n), None)
+        msg = L.nsl_last_error().decode()
+        assert rc == 1 and needle in msg, (args, msg)
+
+
 def test_mixed_sizes_rejected(nsl):
     from dataclasses import replace
     w = I.make_workload("C2", frames=[0, 1])
