@@ -192,7 +192,9 @@ __global__ void __launch_bounds__(kRelightThreads, MINB) relight_kernel(const Re
 #pragma unroll
                 for (int a = 0; a < 3; ++a) dir[a] *= inv;
             }
-            for (int l = 0; l < ns; ++l) {
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {       // ns <= 4: unrolled, so the shadow-map loads overlap
+                if (l >= ns) break;
                 const RelightShadowed& S = fs.sl[l];
                 float s = 0.0f;
 #pragma unroll
