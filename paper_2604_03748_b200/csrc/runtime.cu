@@ -131,6 +131,12 @@ __global__ void __launch_bounds__(32 * kSetupWarps) relight_setup_kernel(const R
 }
 
 constexpr int kRelightThreads = 256;
+#ifndef NSL_RL_SH_PPT           // relight with shadow maps: pixels per thread, CTAs per SM
+#define NSL_RL_SH_PPT 1
+#endif
+#ifndef NSL_RL_SH_MINB
+#define NSL_RL_SH_MINB 8
+#endif
 
 // One CTA = kRelightThreads*PPT consecutive pixels of one frame; the frame's constants are
 // staged to shared memory once.  Maps/depth are streamed (evict-first), the output is written
@@ -233,11 +239,11 @@ cudaError_t launch_relight(const RelightIn* in, int F, int n_lights, RelightFram
     relight_setup_kernel<<<(F + kSetupWarps - 1) / kSetupWarps, 32 * kSetupWarps, 0, s>>>(in, F, n_lights, rc, frames);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const long long per = kRelightThreads * (rc.any_shadow ? 1 : 4);
+    const long long per = kRelightThreads * (rc.any_shadow ? NSL_RL_SH_PPT : 4);
     const long long bpf = ((long long)rc.W * rc.H + per - 1) / per;
     if (bpf * F >= (1LL << 31)) return cudaErrorInvalidConfiguration;
     if (rc.any_shadow)
-        relight_kernel<1, 8><<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
+        relight_kernel<NSL_RL_SH_PPT, NSL_RL_SH_MINB><<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
     else
         relight_kernel<4, 1><<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
     return cudaGetLastError();
