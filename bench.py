@@ -242,6 +242,7 @@ def launches_per_step(w, args) -> int:
     slots = 1 if w.light_mode == 1 else len(w.lights[0])
     per_frame = 8 * astr * astr * kstr * slots
     group = max(1, min(w.n_frames, int(float(os.environ.get("NSL_TV_BUDGET_MB", "4096")) * 1048576 // per_frame)))
+    group = min(group, 65535 // slots)
     return n + 1 + 3 * math.ceil(w.n_frames / group)
 
 

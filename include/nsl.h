@@ -95,6 +95,9 @@ size_t nsl_volume_bytes(const nsl_grid_desc* g, int32_t layout);
  *     values are validated on the host (finite, >= 0) before enqueueing.
  *   density_on_device = 1: `density` is device memory; values are checked by
  *     the layout kernel, and nsl_volume_check() reports the result.
+ * Host input: the call returns once the host->device copy of `density` has
+ * completed (it waits for the copy, not for the layout build), so the host
+ * buffer -- pinned or pageable -- may be refilled or freed on return.
  * The handle does not own `device_storage`; the storage (and, for host
  * input, nothing else) must outlive every call that reads the volume. */
 nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32_t density_on_device,
@@ -217,7 +220,12 @@ nsl_status nsl_guiding_map_batch_counted(const nsl_volume* const* vols, int32_t 
  * volume into the same storage between executions is allowed: the plan keeps
  * the storage pointers, not the host handles).  out_debug / counters as in
  * nsl_guiding_map_batch / _counted (at most one of them non-NULL).
- * nsl_plan_destroy frees the plan's device memory (synchronising the device). */
+ * nsl_plan_destroy frees the plan's device memory (synchronising the device).
+ * Concurrency: a plan owns one device workspace (per-frame parameters, tile
+ * cull flags, TV lattices) that every execution rewrites, so executions of
+ * ONE plan must be ordered -- the same stream, or streams/graphs ordered by
+ * events; never two in flight at once.  Independent plans may run
+ * concurrently. */
 typedef struct nsl_plan nsl_plan;
 nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const int32_t* frame_vol,
                            const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,

@@ -324,6 +324,7 @@ class Plan:
         fv = (ctypes.c_int32 * F)(*frame_vol)
         cs = (CameraS * F)(*[camera_s(c) for c in cams])
         fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+        self._vols = list(vols)      # the plan holds raw storage pointers: keep the storage alive
         h = ctypes.c_void_p()
         _check(lib().nsl_plan_create(hv, len(vols), fv, cs, lights_s(lights), len(lights[0]), light_mode,
                                      ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)), fid, F,

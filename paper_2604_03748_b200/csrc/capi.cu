@@ -5,7 +5,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -192,19 +194,45 @@ VolDesc desc_of(const nsl_volume* v) {
     return d;
 }
 
-// Keep the device's stream-ordered pool from returning freed blocks to the OS at
-// every synchronisation (default release threshold 0), so transient frame tables
-// and host-API staging buffers are recycled instead of re-mapped each call.
-void retain_pool_once() {
-    static thread_local int done_dev = -1;
+// Stream-ordered allocations of the library (frame tables, host-API staging, TV lattices) come
+// from a library-private pool per device, never the device's default pool that torch and other
+// libraries share.  Up to NSL_POOL_RETAIN_MB (default 1024) of it is retained across
+// synchronisations, so per-call tables and the host API's staging are recycled instead of
+// re-mapped each call; anything above is released at the next synchronisation (e.g. the
+// transient TV lattices of up to NSL_TV_BUDGET_MB).
+cudaError_t pool_malloc_v(void** p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props;
+            memset(&props, 0, sizeof props);
+            props.allocType = cudaMemAllocationTypePinned;
+            props.handleTypes = cudaMemHandleTypeNone;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            cudaMemPool_t np = nullptr;
+            e = cudaMemPoolCreate(&np, &props);
+            if (e != cudaSuccess) return e;
+            double mb = 1024.0;
+            if (const char* env = getenv("NSL_POOL_RETAIN_MB")) mb = atof(env);
+            uint64_t thr = mb <= 0.0 ? 0 : (uint64_t)(mb * 1048576.0);
+            cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &thr);
+            pools[dev] = np;
+        }
+        pool = pools[dev];
     }
-    done_dev = dev;
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+template <class T>
+cudaError_t pool_malloc(T** p, size_t bytes, cudaStream_t s) {
+    return pool_malloc_v(reinterpret_cast<void**>(p), bytes, s);
 }
 
 // Frame tables: FrameIn[F] | lights[F*nl] | FrameParams[F] in one stream-ordered allocation.
@@ -225,8 +253,7 @@ nsl_status upload_frames(const std::vector<FrameIn>& frames, const nsl_light* li
     const size_t b_l = align_up(sizeof(nsl_light) * (size_t)F * n_lights, 256);
     const size_t b_p = align_up(sizeof(FrameParams) * F, 256);
     const size_t b_c = march ? march_cull_bytes(F, frames[0].cam.width, frames[0].cam.height) : 0;
-    retain_pool_once();
-    NSL_CUDA(cudaMallocAsync(&ws.base, b_in + b_l + b_p + b_c, s), "cudaMallocAsync(frame tables)");
+    NSL_CUDA(pool_malloc(&ws.base, b_in + b_l + b_p + b_c, s), "cudaMallocAsync(frame tables)");
     ws.in = reinterpret_cast<FrameIn*>(ws.base);
     ws.lights = reinterpret_cast<nsl_light*>(static_cast<char*>(ws.base) + b_in);
     ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l);
@@ -317,19 +344,35 @@ static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* densit
     cudaError_t e = cudaSuccess;
     const float* raw = density;
     void* staging = nullptr;
+    // nsl.h: host density may be reused as soon as nsl_volume_upload returns.  A copy from
+    // pinned memory is still in flight after cudaMemcpyAsync (pageable sources are staged
+    // synchronously by the driver), so the call waits for the copy -- not for the build, which
+    // stays asynchronous.  (The host API, validate_host = false, owns that lifetime itself.)
+    cudaEvent_t copied = nullptr;
+    auto drop = [&](nsl_status st) { if (copied) cudaEventDestroy(copied); return bail(st); };
     if (!density_on_device) {
-        retain_pool_once();
-        e = cudaMallocAsync(&staging, n * sizeof(float), s);
+        e = pool_malloc(&staging, n * sizeof(float), s);
         if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMallocAsync(staging)"));
         e = cudaMemcpyAsync(staging, density, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return bail(cuda_fail(e, "density upload"));
+        if (validate_host) {
+            e = cudaEventCreateWithFlags(&copied, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventRecord(copied, s);
+            if (e != cudaSuccess) return drop(cuda_fail(e, "density upload event"));
+        }
         raw = static_cast<const float*>(staging);
     }
     e = enqueue_build(v, raw, s);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "volume build launch"));
+    if (e != cudaSuccess) return drop(cuda_fail(e, "volume build launch"));
     if (staging) {
         e = cudaFreeAsync(staging, s);
-        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaFreeAsync(staging)"));
+        if (e != cudaSuccess) return drop(cuda_fail(e, "cudaFreeAsync(staging)"));
+    }
+    if (copied) {
+        e = cudaEventSynchronize(copied);
+        cudaEventDestroy(copied);
+        copied = nullptr;
+        if (e != cudaSuccess) return bail(cuda_fail(e, "density upload wait"));
     }
     *out = v;
     return NSL_OK;
@@ -400,6 +443,8 @@ static void tv_geometry(const nsl_volume* const* vols, int n_vols, Prepared& P) 
     const double per_frame = (double)sizeof(float2) * P.tv_slot_elems() * P.tv_slots;
     const double g = std::floor(budget_mb * 1048576.0 / per_frame);
     P.tv_group = g < 1.0 ? 1 : (g > P.F ? P.F : (int)g);
+    // tv_sweep_kernel's grid.y is group * slots (<= 65535)
+    if ((long long)P.tv_group * P.tv_slots > 65535) P.tv_group = 65535 / P.tv_slots;
 }
 
 // The march of a prepared batch: one launch, or (light_model TV) the lattice setup, then per
@@ -490,7 +535,7 @@ static nsl_status batch_impl(const nsl_volume* const* vols, int32_t n_vols, cons
     if (nsl_status st = build_frames(P.frames, lights, n_lights, P.mc, true, s, ws)) return st;
     void* tvws = nullptr;
     cudaError_t e = cudaSuccess;
-    if (P.tv_slots) e = cudaMallocAsync(&tvws, align_up(P.tv_params_bytes(), 256) + P.tv_buf_bytes(), s);
+    if (P.tv_slots) e = pool_malloc(&tvws, align_up(P.tv_params_bytes(), 256) + P.tv_buf_bytes(), s);
     if (e == cudaSuccess)
         e = run_march(P, ws.params, ws.cull, static_cast<TvParams*>(tvws),
                       reinterpret_cast<float2*>(static_cast<char*>(tvws) + align_up(P.tv_params_bytes(), 256)),
@@ -550,9 +595,8 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     const size_t vb = nsl_volume_bytes(g, layout);
     const size_t npix = (size_t)F * cams[0].width * cams[0].height;
     void *vstore = nullptr, *dout = nullptr;
-    retain_pool_once();
-    NSL_CUDA(cudaMallocAsync(&vstore, vb, s), "cudaMallocAsync(volume)");
-    cudaError_t e = cudaMallocAsync(&dout, npix * 20, s);
+    NSL_CUDA(pool_malloc(&vstore, vb, s), "cudaMallocAsync(volume)");
+    cudaError_t e = pool_malloc(&dout, npix * 20, s);
     if (e != cudaSuccess) {
         cudaFreeAsync(vstore, s);
         return cuda_fail(e, "cudaMallocAsync(outputs)");
@@ -684,7 +728,7 @@ nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* 
     if (st == NSL_OK) st = upload_frames(P.frames, lights, n_lights, true, s, ws);
     if (st == NSL_OK && P.tv_slots) {
         Pc.F = per;
-        e = cudaMallocAsync(&tvws, align_up(Pc.tv_params_bytes(), 256) + Pc.tv_buf_bytes(), s);
+        e = pool_malloc(&tvws, align_up(Pc.tv_params_bytes(), 256) + Pc.tv_buf_bytes(), s);
         if (e != cudaSuccess) st = cuda_fail(e, "cudaMallocAsync(TV workspace)");
     }
     for (int f0 = 0; st == NSL_OK && f0 < F; f0 += per) {
@@ -842,7 +886,7 @@ nsl_status nsl_sixway_bake(const nsl_volume* const* vols, int32_t n_vols, const 
     Workspace ws;
     if (nsl_status st = build_frames(P.frames, dummy.data(), 1, P.mc, false, s, ws)) return st;
     BakeFrame* bf = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bf), sizeof(BakeFrame) * F, s);
+    cudaError_t e = pool_malloc(&bf, sizeof(BakeFrame) * F, s);
     if (e == cudaSuccess) e = launch_bake_setup(ws.in, ws.params, F, b->light_step, med->hg_g, bf, s);
     if (e == cudaSuccess && counters) e = cudaMemsetAsync(counters, 0, sizeof(uint64_t), s);
     if (e == cudaSuccess) {
@@ -904,10 +948,9 @@ nsl_status nsl_relight(const nsl_camera* cams, int32_t F, const float* maps, con
         }
     }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    retain_pool_once();
     void* ws = nullptr;
     const size_t b_in = align_up(sizeof(RelightIn) * F, 256);
-    NSL_CUDA(cudaMallocAsync(&ws, b_in + sizeof(RelightFrame) * F, s), "cudaMallocAsync(relight tables)");
+    NSL_CUDA(pool_malloc(&ws, b_in + sizeof(RelightFrame) * F, s), "cudaMallocAsync(relight tables)");
     cudaError_t e = cudaMemcpyAsync(ws, in.data(), sizeof(RelightIn) * F, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) {
         RelightConst rc;
@@ -955,7 +998,7 @@ nsl_status nsl_debug_bake_lights(const nsl_grid_desc* g, const nsl_camera* cam, 
     if (nsl_status st = build_frames(frames, &dummy, 1, mc, false, s, ws)) return st;
     BakeFrame* bf = nullptr;
     BakeFrame h;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bf), sizeof(BakeFrame), s);
+    cudaError_t e = pool_malloc(&bf, sizeof(BakeFrame), s);
     if (e == cudaSuccess) e = launch_bake_setup(ws.in, ws.params, 1, m.step, 0.0f, bf, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bf, sizeof h, cudaMemcpyDeviceToHost, s);
     if (bf) cudaFreeAsync(bf, s);

@@ -249,15 +249,17 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
             const float rho = sample<LAYOUT, COUNT>(v, x, y, z, c_gath);
             if (rho > 0.0f) {
                 ++n_occ;
-                const float sig_t = mc.kappa * rho;
-                const float sig_s = mc.alpha * sig_t;
+                // C6/C7/C11 decide integers from sig_s and T: explicitly rounded ops, so every
+                // kernel variant (FAST, DEBUG, COUNTED; any light set) takes the same decisions
+                const float sig_t = __fmul_rn(mc.kappa, rho);
+                const float sig_s = __fmul_rn(mc.alpha, sig_t);
                 if (n_hit == 0 && sig_s > mc.tau_d) {   // C6
                     n_hit = n;
                     Dout = t;
                 }
-                const float s = sig_t * mc.h;            // C7
+                const float s = __fmul_rn(sig_t, mc.h);  // C7
                 const float Tp = T;
-                tau += s;
+                tau = __fadd_rn(tau, s);
                 T = __expf(-tau);
                 float A;
                 if (mc.form == NSL_OPACITY_EXP) A = mc.alpha * (Tp - T);

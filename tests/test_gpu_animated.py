@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import nsl_inputs as I
-from parity import compare_frame
+from parity import compare_frame, fast_decisions
 
 pytestmark = pytest.mark.gpu
 
@@ -61,9 +61,11 @@ def test_animated_parity_sampled(nsl):
     w = I.make_workload("C4", frames=FRAMES)
     g, gd, n = _animated(nsl, w, 3, 0, check=True)
     assert n == 0
+    dbg = nsl.run_workload(w, layout=3, debug=True)
+    dec = fast_decisions((g, gd), tuple(t.cpu().numpy() for t in dbg))
     pix = np.arange(0, w.height * w.width, 211)
     for f in (0, 5, 6):
-        compare_frame(w, f, g[f], gd[f], None, pixels=pix)
+        compare_frame(w, f, g[f], gd[f], None, pixels=pix, dec=dec[f])
 
 
 def test_animated_counts_invalid_density(nsl):

@@ -9,7 +9,7 @@ import pytest
 
 import nsl_inputs as I
 import oracle
-from parity import compare_frame, value_ok
+from parity import compare_frame, fast_decisions, value_ok
 
 pytestmark = pytest.mark.gpu
 
@@ -31,6 +31,14 @@ def run(nsl, w, layout=1, debug=True, march=None):
     rgbt, depth, dbg = nsl.run_workload(w, layout=layout, debug=debug, march=march)
     torch.cuda.synchronize()
     return (rgbt.cpu().numpy(), depth.cpu().numpy(), None if dbg is None else dbg.cpu().numpy())
+
+
+def run_fast(nsl, w, layout=1, march=None, pixels=None):
+    """The timed FAST launch, plus its (n_hit, n_term) from a DEBUG launch of the same frames
+    (parity.fast_decisions: T and D bitwise equal first), for tie re-verification."""
+    fast = run(nsl, w, layout=layout, debug=False, march=march)
+    dbg = run(nsl, w, layout=layout, debug=True, march=march)
+    return fast[0], fast[1], fast_decisions(fast, dbg, pixels)
 
 
 def bits(a):
@@ -121,8 +129,8 @@ def test_parity_C1_nondebug_front_identity(nsl, kw):
     """The timed path (no debug counters; the guide-set kernel with the C9 front-light
     shortcut, the single-light kernel, the generic one for perspective guide sets)."""
     w = I.make_workload("C1", **kw)
-    g, gd, _ = run(nsl, w, debug=False)
-    compare_frame(w, 0, g[0], gd[0], None)
+    g, gd, dec = run_fast(nsl, w)
+    compare_frame(w, 0, g[0], gd[0], None, dec=dec[0])
 
 
 def test_parity_C1_corner_f16(nsl):
@@ -146,9 +154,14 @@ def test_layouts_agree_bitwise(nsl):
 @pytest.mark.parametrize("debug", [True, False])
 def test_parity_C2(nsl, debug):
     w = I.make_workload("C2", frames=[0, 30])
-    g, gd, gdbg = run(nsl, w, debug=debug)
+    if debug:
+        g, gd, gdbg = run(nsl, w, debug=True)
+        dec = [None, None]
+    else:
+        g, gd, dec = run_fast(nsl, w)
+        gdbg = None
     for f in range(2):
-        compare_frame(w, f, g[f], gd[f], None if gdbg is None else gdbg[f])
+        compare_frame(w, f, g[f], gd[f], None if gdbg is None else gdbg[f], dec=dec[f])
 
 
 def test_parity_C2_bench_launch_configuration(nsl):
@@ -166,9 +179,10 @@ def test_parity_C2_bench_launch_configuration(nsl):
         plan.execute(outs[0], outs[1])
     torch.cuda.synchronize()
     g, gd = outs[0].cpu().numpy(), outs[1].cpu().numpy()
+    dec = fast_decisions((g, gd), run(nsl, w, layout=3, debug=True))
     pix = np.arange(0, w.height * w.width, 97)
     for f in range(w.n_frames):
-        compare_frame(w, f, g[f], gd[f], None, pixels=(pix + 13 * f) % (w.height * w.width))
+        compare_frame(w, f, g[f], gd[f], None, pixels=(pix + 13 * f) % (w.height * w.width), dec=dec[f])
 
 
 def test_parity_C2_density_sweep(nsl):
@@ -181,9 +195,14 @@ def test_parity_C2_density_sweep(nsl):
 @pytest.mark.parametrize("debug", [True, False])
 def test_parity_C3(nsl, debug):
     w = I.make_workload("C3", frames=[0, 30])
-    g, gd, gdbg = run(nsl, w, debug=debug)
+    if debug:
+        g, gd, gdbg = run(nsl, w, debug=True)
+        dec = [None, None]
+    else:
+        g, gd, dec = run_fast(nsl, w)
+        gdbg = None
     for f in range(2):
-        compare_frame(w, f, g[f], gd[f], None if gdbg is None else gdbg[f])
+        compare_frame(w, f, g[f], gd[f], None if gdbg is None else gdbg[f], dec=dec[f])
 
 
 def _subsample(H, W, step):
@@ -202,10 +221,10 @@ def test_parity_C4_subsampled(nsl):
 def test_parity_C5_subsampled_full_size(nsl):
     """512^3, 2048^2 in the bench launch configuration (no debug), sampled 1/64."""
     w = I.make_workload("C5", frames=[0, 512])
-    g, gd, _ = run(nsl, w, debug=False)
     pix = _subsample(w.height, w.width, 8)
+    g, gd, dec = run_fast(nsl, w, layout=3, pixels=pix)
     for f in range(2):
-        compare_frame(w, f, g[f], gd[f], None, pixels=pix)
+        compare_frame(w, f, g[f], gd[f], None, pixels=pix, dec=dec[f])
 
 
 # ------------------------------------------------------------------ batch / determinism / sharding / host API
@@ -330,8 +349,8 @@ def test_edge_cases(nsl):
     for name, w in cases.items():
         g, gd, gdbg = run(nsl, w)
         compare_frame(w, 0, g[0], gd[0], gdbg[0])
-        g2, gd2, _ = run(nsl, w, debug=False)
-        compare_frame(w, 0, g2[0], gd2[0], None)
+        g2, gd2, dec = run_fast(nsl, w)
+        compare_frame(w, 0, g2[0], gd2[0], None, dec=dec[0])
     # the miss case touches nothing; the zero grid is transparent
     g, _, gdbg = run(nsl, cases["miss"])
     assert np.all(g[0][..., 3] == 1.0) and not gdbg.any()

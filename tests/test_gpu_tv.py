@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import nsl_inputs as I
-from parity import compare_frame
+from parity import compare_frame, fast_decisions
 
 pytestmark = pytest.mark.gpu
 
@@ -28,18 +28,27 @@ def tv(w):
 
 
 def run(nsl, w, layout=3, debug=True):
+    """debug=False: the FAST launch, its third element the (n_hit, n_term) of a DEBUG launch
+    of the same frames (parity.fast_decisions) for tie re-verification."""
     import torch
     rgbt, depth, dbg = nsl.run_workload(w, layout=layout, debug=debug)
     torch.cuda.synchronize()
-    return rgbt.cpu().numpy(), depth.cpu().numpy(), None if dbg is None else dbg.cpu().numpy()
+    out = rgbt.cpu().numpy(), depth.cpu().numpy(), None if dbg is None else dbg.cpu().numpy()
+    if debug:
+        return out
+    return out[0], out[1], fast_decisions(out, run(nsl, w, layout=layout, debug=True))
+
+
+def cmp(w, f, g, gd, d, debug, **kw):
+    return compare_frame(w, f, g[f], gd[f], d[f] if debug else None, dec=None if debug else d[f], **kw)
 
 
 @pytest.mark.parametrize("debug", [True, False])
 @pytest.mark.parametrize("kw", [{}, {"perspective": True}, {"single_light": True}])
 def test_tv_parity_C1(nsl, debug, kw):
     w = tv(I.make_workload("C1", **kw))
-    g, gd, gdbg = run(nsl, w, debug=debug)
-    compare_frame(w, 0, g[0], gd[0], gdbg[0] if gdbg is not None else None)
+    g, gd, d = run(nsl, w, debug=debug)
+    cmp(w, 0, g, gd, d, debug)
 
 
 @pytest.mark.parametrize("debug", [True, False])
@@ -48,8 +57,8 @@ def test_tv_long_windows_C1(nsl, debug):
     so the sweep takes its long-window path."""
     w = tv(I.make_workload("C1"))
     w = replace(w, march=replace(w.march, light_step=w.march.step / 8))
-    g, gd, gdbg = run(nsl, w, debug=debug)
-    compare_frame(w, 0, g[0], gd[0], gdbg[0] if gdbg is not None else None)
+    g, gd, d = run(nsl, w, debug=debug)
+    cmp(w, 0, g, gd, d, debug)
 
 
 def test_tv_differs_from_march_only_in_light_transmittance(nsl):
@@ -107,7 +116,7 @@ def test_tv_parity_C4_C5_subsampled(nsl):
     config (C5, groups of one frame under the default budget): sampled pixels vs the oracle."""
     for cfg, frames, step in (("C4", [0, 120], 613), ("C5", [0, 700], 4099)):
         w = tv(I.make_workload(cfg, frames=frames))
-        g, gd, _ = run(nsl, w, debug=False)
+        g, gd, dec = run(nsl, w, debug=False)
         pix = np.arange(0, w.height * w.width, step)
         for f in range(len(frames)):
-            compare_frame(w, f, g[f], gd[f], None, pixels=pix)
+            compare_frame(w, f, g[f], gd[f], None, pixels=pix, dec=dec[f])

@@ -540,6 +540,71 @@ def test_early_termination_rule(orc):
     assert np.array_equal(rf["rgbt"][term], r["rgbt"][term])
 
 
+def test_early_termination_is_the_first_crossing(orc):
+    """C11: n_term is the FIRST step whose T_n (fp32
+    decision) falls below T_min.  T_n is taken from runs with the rule switched off
+    (t_min = 0) and capped at N (Alg. 1's step count input): at N = n_term
+    T < T_min, at N = n_term - 1 still T >= T_min; pixels that never terminate keep
+    T >= T_min at n_hi.  An oracle that stops one occupied step late (or early) fails."""
+    w = I.make_workload("C2", frames=[0], kappa=128.0)
+    pix = np.arange(0, 512 * 512, 53)
+    m = w.march
+    r = orc.run_workload_frame(w, 0, pixels=pix)
+    d = r["debug"].astype(np.int64)
+    term = (d[:, 3] > 0) & (d[:, 3] < d[:, 1])
+    assert term.sum() > 50
+    assert np.all(r["rgbt"][~term & (d[:, 0] > 0), 3].astype(np.float32) >= np.float32(m.t_min))
+    T_at = {}
+    for N in sorted(set(d[term, 3].tolist()) | set((d[term, 3] - 1).tolist())):
+        sel = term & ((d[:, 3] == N) | (d[:, 3] - 1 == N))
+        mN = I.March(**{**m.__dict__, "t_min": 0.0, "max_steps": int(N)})
+        rN = orc.guiding_map(w.grid, w.volume(0), w.cameras[0], w.lights[0], w.light_mode, w.medium, mN,
+                             frame_id=w.frame_ids[0], pixels=pix[sel])
+        for p, t in zip(pix[sel], rN["rgbt"][:, 3]):
+            T_at[(int(p), int(N))] = np.float32(t)
+    for p, nt in zip(pix[term], d[term, 3]):
+        assert T_at[(int(p), int(nt))] < np.float32(m.t_min), (p, nt)
+        assert T_at[(int(p), int(nt) - 1)] >= np.float32(m.t_min), (p, nt)
+        # and the terminated run reports exactly T_{n_term}
+    assert np.array_equal(r["rgbt"][term, 3].astype(np.float32),
+                          np.array([T_at[(int(p), int(nt))] for p, nt in zip(pix[term], d[term, 3])]))
+
+
+def test_guide_axis_fallback_closed_form(orc):
+    """Ledger #8 ("omega x z"): when omega is parallel to the guide axis,
+    omega x z vanishes and the side lights fall back to +-normalize(omega x x_hat).  A camera
+    looking straight down (forward -z, omega = +z) with axis z gives omega x x_hat =
+    (0,0,1) x (1,0,0) = (0,1,0): top = +y_hat, bottom = -y_hat, front = +z_hat (closed form)."""
+    g = grid64(32)
+    med = I.Medium(32.0, 1.0, 0.0)
+    guide = I.guide_lights()
+    inv = np.float32(1.0 / np.float64(g.voxel_width))
+    fc = orc.frame_constants(g, cam_down(), guide, I.LIGHTS_GUIDE, med, march(10.0 / 32))
+    np.testing.assert_array_equal(fc["Ln"], np.array([[0, 0, 1], [0, 1, 0], [0, -1, 0]], np.float32))
+    np.testing.assert_array_equal(fc["Lg"], np.array([[0, 0, inv], [0, inv, 0], [0, -inv, 0]], np.float32))
+    # omega = -z (camera looking up): (0,0,-1) x (1,0,0) = (0,-1,0)
+    cam_up = I.Camera(I.ORTHO, (0.5, 0.5, -1.0), (0.0, 0.0, 1.0), (0.0, 1.0, 0.0), 0.9, 32, 32)
+    fc = orc.frame_constants(g, cam_up, guide, I.LIGHTS_GUIDE, med, march(10.0 / 32))
+    np.testing.assert_array_equal(fc["Ln"], np.array([[0, 0, -1], [0, -1, 0], [0, 1, 0]], np.float32))
+    # rendered consequence: with a blob off-centre in +y (and centred in x) the guide set's
+    # image equals front + explicit lights along the closed-form directions +-y (additivity
+    # over lights, P7) -- and differs from the +-x pair a wrong fallback would pick
+    vals = np.zeros((32, 32, 32), np.float32)
+    vals[10:22, 21:27, 8:24] = 0.7
+    m = march(1.0 / 32)
+
+    def explicit(d):
+        return orc.guiding_map(g, vals, cam_down(), [I.Light(d, (1.0, 1.0, 1.0))], I.LIGHTS_EXPLICIT, med,
+                               m)["rgbt"][:, 0]
+
+    gm = orc.guiding_map(g, vals, cam_down(), guide, I.LIGHTS_GUIDE, med, m)["rgbt"][:, 0]
+    front = explicit((0.0, 0.0, 1.0))
+    np.testing.assert_allclose(gm, front + explicit((0.0, 1.0, 0.0)) + explicit((0.0, -1.0, 0.0)),
+                               rtol=1e-12, atol=1e-15)
+    wrong = front + explicit((1.0, 0.0, 0.0)) + explicit((-1.0, 0.0, 0.0))
+    assert np.abs(gm - wrong).max() > 1e-3 * np.abs(gm).max()
+
+
 def test_golden_hash_table_is_current(orc):
     """tests/golden/jitter_hash.txt was written by tests/golden/make_golden.py from the oracle."""
     import os
