@@ -227,6 +227,72 @@ def sampler_ceiling(layout, counts, march_s):
 
 
 
+def l1_patterns(w, nsl):
+    """Lane element offsets [16, 32] for the hardware L1/TEX ceiling (nsl_bench_l1_peak), all in
+    the OCT layout of w's grid (one 32-B element per trilinear sample):
+      footprint: the march's own gathers for one warp -- 8 x 4 pixels at the image centre of
+        frame 0, patterns 0-7 at 8 consecutive primary steps through the volume centre, 8-15 at
+        light steps 1..8 of the guide set's first side light from the middle sample;
+      coalesced: 32 consecutive elements per pattern (8 distinct 128-B lines per load);
+      broadcast: one element for every lane."""
+    g = w.grid
+    fc = nsl.debug_frame_constants(g, w.cameras[0], w.lights[0], w.light_mode, w.medium, w.march)
+    sy, sz = g.nx + 1, (g.nx + 1) * (g.ny + 1)
+    W, H = w.width, w.height
+    lane = np.arange(32)
+    px = (W // 2 - 4) + lane % 8
+    py = (H // 2 - 2) + lane // 8
+    B, Ex, Ey, Dg = (np.asarray(fc[k], np.float64) for k in ("B", "Ex", "Ey", "Dg"))
+    O = B[None, :] + px[:, None] * Ex[None, :] + py[:, None] * Ey[None, :]
+    centre = np.array([g.nx, g.ny, g.nz], np.float64) / 2.0 + 0.5
+    hidx = w.march.step / g.voxel_width                                   # h in index units
+    dlen = np.linalg.norm(Dg)
+    tc = float(np.dot(centre - O[0], Dg) / dlen ** 2)                     # ray parameter at the centre
+    pos = []
+    for k in range(8):
+        pos.append(O + (tc + (k - 4) * hidx / dlen) * Dg[None, :])
+    L = np.asarray(fc["Lg"][1], np.float64) * w.march.step               # one light step (index units)
+    for j in range(1, 9):
+        pos.append(pos[4] + j * L[None, :])
+    lim = np.array([g.nx, g.ny, g.nz], np.float64)
+    e = []
+    for u in pos:
+        c = np.clip(np.floor(u), 0, lim).astype(np.int64)
+        e.append(c[:, 0] + c[:, 1] * sy + c[:, 2] * sz)
+    e = np.stack(e)
+    foot = e - e.min()
+    coal = np.arange(16)[:, None] * 32 + lane[None, :]
+    bcast = np.zeros((16, 32), np.int64)
+    return {"footprint": foot, "coalesced": coal, "broadcast": bcast}
+
+
+def l1_hw_ceiling(w, nsl, patterns=("footprint",), stride=0, span=1, reps=256, waves=8, iters=7):
+    """Measured lane bytes/s of nsl_bench_l1_peak per lane pattern (CUDA events, median)."""
+    import torch
+    pats = l1_patterns(w, nsl)
+    out = {}
+    for name in patterns:
+        off = torch.from_numpy(pats[name].astype(np.int32)).cuda()
+        max_off = int(pats[name].max())
+        buf = torch.ones((span + max_off + 1) * 8, dtype=torch.float32, device="cuda")
+        sink = torch.empty(148 * 8 * 256 * waves, dtype=torch.float32, device="cuda")
+        nbytes = nsl.bench_l1_peak(buf, off, stride, span, waves, reps, sink)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            nsl.bench_l1_peak(buf, off, stride, span, waves, reps, sink)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        t = statistics.median(ts)
+        lines = [len(set((pats[name][k] * 32 // 128).tolist())) for k in range(16)]
+        out[name] = {"lane_gbs": nbytes / t / 1e9, "launch_ms": t * 1e3, "bytes": nbytes,
+                     "lines_per_load": float(np.mean(lines))}
+    return out
+
+
 def launches_per_step(w, args) -> int:
     """Kernels of one timed step: volume_build + occ_finalize per distinct volume, then
     frame_setup, tile_cull and march_kernel; the TV light model adds tv_setup and, per frame

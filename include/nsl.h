@@ -341,6 +341,19 @@ nsl_status nsl_guide_lights(const nsl_camera* cam, const float axis[3], const fl
 nsl_status nsl_bench_l1_gather(const nsl_volume* vol, int32_t waves, int32_t reps, float* sink, size_t sink_floats,
                                uint64_t* samples, nsl_stream stream);
 
+/* Hardware L1/TEX gather ceiling (the roofline denominator of the march): every
+ * lane of waves x (SMs x resident CTAs) CTAs of 256 threads issues reps x 16 loads of one
+ * 32-B element (ld.global.nc.v8.f32, the OCT sampler's gather) at element offsets
+ * lane_off[k*32 + lane] (k = 0..15; device int32[512], each in [0, max_off]) from
+ * buf + 32 B * shift_r, shift_r = (r * stride_elems) mod span_elems, and sums the eight
+ * floats -- no other work.  stride_elems = 0: every load hits the same few L1-resident
+ * lines (the L1 ceiling for that lane pattern).  buf: device, 32-B aligned, >= (span_elems +
+ * max_off) * 8 floats; sink: device, >= threads floats.  *bytes (host) = lane bytes the
+ * launch loads (threads * reps * 16 * 32).  Time it with events on `stream`.  Asynchronous. */
+nsl_status nsl_bench_l1_peak(const float* buf, size_t buf_floats, const int32_t* lane_off, int32_t max_off,
+                             int64_t stride_elems, int64_t span_elems, int32_t waves, int32_t reps, float* sink,
+                             size_t sink_floats, uint64_t* bytes, nsl_stream stream);
+
 /* ------------------------------------------------------------------ debug / verification
  * Frame constants of DESIGN.md C3/C3b/C10 as the device computes them
  * (fp64 evaluation rounded once to fp32), for bitwise comparison with the

@@ -104,7 +104,7 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
            "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
-           "nsl_guiding_map_animated", "nsl_bench_l1_gather"]
+           "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak"]
 
 
 class BakeS(ctypes.Structure):
@@ -149,6 +149,8 @@ def lib():
                                            i32, i32, P(MediumS), P(MarchS), P(u32), i32, i32, vp, vp,
                                            P(ctypes.c_uint64), vp]
     L.nsl_bench_l1_gather.argtypes = [vp, i32, i32, vp, ctypes.c_size_t, P(ctypes.c_uint64), vp]
+    L.nsl_bench_l1_peak.argtypes = [vp, ctypes.c_size_t, vp, i32, ctypes.c_int64, ctypes.c_int64, i32, i32, vp,
+                                    ctypes.c_size_t, P(ctypes.c_uint64), vp]
     L.nsl_debug_frame_constants.argtypes = [P(GridDesc), P(CameraS), P(LightS), i32, i32, P(MediumS),
                                             P(MarchS), P(FrameConstantsS), vp]
     L.nsl_debug_jitter.argtypes = [P(MarchS), u32, i32, vp, vp, vp]
@@ -502,6 +504,18 @@ def bench_l1_gather(vol: Volume, sink, waves: int = 4, reps: int = 64, stream=No
     n = ctypes.c_uint64()
     _check(lib().nsl_bench_l1_gather(vol.handle, waves, reps, sink.data_ptr(), sink.numel(), ctypes.byref(n),
                                      _stream_handle(stream)), "nsl_bench_l1_gather")
+    return n.value
+
+
+def bench_l1_peak(buf, lane_off, stride: int = 0, span: int = 1, waves: int = 4, reps: int = 64, sink=None,
+                  stream=None) -> int:
+    """Enqueue the hardware L1/TEX gather ceiling (nsl_bench_l1_peak); returns the lane bytes it loads.
+    buf: cuda float32 (32-B aligned); lane_off: cuda int32 [16, 32] element offsets."""
+    n = ctypes.c_uint64()
+    max_off = int(lane_off.max().item())
+    _check(lib().nsl_bench_l1_peak(buf.data_ptr(), buf.numel(), lane_off.data_ptr(), max_off, stride, span, waves,
+                                   reps, sink.data_ptr(), sink.numel(), ctypes.byref(n), _stream_handle(stream)),
+           "nsl_bench_l1_peak")
     return n.value
 
 

@@ -1116,6 +1116,31 @@ nsl_status nsl_bench_l1_gather(const nsl_volume* vol, int32_t waves, int32_t rep
     return NSL_OK;
 }
 
+nsl_status nsl_bench_l1_peak(const float* buf, size_t buf_floats, const int32_t* lane_off, int32_t max_off,
+                             int64_t stride_elems, int64_t span_elems, int32_t waves, int32_t reps, float* sink,
+                             size_t sink_floats, uint64_t* bytes, nsl_stream stream) {
+    g_err.clear();
+    if (!buf || !lane_off || !sink || !bytes) return fail(NSL_ERR_INVALID_ARG, "NULL buf/lane_off/sink/bytes");
+    if (waves < 1 || reps < 1 || max_off < 0 || stride_elems < 0 || span_elems < 1)
+        return fail(NSL_ERR_INVALID_ARG, "bad waves/reps/max_off/stride/span");
+    if (reinterpret_cast<uintptr_t>(buf) % 32) return fail(NSL_ERR_INVALID_ARG, "buf must be 32-B aligned");
+    // every load stays inside buf: (span - 1 + max_off + 1) elements of 8 floats
+    if ((uint64_t)(span_elems + max_off) * 8 > buf_floats)
+        return fail(NSL_ERR_INVALID_ARG, "buf needs %lld floats", (long long)(span_elems + max_off) * 8);
+    int dev = 0, sms = 0;
+    NSL_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    NSL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    const int per_sm = l1_peak_max_blocks_per_sm();
+    const size_t blocks = (size_t)sms * (per_sm > 0 ? per_sm : 1) * waves;
+    const size_t threads = blocks * l1_peak_threads();
+    if (sink_floats < threads) return fail(NSL_ERR_INVALID_ARG, "sink needs %zu floats", threads);
+    NSL_CUDA(launch_l1_peak(buf, lane_off, (long long)(stride_elems % span_elems), (long long)span_elems,
+                            (int)blocks, reps, sink, reinterpret_cast<cudaStream_t>(stream)),
+             "l1_peak_kernel launch");
+    *bytes = (uint64_t)threads * reps * l1_peak_patterns() * 32;
+    return NSL_OK;
+}
+
 nsl_status nsl_debug_jitter(const nsl_march* m, uint32_t frame_id, int32_t n, uint32_t* out_hash, float* out_delta,
                             nsl_stream stream) {
     g_err.clear();

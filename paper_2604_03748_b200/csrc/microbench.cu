@@ -30,7 +30,59 @@ __global__ void __launch_bounds__(kMbThreads) l1_gather_kernel(Vol v, int reps, 
     sink[blockIdx.x * kMbThreads + threadIdx.x] = acc;
 }
 
+// Hardware L1/TEX gather ceiling (no sampler arithmetic): every lane issues 16 x reps
+// ld.global.nc.v8.f32 -- one 32-B element each, the OCT gather's width -- at element offsets
+// lane_off[k][lane] from buf + shift_r (shift_r = r * stride mod span), summing the eight
+// floats.  Per load: one IMAD.WIDE, the LDG.256 and seven FADDs (all eight floats used).  With stride 0 every load of
+// the launch hits the same few L1-resident lines: the L1 data path's own rate for the lane
+// pattern in lane_off.
+constexpr int kPkThreads = 256, kPkPat = 16;
+
+__global__ void __launch_bounds__(kPkThreads) l1_peak_kernel(const float* __restrict__ buf,
+                                                             const int* __restrict__ lane_off, long long stride,
+                                                             long long span, int reps, float* __restrict__ sink) {
+    const int lane = threadIdx.x & 31;
+    int off[kPkPat];
+#pragma unroll
+    for (int k = 0; k < kPkPat; ++k) off[k] = __ldg(lane_off + k * 32 + lane);
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    long long shift = 0;
+    for (int r = 0; r < reps; ++r) {
+        const float* base = buf + 8 * shift;
+#pragma unroll
+        for (int k0 = 0; k0 < kPkPat; k0 += 4) {       // 4 independent loads in flight per thread
+            float v[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                             : "=f"(v[q][0]), "=f"(v[q][1]), "=f"(v[q][2]), "=f"(v[q][3]), "=f"(v[q][4]),
+                               "=f"(v[q][5]), "=f"(v[q][6]), "=f"(v[q][7])
+                             : "l"(base + 8 * off[k0 + q]));
+            // all eight floats are consumed (else ptxas narrows the 256-bit load's register write)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                acc[q] += ((v[q][0] + v[q][1]) + (v[q][2] + v[q][3])) + ((v[q][4] + v[q][5]) + (v[q][6] + v[q][7]));
+        }
+        shift += stride;
+        if (shift >= span) shift -= span;
+    }
+    sink[(size_t)blockIdx.x * kPkThreads + threadIdx.x] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
 }  // namespace
+
+int l1_peak_threads() { return kPkThreads; }
+int l1_peak_patterns() { return kPkPat; }
+int l1_peak_max_blocks_per_sm() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, l1_peak_kernel, kPkThreads, 0);
+    return n;
+}
+cudaError_t launch_l1_peak(const float* buf, const int* lane_off, long long stride, long long span, int blocks,
+                           int reps, float* sink, cudaStream_t s) {
+    l1_peak_kernel<<<blocks, kPkThreads, 0, s>>>(buf, lane_off, stride, span, reps, sink);
+    return cudaGetLastError();
+}
 
 int l1_gather_threads() { return kMbThreads; }
 int l1_gather_line() { return kMbLine; }

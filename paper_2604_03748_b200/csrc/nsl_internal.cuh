@@ -210,6 +210,11 @@ cudaError_t launch_l1_gather(const FrameParams& p, int blocks, int reps, float* 
 int l1_gather_threads();
 int l1_gather_line();
 int l1_gather_max_blocks_per_sm(int layout);
+int l1_peak_threads();
+int l1_peak_patterns();
+int l1_peak_max_blocks_per_sm();
+cudaError_t launch_l1_peak(const float* buf, const int* lane_off, long long stride, long long span, int blocks,
+                           int reps, float* sink, cudaStream_t s);
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s);
 // mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path.
