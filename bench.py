@@ -10,10 +10,14 @@ prepared plan (nsl_plan_execute).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
 
-Multi-GPU (torchrun, one process per GPU): frames are independent, so each
-rank marches its own 60 frames (global frame ids rank + N*k, weak scaling)
-with no data-path collective; time = max over ranks of the device-timed loop.
-Rank 0 prints ONE JSON line.
+Multi-GPU (torchrun, one process per GPU; `--gpus N` outside torchrun re-launches
+itself as N ranks): frames are independent, so by default each rank marches its
+own 60 frames (global frame ids rank + N*k, weak scaling) with no data-path
+collective; time = max over ranks of the device-timed loop.  `--scaling strong`
+splits the config's fixed batch (C4: 240, C5: 1024 frames) cyclically over the
+ranks and `--gather` gathers every step's guiding maps to rank 0 inside the
+timed step (chunked, overlapped with the march).  Rank 0
+prints ONE JSON line.
 """
 import argparse
 import json
@@ -52,11 +56,18 @@ def parse():
                    help="march: canonical C8 (the headline); tv: NEXT-4 transmittance volume (DESIGN.md §12)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--gather", action="store_true",
-                   help="N>1: after the timed loop, time the NCCL gather of all guiding maps to rank 0")
+                   help="N>1: gather every step's guiding maps to rank 0 inside the timed step (chunked, overlapped)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sampler-ceiling", action="store_true",
                    help="skip the sampler microbenchmark after the timed region (ncu launch lists)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: every rank its own F frames (default); strong: the config's fixed batch "
+                        "(C4: 240, C5: 1024 frames) split cyclically over the ranks")
+    p.add_argument("--chunk", type=int, default=0,
+                   help="sharded runs: frames per chunk (a gathered chunk's send overlaps the next chunk's march)")
+    p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                   help="process group backend (gloo: functional runs of ranks sharing one GPU, host-staged gather)")
     return p.parse_args()
 
 
@@ -312,8 +323,167 @@ def launches_per_step(w, args) -> int:
     return n + 1 + 3 * math.ceil(w.n_frames / group)
 
 
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this command as N ranks
+    under torch.distributed.run on 127.0.0.1 (one process per GPU) and return its exit code."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+# ------------------------------------------------------------------ sharded runs (--scaling strong / --gather)
+def run_sharded(args, rank, world, local):
+    """Frame-sharded step with the result gather to rank 0 inside the timed region (SURVEY
+    §8(d): t_P from a barrier to gather completion on rank 0; §8(e): cyclic shards, chunked
+    gather overlapped with the march).  strong: the config's fixed batch (C2 60, C3 60, C4 240,
+    C5 1024 frames) over the ranks; weak: every rank F frames.  One step: per chunk of the
+    rank's padded shard, the layouts of the chunk's volumes (every chunk when frames view
+    different volumes -- C4 -- else once per step), the chunk's plan (frame setup, cull,
+    march) into its rows of the shard, then the chunk's send to rank 0 on a side stream."""
+    import torch
+    import torch.distributed as dist
+    import nsl_inputs as I
+    import paper_2604_03748_b200 as nsl
+    from paper_2604_03748_b200 import sharding
+
+    cfg = args.config
+    layout = nsl.LAYOUTS[args.layout]
+    n_cfg = {"C1": 1, "C2": 60, "C3": 60, "C4": 240, "C5": 1024}[cfg]
+    if args.scaling == "strong":
+        F_total = args.frames or n_cfg
+        mine = sharding.shard_frames(F_total, world, rank)
+        full = I.make_workload(cfg, frames=[0]) if cfg in ("C4", "C5") else I.make_workload(cfg)
+        w = (I.make_workload(cfg, frames=[g % n_cfg for g in mine]) if cfg in ("C4", "C5")
+             else full.subset([g % n_cfg for g in mine]))
+        w.frame_ids = list(mine)
+    else:
+        w = rank_workload(cfg, rank, world, args.frames)
+        F_total = w.n_frames * world
+    if args.light_model == "tv":
+        from dataclasses import replace
+        w = replace(w, march=replace(w.march, light_model=1))
+    L = sharding.shard_len(F_total, world) if args.scaling == "strong" else w.n_frames
+    n_real, H, W = w.n_frames, w.height, w.width
+    animated = len(w.volume_specs) > 1
+    chunk = args.chunk or (max(1, min(L, 8 if animated else 16)))
+    bounds = sharding.chunk_bounds(L, chunk)
+    stream = torch.cuda.current_stream()
+
+    # inputs resident in HBM: raw densities of the rank's volumes; layout storage for one chunk
+    # of per-frame volumes (animated) or the single volume; outputs (rank 0: the rank-major
+    # result tensors of all ranks, its own shard = row 0)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        host = list(ex.map(w.volume, range(len(w.volume_specs))))
+    raw = [torch.from_numpy(v).cuda() for v in host]
+    del host
+    nslot = chunk if animated else 1
+    storage = [torch.empty(nsl.volume_bytes(w.grid, layout), dtype=torch.uint8, device="cuda") for _ in range(nslot)]
+    if rank == 0:
+        outs = [torch.empty((world, L, H, W, 4), dtype=torch.float32, device="cuda"),
+                torch.empty((world, L, H, W), dtype=torch.float32, device="cuda")]
+        bufs = [outs[0][0], outs[1][0]]
+    else:
+        outs = None
+        bufs = [torch.empty((L, H, W, 4), dtype=torch.float32, device="cuda"),
+                torch.empty((L, H, W), dtype=torch.float32, device="cuda")]
+    comm = torch.cuda.Stream() if args.backend == "nccl" else None
+
+    # one plan per chunk (its real frames), built once: frame tables uploaded, storage pointers kept
+    def chunk_vols(a, b):
+        frames = [f for f in range(a, min(b, n_real))]
+        if animated:
+            return frames, [nsl.Volume(w.grid, raw[w.frame_vol[f]], layout, storage=storage[i])
+                            for i, f in enumerate(frames)]
+        return frames, None
+
+    static_vol = None if animated else [nsl.Volume(w.grid, raw[0], layout, storage=storage[0])]
+    plans = []
+    for a, b in bounds:
+        frames, vols = chunk_vols(a, b)
+        if not frames:
+            plans.append(None)
+            continue
+        sub = w.subset(frames)
+        fv = list(range(len(frames))) if animated else [0] * len(frames)
+        plans.append(nsl.Plan(vols if animated else static_vol, fv, sub.cameras, sub.lights, sub.light_mode,
+                              sub.medium, sub.march, sub.frame_ids))
+    torch.cuda.synchronize()
+
+    def step():
+        g = sharding.ChunkedGather(bufs, outs, comm_stream=comm) if world > 1 else None
+        keep = [nsl.Volume(w.grid, raw[0], layout, storage=storage[0])] if not animated else []
+        for (a, b), plan in zip(bounds, plans):
+            if plan is not None:
+                if animated:
+                    keep = chunk_vols(a, b)[1]                               # a1: this chunk's layouts
+                e = min(b, n_real)
+                plan.execute(bufs[0][a:e], bufs[1][a:e])                     # a2-a9
+            if g is not None:
+                g.send_chunk(a, b)
+        if g is not None:
+            g.finish()
+        return keep
+
+    step()
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    clocks = ClockSampler(local).start()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    times = []
+    for _ in range(K):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)                   # after finish(): the last receive on rank 0
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    clk = clocks.stop()
+    t_loop = sum(times)
+    if world > 1:
+        t = torch.tensor([t_loop], device="cuda")
+        if args.backend == "gloo":
+            t = t.cpu()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_loop = float(t.item())
+    rays = W * H * F_total * K
+    line = {"metric": METRIC, "value": rays / t_loop, "unit": "rays/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_loop / K, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f16" if layout == 2 else "f32",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT[cfg], "frames_total": F_total, "frames_per_rank": L,
+                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": args.layout,
+                       "light_model": args.light_model, "chunk_frames": chunk,
+                       "l2": "flushed (512 MiB write) before each timed step, outside the events",
+                       "parallelism": f"frame-sharded x{world} (cyclic), results gathered to rank 0 "
+                                      f"inside the step ({args.backend}, chunked, overlapped)"},
+            "frames_per_s": F_total * K / t_loop, "ms_per_frame": 1e3 * t_loop / (K * F_total),
+            "gather_bytes_to_rank0_per_step": int((world - 1) * L * H * W * 20),
+            "gpu_launches": K * sum(2 * (len(p._vols) if animated else 0) + 3 for p in plans if p is not None)
+                            + (K * 2 if not animated else 0),
+            "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return line
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -324,9 +494,19 @@ def main():
     import torch.distributed as dist
     import paper_2604_03748_b200 as nsl
 
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())        # ranks may share a GPU (gloo functional runs)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    if args.scaling == "strong" or (args.gather and world > 1):
+        run_sharded(args, rank, world, dev)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     layout = nsl.LAYOUTS[args.layout]
     cfg = args.config
     w = rank_workload(cfg, rank, world, args.frames)
@@ -364,7 +544,7 @@ def main():
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    clocks = ClockSampler(local).start()
+    clocks = ClockSampler(dev).start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -449,22 +629,6 @@ def main():
             "march_ms_per_step": statistics.mean(march_ms), "layout_ms_per_step": statistics.mean(layout_ms),
             "counts_per_rank_step": counts, "gpu_launches": launches_per_step(w, args) * K, "clocks": clk,
             "roofline": roof}
-
-    # optional result gather to rank 0 (the only collective of the design; not in the timed step)
-    if world > 1 and args.gather:
-        from paper_2604_03748_b200 import sharding
-        rgbt_local = outputs[0]
-        dist.barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        full = sharding.gather_frames(rgbt_local, F * world)
-        g1.record(stream)
-        torch.cuda.synchronize()
-        tg = torch.tensor([g0.elapsed_time(g1)], device="cuda")
-        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
-        line["gather"] = {"ms": float(tg.item()), "bytes_to_rank0": int(rgbt_local.numel() * 4 * (world - 1)),
-                          "what": "rgbt float4 maps of all ranks -> rank 0 (torch.distributed.gather, NCCL)"}
-        del full
 
     # end-to-end through the public host API: pinned host density in, pinned host guiding maps out
     if not args.no_e2e:

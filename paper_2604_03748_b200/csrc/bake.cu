@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kBakeThreads, NSL_BAKE_MINB) bake_kernel(const
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
     v.mask_words = sp.slab_off;
+    v.zero_e = sp.zero_e;
 
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t gath = 0;

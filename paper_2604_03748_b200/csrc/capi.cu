@@ -57,6 +57,10 @@ double norm3(const float v[3]) {
 }
 
 constexpr size_t kTail = 256;  // counter area after the layout (keeps 16-B alignment)
+// In the tail: +0 invalid-value counter, +16 occupied block box, +kZeroElem a 32-B all-zero
+// element (written by occ_finalize_kernel) that the march's branch-free gathers read for
+// samples in empty blocks.
+constexpr size_t kZeroElem = 128;
 
 size_t body_bytes(const nsl_grid_desc* g, int layout) {
     return layout_elems(layout, g->nx, g->ny, g->nz) * layout_elem_bytes(layout);
@@ -191,6 +195,7 @@ VolDesc desc_of(const nsl_volume* v) {
     d.occ = v->occ;
     d.og = v->og;
     d.aabb = v->aabb;
+    d.zero_e = (int32_t)((tail_offset(&v->g, v->layout) + kZeroElem) / 32);
     return d;
 }
 
@@ -1110,6 +1115,7 @@ nsl_status nsl_bench_l1_gather(const nsl_volume* vol, int32_t waves, int32_t rep
     p.occ_nbx = vol->og.nbx;
     p.occ_nby = vol->og.nby;
     p.slab_off = vol->og.words;
+    p.zero_e = desc_of(vol).zero_e;
     NSL_CUDA(launch_l1_gather(p, (int)blocks, reps, sink, reinterpret_cast<cudaStream_t>(stream)),
              "l1_gather_kernel launch");
     *samples = (uint64_t)threads * reps * l1_gather_line();

@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
     v.mask_words = sp.slab_off;
+    v.zero_e = sp.zero_e;
     if (PROJ == 0 && (cflag & (DEBUG || COUNT ? 2 : 1))) {
         if (valid) {                   // the empty map: L = 0, T = 1, D = 0, counters 0
             out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
@@ -289,8 +290,12 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
                     }
                     if (COUNT) c_tl += (uint32_t)(ma + mb);
                     float sa, sb;
-                    light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, ma, mb, sa,
-                                                  sb, c_gath);
+                    if (NSL_HZ && ((sp.lz0 >> 1) & 3) == 3)     // both side lights horizontal: hoisted z plane
+                        light_sum_pair_hz<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], mc.hl, ma, mb, sa, sb,
+                                                         c_gath);
+                    else
+                        light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, ma, mb,
+                                                      sa, sb, c_gath);
                     S[1] = __fmaf_rn(A, __expf(-kl * sa), S[1]);
                     S[2] = __fmaf_rn(A, __expf(-kl * sb), S[2]);
                     lsamp += (uint32_t)(Ma + Mb);

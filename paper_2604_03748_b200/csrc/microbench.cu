@@ -100,6 +100,7 @@ cudaError_t launch_l1_gather(const FrameParams& p, int blocks, int reps, float* 
     v.sy1 = p.supp[1];
     v.sz1 = p.supp[2];
     v.mask_words = p.slab_off;
+    v.zero_e = p.zero_e;
     switch (p.layout) {
         case kLinearF32: l1_gather_kernel<kLinearF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
         case kQuadF32: l1_gather_kernel<kQuadF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;

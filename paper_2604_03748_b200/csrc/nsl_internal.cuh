@@ -35,6 +35,7 @@ struct VolDesc {
     const uint32_t* occ;
     OccGeom og;
     const int32_t* aabb;       // occupied block bounds: bmin xyz, bmax xyz (bmin > bmax: empty volume)
+    int32_t zero_e;            // OCT layouts: element index (from data) of a 32-B all-zero element
 };
 
 // Raw per-frame input (host -> device, one memcpy per call).
@@ -72,7 +73,8 @@ struct FrameParams {
     float alim[4][3];          // light march exit plane of the occupied box per axis
     int32_t slab_off;          // word offset of the slab boxes in the staged occupancy region
     int32_t lz0;               // bit l: L_g,l,z == 0 exactly (the march of light l stays in its z slab)
-    int32_t pad2[3];
+    int32_t zero_e;            // OCT layouts: element index of the all-zero element (VolDesc)
+    int32_t pad2[2];
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 

@@ -63,6 +63,9 @@ static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (3
 #ifndef NSL_MINB_G3
 #define NSL_MINB_G3 6   // its register cap (40: 48 warps/SM)
 #endif
+#ifndef NSL_HZ                  // horizontal guide pair: z plane hoisted out of the light loop
+#define NSL_HZ 1
+#endif
 constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
@@ -72,6 +75,7 @@ struct Vol {
     int shift, nbx, nby;
     float sx1, sy1, sz1;          // support upper bounds n+1
     int mask_words;               // NSL_CHECK only: occupancy mask words
+    int zero_e;                   // OCT layouts: the all-zero element (branch-free gathers)
 };
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return __fmaf_rn(t, b - a, a); }
@@ -88,24 +92,10 @@ __device__ __forceinline__ bool inside(const Vol& v, float x, float y, float z) 
 // low mantissa bits and r - 1.5*2^23 is floor(x) exactly.  No F2I/FRND (the
 // quarter-rate XU pipe) per sample.  Positions in support satisfy 0 < x < n+1.
 constexpr float kFloorBias = 12582912.0f;   // 1.5 * 2^23, bit pattern 0x4B400000
-template <int LAYOUT, bool COUNT>
-__device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
-    // cell floors (shared with the gather below), block = cell >> shift
-    const float rx = __fadd_rd(x, kFloorBias), ry = __fadd_rd(y, kFloorBias), rz = __fadd_rd(z, kFloorBias);
-    const int ix = __float_as_int(rx) - 0x4B400000, iy = __float_as_int(ry) - 0x4B400000,
-              iz = __float_as_int(rz) - 0x4B400000;
-    const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
-    NSL_ASSERT(ix >= 0 && iy >= 0 && iz >= 0 && (float)ix < v.sx1 && (float)iy < v.sy1 && (float)iz < v.sz1);
-    NSL_ASSERT(b >= 0 && (b >> 5) < v.mask_words);
-    const uint32_t word = __ldg(v.occ + (b >> 5));
-    if (!((word >> (b & 31)) & 1u)) return 0.0f;
-    if (COUNT) ++gathers;
-    const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias)),
-                fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
-    const int e = LAYOUT == kBrickOctF32
-                      ? (((iz >> 2) * v.sz + (iy >> 2) * v.sy + (ix >> 2)) << 6) | ((iz & 3) << 4) | ((iy & 3) << 2) |
-                            (ix & 3)
-                      : ix + iy * v.sy + iz * v.sz;
+// C1 trilinear from the gathered corners of element e (cell floors ix, iy, iz) with the exact
+// fractions (fx, fy, fz): one load per layout as DESIGN.md §6 describes.
+template <int LAYOUT>
+__device__ __forceinline__ float gather_interp(const Vol& v, int e, float fx, float fy, float fz) {
     if (LAYOUT == kLinearF32) {
         const float* p = static_cast<const float*>(v.data) + e;
         const float c000 = __ldg(p), c100 = __ldg(p + 1);
@@ -146,6 +136,96 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
         const float x01 = lerpf(c.x, c.y, fx), x11 = lerpf(d.x, d.y, fx);
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
     }
+}
+
+// OCT / BRICK_OCT gather issued under a predicate (no branch): an empty sample's load is not
+// issued and its lerps run on whatever the registers hold; the select returns exactly 0.
+template <int LAYOUT>
+__device__ __forceinline__ float gather_interp_pred(const Vol& v, int e, float fx, float fy, float fz, bool occ) {
+    static_assert(LAYOUT == kOctF32 || LAYOUT == kBrickOctF32, "predicated gather: OCT layouts only");
+    float a0, a1, a2, a3, b0, b1, b2, b3;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %9, 0;\n\t"
+        "@p ld.global.nc.L1::evict_first.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
+        : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
+        : "l"(static_cast<const float*>(v.data) + 8 * (size_t)e), "r"((uint32_t)occ));
+    const float x00 = __fmaf_rn(fx, a1, a0), x10 = __fmaf_rn(fx, a3, a2);
+    const float x01 = __fmaf_rn(fx, b1, b0), x11 = __fmaf_rn(fx, b3, b2);
+    const float r = lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
+    return occ ? r : 0.0f;
+}
+#ifndef NSL_PRED
+#define NSL_PRED 0
+#endif
+__host__ __device__ constexpr bool kPredOct(int layout) { return NSL_PRED && (layout == kOctF32 || layout == kBrickOctF32); }
+// NSL_ZSEL: branch-free OCT samples -- an empty sample gathers the tail's all-zero element (an L1
+// hit) instead of branching around the gather; its trilinear of zeros is exactly +0.
+#ifndef NSL_ZSEL
+#define NSL_ZSEL 0
+#endif
+__host__ __device__ constexpr bool kZsel(int layout) { return NSL_ZSEL && (layout == kOctF32 || layout == kBrickOctF32); }
+
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
+    // cell floors (shared with the gather below), block = cell >> shift
+    const float rx = __fadd_rd(x, kFloorBias), ry = __fadd_rd(y, kFloorBias), rz = __fadd_rd(z, kFloorBias);
+    const int ix = __float_as_int(rx) - 0x4B400000, iy = __float_as_int(ry) - 0x4B400000,
+              iz = __float_as_int(rz) - 0x4B400000;
+    const int b = ((iz >> v.shift) * v.nby + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
+    NSL_ASSERT(ix >= 0 && iy >= 0 && iz >= 0 && (float)ix < v.sx1 && (float)iy < v.sy1 && (float)iz < v.sz1);
+    NSL_ASSERT(b >= 0 && (b >> 5) < v.mask_words);
+    const uint32_t word = __ldg(v.occ + (b >> 5));
+    const bool occ = (word >> (b & 31)) & 1u;
+    if (!kPredOct(LAYOUT) && !kZsel(LAYOUT) && !occ) return 0.0f;
+    if (COUNT) gathers += occ;
+    const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias)),
+                fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
+    const int e = LAYOUT == kBrickOctF32
+                      ? (((iz >> 2) * v.sz + (iy >> 2) * v.sy + (ix >> 2)) << 6) | ((iz & 3) << 4) | ((iy & 3) << 2) |
+                            (ix & 3)
+                      : ix + iy * v.sy + iz * v.sz;
+    if constexpr (kZsel(LAYOUT)) return gather_interp<LAYOUT>(v, occ ? e : v.zero_e, fx, fy, fz);
+    if constexpr (kPredOct(LAYOUT)) return gather_interp_pred<LAYOUT>(v, e, fx, fy, fz, occ);
+    else return gather_interp<LAYOUT>(v, e, fx, fy, fz);
+}
+
+// A horizontal light line (L_z == 0 bit-exactly: every Y_j keeps U_z, since fma(s, 0, u_z) ==
+// u_z) shares one z cell, fraction and block row: computed once per occupied primary sample
+// instead of per light sample.  sample_hz(v, zp, x, y) == sample(v, x, y, z) bit for bit.
+struct ZPlane {
+    int zb;      // (iz >> shift) * nby: the block row base
+    int ze;      // the z part of the element index (BRICK: the brick plane, times sz)
+    int zl;      // BRICK: the z part inside the brick
+    float fz;
+};
+template <int LAYOUT>
+__device__ __forceinline__ ZPlane zplane(const Vol& v, float z) {
+    const float rz = __fadd_rd(z, kFloorBias);
+    const int iz = __float_as_int(rz) - 0x4B400000;
+    ZPlane p;
+    p.zb = (iz >> v.shift) * v.nby;
+    p.ze = LAYOUT == kBrickOctF32 ? (iz >> 2) * v.sz : iz * v.sz;
+    p.zl = LAYOUT == kBrickOctF32 ? (iz & 3) << 4 : 0;
+    p.fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
+    return p;
+}
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ float sample_hz(const Vol& v, const ZPlane& zp, float x, float y, uint32_t& gathers) {
+    const float rx = __fadd_rd(x, kFloorBias), ry = __fadd_rd(y, kFloorBias);
+    const int ix = __float_as_int(rx) - 0x4B400000, iy = __float_as_int(ry) - 0x4B400000;
+    const int b = (zp.zb + (iy >> v.shift)) * v.nbx + (ix >> v.shift);
+    NSL_ASSERT(ix >= 0 && iy >= 0 && (float)ix < v.sx1 && (float)iy < v.sy1);
+    NSL_ASSERT(b >= 0 && (b >> 5) < v.mask_words);
+    const uint32_t word = __ldg(v.occ + (b >> 5));
+    const bool occ = (word >> (b & 31)) & 1u;
+    if (!kPredOct(LAYOUT) && !kZsel(LAYOUT) && !occ) return 0.0f;
+    if (COUNT) gathers += occ;
+    const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias));
+    const int e = LAYOUT == kBrickOctF32
+                      ? ((zp.ze + (iy >> 2) * v.sy + (ix >> 2)) << 6) | zp.zl | ((iy & 3) << 2) | (ix & 3)
+                      : ix + iy * v.sy + zp.ze;
+    if constexpr (kZsel(LAYOUT)) return gather_interp<LAYOUT>(v, occ ? e : v.zero_e, fx, fy, zp.fz);
+    if constexpr (kPredOct(LAYOUT)) return gather_interp_pred<LAYOUT>(v, e, fx, fy, zp.fz, occ);
+    else return gather_interp<LAYOUT>(v, e, fx, fy, zp.fz);
 }
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
@@ -283,6 +363,24 @@ __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy,
         if (j <= Ma) a += sample<LAYOUT, COUNT>(v, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), __fmaf_rn(s, lz, uz), gathers);
         if (j <= Mb)
             b += sample<LAYOUT, COUNT>(v, __fmaf_rn(-s, lx, ux), __fmaf_rn(-s, ly, uy), __fmaf_rn(-s, lz, uz), gathers);
+    }
+    sa = a;
+    sb = b;
+}
+
+// light_sum_pair for a horizontal pair (both lights' L_z == 0 bit-exactly): the same samples
+// through sample_hz, the z plane of U computed once.
+template <int LAYOUT, bool COUNT>
+__device__ __forceinline__ void light_sum_pair_hz(const Vol& v, float ux, float uy, float uz, float lx, float ly,
+                                                  float hl, int Ma, int Mb, float& sa, float& sb, uint32_t& gathers) {
+    const ZPlane zp = zplane<LAYOUT>(v, uz);
+    float a = 0.0f, b = 0.0f;
+    const int M = max(Ma, Mb);
+    float jf = 1.0f;
+    for (int j = 1; j <= M; ++j, jf += 1.0f) {
+        const float s = __fmul_rn(jf, hl);
+        if (j <= Ma) a += sample_hz<LAYOUT, COUNT>(v, zp, __fmaf_rn(s, lx, ux), __fmaf_rn(s, ly, uy), gathers);
+        if (j <= Mb) b += sample_hz<LAYOUT, COUNT>(v, zp, __fmaf_rn(-s, lx, ux), __fmaf_rn(-s, ly, uy), gathers);
     }
     sa = a;
     sb = b;

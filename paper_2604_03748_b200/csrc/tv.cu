@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __rest
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
     v.mask_words = sp.slab_off;
+    v.zero_e = sp.zero_e;
     const float af = t.a0 + (float)i, bf = t.b0 + (float)j;
     float base[3];
 #pragma unroll

@@ -383,6 +383,8 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
     __syncthreads();
     if (threadIdx.x < 6) aabb[threadIdx.x] = am[threadIdx.x];
     if (threadIdx.x == 0) *invalid = nbad;
+    // the all-zero element of the tail (capi.cu kZeroElem = tail + 128 B), read by branch-free gathers
+    if (threadIdx.x < 8) reinterpret_cast<float*>(reinterpret_cast<char*>(invalid) + 128)[threadIdx.x] = 0.0f;
 }
 
 }  // namespace

@@ -12,6 +12,15 @@ The only collective is the optional result gather to rank 0 (NCCL over
 NVLink on GPUs; gloo works for the CPU tests): every rank contributes a tensor
 of identical shape [F_per_rank, ...] (shards are padded to equal length) and
 rank 0 receives them in rank order and undoes the cyclic interleave.
+
+ChunkedGather overlaps that gather with the march (SURVEY §8(e) "Overlap"):
+each rank's padded shard [L, ...] is marched in chunks of c frames; as soon as
+chunk k is done on the compute stream it is sent to rank 0 on a communication
+stream (point-to-point sends, one receive per peer on rank 0, grouped so NCCL
+runs them concurrently) while chunk k+1 marches.  Rank 0 receives peer r's
+chunk straight into its rank-major result buffer out[r, k*c:(k+1)*c] and marches
+its own frames into out[0], so nothing is copied twice; unshard_order maps a
+global frame to its row of out.view(P*L, ...).
 """
 from __future__ import annotations
 
@@ -68,3 +77,76 @@ def pad_shard(t, n_frames: int, world: int, rank: int):
         return t
     pad = torch.zeros((L - t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
     return torch.cat([t, pad], dim=0)
+
+
+def chunk_bounds(L: int, chunk: int) -> List[tuple]:
+    """[start, end) rows of each chunk of a padded shard of L rows (the last may be short)."""
+    if chunk < 1:
+        raise ValueError("chunk must be >= 1")
+    return [(a, min(a + chunk, L)) for a in range(0, L, chunk)]
+
+
+class ChunkedGather:
+    """Chunked result gather to rank 0, overlapped with the march (module docstring).
+
+    bufs: the per-rank shard buffers, one tensor per output kind (e.g. rgbt [L,H,W,4] and
+    depth [L,H,W]); on rank 0 these are out[0] views of the rank-major result tensors
+    `outs` ([P, L, ...] each), on the other ranks plain [L, ...] tensors.  After chunk k
+    rows a:b of every buf are final on the compute stream, call send_chunk(a, b); at the
+    end call finish().  NCCL: device tensors, the sends/receives run on `comm_stream`
+    (which first waits for the compute stream), so they overlap the next chunk's march.
+    gloo (CPU tests, ranks sharing one GPU): tensors are staged through host memory and
+    the exchange is synchronous."""
+
+    def __init__(self, bufs, outs=None, group=None, comm_stream=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.bufs = list(bufs)
+        self.outs = None if outs is None else list(outs)
+        if self.rank == 0 and self.outs is None:
+            raise ValueError("rank 0 needs the rank-major result tensors")
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.comm = comm_stream
+        self.works = []
+
+    def send_chunk(self, a: int, b: int):
+        import torch
+        dist = self.dist
+        if self.world == 1:
+            return
+        if self.nccl:
+            ev = torch.cuda.Event()
+            ev.record()                                   # the chunk's march on the compute stream
+            self.comm.wait_event(ev)
+            with torch.cuda.stream(self.comm):
+                ops = []
+                for t, o in zip(self.bufs, self.outs or [None] * len(self.bufs)):
+                    if self.rank == 0:
+                        for r in range(1, self.world):
+                            ops.append(dist.P2POp(dist.irecv, o[r, a:b], r, self.group))
+                    else:
+                        ops.append(dist.P2POp(dist.isend, t[a:b], 0, self.group))
+                self.works += dist.batch_isend_irecv(ops)
+            return
+        # gloo: host staging, synchronous
+        for i, t in enumerate(self.bufs):
+            if self.rank == 0:
+                for r in range(1, self.world):
+                    h = torch.empty(t[a:b].shape, dtype=t.dtype)
+                    dist.recv(h, src=r, group=self.group)
+                    self.outs[i][r, a:b].copy_(h)
+            else:
+                dist.send(t[a:b].detach().cpu().contiguous(), dst=0, group=self.group)
+
+    def finish(self):
+        """Make the current stream wait for every outstanding send/receive."""
+        import torch
+        if self.nccl and self.works:
+            with torch.cuda.stream(self.comm):
+                for w in self.works:
+                    w.wait()
+            torch.cuda.current_stream().wait_stream(self.comm)
+        self.works = []

@@ -82,3 +82,48 @@ def test_bench_rank_workloads_partition_frames():
         ids += list(w.frame_ids)
         assert w.frame_ids == sharding.shard_frames(6 * world, world, r)
     assert sorted(ids) == list(range(24))
+
+
+def _chunk_worker(rank, world, port, F, chunk, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    L = sharding.shard_len(F, world)
+    mine = sharding.shard_frames(F, world, rank)
+    if rank == 0:
+        outs = [torch.full((world, L, 3, 5, 4), -1.0), torch.full((world, L, 3, 5), -1.0)]
+        bufs = [outs[0][0], outs[1][0]]
+    else:
+        outs = None
+        bufs = [torch.full((L, 3, 5, 4), -1.0), torch.full((L, 3, 5), -1.0)]
+    g = sharding.ChunkedGather(bufs, outs)
+    for a, b in sharding.chunk_bounds(L, chunk):
+        for i in range(a, min(b, len(mine))):          # the stand-in "march" of the chunk's real frames
+            bufs[0][i] = float(mine[i])
+            bufs[1][i] = 1000.0 + mine[i]
+        g.send_chunk(a, b)
+    g.finish()
+    if rank == 0:
+        order = torch.tensor(sharding.unshard_order(F, world))
+        torch.save((outs[0].reshape(world * L, 3, 5, 4)[order], outs[1].reshape(world * L, 3, 5)[order]), out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("F,chunk", [(8, 3), (7, 2), (9, 16), (2, 1)])
+def test_chunked_gather_world2_gloo(tmp_path, F, chunk):
+    """ChunkedGather (the bench's overlapped result gather): chunk by chunk, rank 0 receives
+    every peer's rows straight into the rank-major result; unshard_order restores frame order."""
+    out = str(tmp_path / "full.pt")
+    mp.spawn(_chunk_worker, args=(2, _free_port(), F, chunk, out), nprocs=2, join=True)
+    rgbt, depth = torch.load(out)
+    assert rgbt.shape == (F, 3, 5, 4) and depth.shape == (F, 3, 5)
+    for f in range(F):
+        assert torch.all(rgbt[f] == float(f)) and torch.all(depth[f] == 1000.0 + f)
+
+
+def test_chunk_bounds():
+    assert sharding.chunk_bounds(10, 4) == [(0, 4), (4, 8), (8, 10)]
+    assert sharding.chunk_bounds(3, 8) == [(0, 3)]
+    with pytest.raises(ValueError):
+        sharding.chunk_bounds(3, 0)
