@@ -243,7 +243,8 @@ def l1_patterns(w, nsl):
     the OCT layout of w's grid (one 32-B element per trilinear sample):
       footprint: the march's own gathers for one warp -- 8 x 4 pixels at the image centre of
         frame 0, patterns 0-7 at 8 consecutive primary steps through the volume centre, 8-15 at
-        light steps 1..8 of the guide set's first side light from the middle sample;
+        light steps 1..8 of the guide set's first side light (else the only light) from the
+        middle sample;
       coalesced: 32 consecutive elements per pattern (8 distinct 128-B lines per load);
       broadcast: one element for every lane."""
     g = w.grid
@@ -262,7 +263,8 @@ def l1_patterns(w, nsl):
     pos = []
     for k in range(8):
         pos.append(O + (tc + (k - 4) * hidx / dlen) * Dg[None, :])
-    L = np.asarray(fc["Lg"][1], np.float64) * w.march.step               # one light step (index units)
+    li = 1 if len(fc["Lg"]) > 1 else 0                                    # a side light, else the only light
+    L = np.asarray(fc["Lg"][li], np.float64) * w.march.step              # one light step (index units)
     for j in range(1, 9):
         pos.append(pos[4] + j * L[None, :])
     lim = np.array([g.nx, g.ny, g.nz], np.float64)
@@ -572,20 +574,31 @@ def main():
     value = total_rays / t_loop
     ms_step = 1e3 * t_loop / K
 
-    # roofline of the dominant kernel (march_kernel).  ncu shows it issue/ALU-bound
-    # (no memory unit near its peak), so bound = "alu": algorithmic work = SURVEY §8(d)'s 25
-    # FP32/INT ops per canonical march sample x the canonical samples of one launch; peak =
-    # 148 SMs x 128 FP32/INT32 lanes x max SM clock.  The L1 view (32 B per canonical sample
-    # through L1/TEX vs 148 x 128 B/clk) and the gathers actually executed are reported beside it.
+    # roofline of the dominant kernel (march_kernel): bound = L1/TEX.  Algorithmic
+    # bytes = SURVEY §8(d)'s 32 B (8 fp32 corners) per canonical march sample x the canonical
+    # samples of one launch, over the plan's device time (frame setup + cull + march, CUDA events
+    # on the launch stream).  Peak = the hardware L1/TEX gather ceiling measured live after the
+    # timed region (nsl_bench_l1_peak: ld.global.nc.v8.f32 at this march's own 8 x 4 warp
+    # footprint, L1-resident, no sampler arithmetic; profiles/r2_l1_hw_peak.jsonl).  Beside it: the
+    # FP32 view in one unit (flops, FMA = 2 on both sides), the gathers actually executed and the
+    # sampler's own ceiling.
     peaks = load_peaks()
     march_s = statistics.mean(march_ms) / 1e3
     sm_mhz = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
-    ops = 25 * counts["canonical_samples"]
-    achieved = ops / march_s / 1e9
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9          # Gop/s
     bytes_per_sample = 16 if layout == 2 else 32
-    l1_achieved = counts["canonical_samples"] * 32 / march_s / 1e9
-    l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e9           # GB/s
+    alg_bytes = counts["canonical_samples"] * 32
+    l1_achieved = alg_bytes / march_s / 1e9
+    try:
+        hw = l1_hw_ceiling(w, nsl, patterns=("footprint", "coalesced"))
+        l1_peak = hw["footprint"]["lane_gbs"]
+        peak_src = ("measured: nsl_bench_l1_peak, ld.global.nc.v8.f32 at the march's 8x4 warp footprint "
+                    "(C2 frame 0 geometry), L1-resident, this run")
+    except Exception as e:                    # never fatal: fall back to the nominal figure, say so
+        hw = {"error": str(e)[:200]}
+        l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e9
+        peak_src = "nominal 148 SMs x 128 B/clk x sm_max_mhz (the measurement failed)"
+    flops = 25 * counts["canonical_samples"]        # 25 flops per sample (lerp = 2)
+    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e9  # GFLOP/s, FMA = 2 flops
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_march_traffic.json")
     if os.path.exists(tpath):
@@ -595,14 +608,17 @@ def main():
                 traffic = tj["dram_bytes_per_launch"]
         except Exception:
             traffic = None
-    roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak,
-            "traffic": traffic,
-            "peak_source": "derived: 148 SMs x 128 FP32/INT32 lanes x sm_max_mhz (B200_PROFILING.md unit counts)",
-            "per_unit": "25 ops per canonical march sample (SURVEY 8(d))",
-            "kernel": "march_kernel (+ frame_setup_kernel, same launch sequence)", "kernel_ms": march_s * 1e3,
-            "algorithmic_ops_per_launch": ops,
-            "l1tex_view": {"achieved_gbs": l1_achieved, "peak_gbs": l1_peak, "frac": l1_achieved / l1_peak,
-                           "per_unit": "32 B (8 fp32 corners) per canonical sample"},
+    roof = {"bound": "l1tex", "achieved": l1_achieved, "peak": l1_peak, "unit": "GB/s", "frac": l1_achieved / l1_peak,
+            "traffic": traffic, "peak_source": peak_src,
+            "per_unit": "32 B (8 fp32 corners) per canonical march sample (SURVEY 8(d))",
+            "kernel": "march_kernel (+ frame_setup_kernel, tile_cull_kernel: the plan's launch sequence)",
+            "kernel_ms": march_s * 1e3, "algorithmic_bytes_per_launch": alg_bytes,
+            "canonical_samples_per_launch": counts["canonical_samples"],
+            "l1_ceiling": hw,
+            "fp32_view": {"achieved_gflops": flops / march_s / 1e9, "peak_gflops": fp32_peak,
+                          "frac": flops / march_s / 1e9 / fp32_peak,
+                          "per_unit": "25 flops per canonical sample (SURVEY 8(d), lerp = 2); peak 148 x 128 "
+                                      "lanes x 2 (FMA) x sm_max_mhz"},
             "executed_gathers_per_launch": counts["gathers"],
             "executed_gather_gbs": counts["gathers"] * bytes_per_sample / march_s / 1e9,
             "algorithmic_output_bytes_per_launch": 20 * W * H * F,
@@ -664,7 +680,12 @@ def main():
         res = time_oracle(cfg, args.cpu_seconds)
         line["cpu_baseline"] = {"value": res["rays_per_s"], "unit": "rays/s", "cores": 1, "kind": "oracle",
                                 "sample": res["sample"], "samples_per_s": res["samples_per_s"],
-                                "cpu": host_cpu_name(), "seconds": res["seconds"]}
+                                "cpu": host_cpu_name(), "seconds": res["seconds"],
+                                # whole frames of this workload at the oracle's measured sample rate
+                                "extrapolated_ms_per_frame": 1e3 * counts["canonical_samples"] / F
+                                                            / res["samples_per_s"],
+                                "extrapolation": "canonical march samples per frame (this run's counted launch) / "
+                                                 "the oracle's measured samples/s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
