@@ -51,7 +51,8 @@ def parse():
     p.add_argument("--impl", default="nsl", choices=["nsl", "reference"])
     p.add_argument("--config", default="C2")
     p.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
-    p.add_argument("--layout", default="oct_f32", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32", "brick_oct_f32"])
+    p.add_argument("--layout", default="oct_f32", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32",
+                                                           "brick_oct_f32", "tex3d_f32", "morton_oct_f32"])
     p.add_argument("--light-model", default="march", choices=["march", "tv"],
                    help="march: canonical C8 (the headline); tv: NEXT-4 transmittance volume (DESIGN.md §12)")
     p.add_argument("--no-e2e", action="store_true")
@@ -397,41 +398,37 @@ def run_sharded(args, rank, world, local):
                 torch.empty((L, H, W), dtype=torch.float32, device="cuda")]
     comm = torch.cuda.Stream() if args.backend == "nccl" else None
 
-    # one plan per chunk (its real frames), built once: frame tables uploaded, storage pointers kept
-    def chunk_vols(a, b):
-        frames = [f for f in range(a, min(b, n_real))]
-        if animated:
-            return frames, [nsl.Volume(w.grid, raw[w.frame_vol[f]], layout, storage=storage[i])
-                            for i, f in enumerate(frames)]
-        return frames, None
-
+    # one plan per chunk (its real frames), built once: frame tables uploaded; the chunk's volume
+    # slots (animated) or the single volume are rebuilt in place every step (nsl_volume_rebuild)
+    slot_vols = [nsl.Volume(w.grid, raw[0], layout, storage=st) for st in storage] if animated else None
     static_vol = None if animated else [nsl.Volume(w.grid, raw[0], layout, storage=storage[0])]
     plans = []
     for a, b in bounds:
-        frames, vols = chunk_vols(a, b)
+        frames = list(range(a, min(b, n_real)))
         if not frames:
             plans.append(None)
             continue
         sub = w.subset(frames)
         fv = list(range(len(frames))) if animated else [0] * len(frames)
-        plans.append(nsl.Plan(vols if animated else static_vol, fv, sub.cameras, sub.lights, sub.light_mode,
-                              sub.medium, sub.march, sub.frame_ids))
+        plans.append(nsl.Plan(slot_vols[:len(frames)] if animated else static_vol, fv, sub.cameras, sub.lights,
+                              sub.light_mode, sub.medium, sub.march, sub.frame_ids))
     torch.cuda.synchronize()
 
     def step():
         g = sharding.ChunkedGather(bufs, outs, comm_stream=comm) if world > 1 else None
-        keep = [nsl.Volume(w.grid, raw[0], layout, storage=storage[0])] if not animated else []
+        if not animated:
+            static_vol[0].rebuild(raw[0])                                    # a1: the volume, once per step
         for (a, b), plan in zip(bounds, plans):
             if plan is not None:
-                if animated:
-                    keep = chunk_vols(a, b)[1]                               # a1: this chunk's layouts
+                if animated:                                                 # a1: this chunk's layouts
+                    for i, f in enumerate(range(a, min(b, n_real))):
+                        slot_vols[i].rebuild(raw[w.frame_vol[f]])
                 e = min(b, n_real)
                 plan.execute(bufs[0][a:e], bufs[1][a:e])                     # a2-a9
             if g is not None:
                 g.send_chunk(a, b)
         if g is not None:
             g.finish()
-        return keep
 
     step()
     torch.cuda.synchronize()
@@ -529,11 +526,11 @@ def main():
     plan = nsl.make_plan(w, vols)
 
     def step():
-        vols = [nsl.Volume(w.grid, r, layout, storage=s) for r, s in zip(raw, storage)]       # a1
+        for v, r in zip(vols, raw):
+            v.rebuild(r)                                                                       # a1
         plan.execute(outputs[0], outputs[1])                                                   # a2-a9
-        return vols
 
-    vols = step()
+    step()
     torch.cuda.synchronize()
     counts = plan.execute_counted(outputs[0], outputs[1])
     torch.cuda.synchronize()
@@ -554,7 +551,8 @@ def main():
         flush.zero_()                       # L2 flushed between timed iterations (outside the events)
         e0, e1, e2 = ev[i]
         e0.record(stream)
-        vols = [nsl.Volume(w.grid, r, layout, storage=s) for r, s in zip(raw, storage)]
+        for v, r in zip(vols, raw):
+            v.rebuild(r)
         e1.record(stream)
         plan.execute(outputs[0], outputs[1])
         e2.record(stream)

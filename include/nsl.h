@@ -72,13 +72,25 @@ typedef struct {
  *               storage must be 32-B aligned.  Measured against OCT: the
  *               better choice for a static volume far beyond L2 (512^3, 4.3 GB: C5 march
  *               -5 % over 1024 frames, -11 % over 64), worse at 256^3 (C3 +2 %) and for
- *               a fresh volume per frame (its build costs 2x).  DEFAULT = OCT_F32. */
+ *               a fresh volume per frame (its build costs 2x).
+ *  TEX3D_F32  : the QUAD float4 of every padded cell in a LIBRARY-OWNED 3-D cudaArray read
+ *               through a point-sampled texture object (2 tex fetches/sample, hardware
+ *               3-D addressing, block-linear tiling); `device_storage` holds only the
+ *               occupancy region and tail (nsl_volume_bytes says how much).  Exact fp32
+ *               values (hardware trilinear FILTERING is not used: its 8-bit fractional
+ *               weights cannot meet the 1e-4 bar).  nsl_volume_release frees
+ *               the array; nsl_volume_rebuild refills it in place.
+ *  MORTON_OCT_F32: the OCT elements in 8x8x8-cell tiles (16 KB, tiles x-fastest), Morton
+ *               (z-order) inside a tile; one 256-bit gather/sample; 32-B aligned storage.
+ *  DEFAULT = OCT_F32. */
 typedef enum {
     NSL_LAYOUT_LINEAR_F32 = 0,
     NSL_LAYOUT_QUAD_F32 = 1,
     NSL_LAYOUT_CORNER_F16 = 2,
     NSL_LAYOUT_OCT_F32 = 3,
     NSL_LAYOUT_BRICK_OCT_F32 = 4,
+    NSL_LAYOUT_TEX3D_F32 = 5,
+    NSL_LAYOUT_MORTON_OCT_F32 = 6,
     NSL_LAYOUT_DEFAULT = 3
 } nsl_layout;
 
@@ -108,6 +120,12 @@ nsl_status nsl_volume_upload(const nsl_grid_desc* g, const float* density, int32
 nsl_status nsl_volume_check(const nsl_volume* v, nsl_stream stream, uint64_t* n_invalid);
 /* Frees the handle (never the caller's storage).  NULL is a no-op. */
 nsl_status nsl_volume_release(nsl_volume* v);
+/* Rebuild an existing handle's layout in place from new density values (same grid, layout and
+ * storage; TEX3D: the same array), e.g. a simulator streaming one frame after another into one
+ * volume slot.  Host / device density and validation exactly as
+ * nsl_volume_upload; plans referencing the volume see the new values.  Asynchronous on
+ * `stream` (host input: returns once the density has been copied). */
+nsl_status nsl_volume_rebuild(nsl_volume* v, const float* density, int32_t density_on_device, nsl_stream stream);
 
 /* ------------------------------------------------------------------ frame parameters
  * Camera (C3).  forward and up must be finite,

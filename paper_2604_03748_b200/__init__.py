@@ -26,8 +26,10 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
 
 LAYOUT_LINEAR_F32, LAYOUT_QUAD_F32, LAYOUT_CORNER_F16, LAYOUT_OCT_F32, LAYOUT_BRICK_OCT_F32 = 0, 1, 2, 3, 4
+LAYOUT_TEX3D_F32, LAYOUT_MORTON_OCT_F32 = 5, 6
 LAYOUT_DEFAULT = LAYOUT_OCT_F32
-LAYOUTS = {"linear_f32": 0, "quad_f32": 1, "corner_f16": 2, "oct_f32": 3, "brick_oct_f32": 4}
+LAYOUTS = {"linear_f32": 0, "quad_f32": 1, "corner_f16": 2, "oct_f32": 3, "brick_oct_f32": 4, "tex3d_f32": 5,
+           "morton_oct_f32": 6}
 LIGHTS_EXPLICIT, LIGHTS_GUIDE = 0, 1
 LIGHT_MARCH, LIGHT_TV = 0, 1
 
@@ -104,7 +106,7 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
            "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
-           "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak"]
+           "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak", "nsl_volume_rebuild"]
 
 
 class BakeS(ctypes.Structure):
@@ -133,6 +135,7 @@ def lib():
     L.nsl_volume_upload.argtypes = [P(GridDesc), vp, i32, i32, vp, ctypes.c_size_t, vp, P(vp)]
     L.nsl_volume_check.argtypes = [vp, vp, P(ctypes.c_uint64)]
     L.nsl_volume_release.argtypes = [vp]
+    L.nsl_volume_rebuild.argtypes = [vp, vp, i32, vp]
     L.nsl_guiding_map.argtypes = [vp, P(CameraS), P(LightS), i32, i32, P(MediumS), P(MarchS), u32,
                                   vp, vp, vp, vp]
     L.nsl_guiding_map_batch.argtypes = [P(vp), i32, P(i32), P(CameraS), P(LightS), i32, i32, P(MediumS),
@@ -248,6 +251,22 @@ class Volume:
                                        storage.data_ptr(), storage.numel(), _stream_handle(stream),
                                        ctypes.byref(h)), "nsl_volume_upload")
         self.handle = h
+
+    def rebuild(self, density, stream=None):
+        """Rebuild this volume's layout in place from new density values (nsl_volume_rebuild):
+        same grid, layout, storage (and TEX3D array); plans referencing it see the new values."""
+        import torch
+        on_dev = 1 if (hasattr(density, "is_cuda") and density.is_cuda) else 0
+        if hasattr(density, "data_ptr"):
+            assert density.dtype == torch.float32 and density.is_contiguous()
+            ptr = density.data_ptr()
+        else:
+            import numpy as np
+            assert density.dtype == np.float32 and density.flags["C_CONTIGUOUS"]
+            ptr = density.ctypes.data
+        self._density = density
+        _check(lib().nsl_volume_rebuild(self.handle, ptr, on_dev, _stream_handle(stream)), "nsl_volume_rebuild")
+        return self
 
     def check(self, stream=None) -> int:
         n = ctypes.c_uint64()

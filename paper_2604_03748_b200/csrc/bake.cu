@@ -166,7 +166,6 @@ __global__ void __launch_bounds__(kBakeThreads, NSL_BAKE_MINB) bake_kernel(const
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
     v.mask_words = sp.slab_off;
-    v.zero_e = sp.zero_e;
 
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t gath = 0;
@@ -322,6 +321,8 @@ cudaError_t launch_bake(const FrameParams* fp, const BakeFrame* bf, const BakeCo
         case kCornerF16: return launch_bake_l<kCornerF16>(fp, bf, bc, F, W, H, projection, out, s);
         case kOctF32: return launch_bake_l<kOctF32>(fp, bf, bc, F, W, H, projection, out, s);
         case kBrickOctF32: return launch_bake_l<kBrickOctF32>(fp, bf, bc, F, W, H, projection, out, s);
+        case kTex3dF32: return launch_bake_l<kTex3dF32>(fp, bf, bc, F, W, H, projection, out, s);
+        case kMortonOctF32: return launch_bake_l<kMortonOctF32>(fp, bf, bc, F, W, H, projection, out, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -24,6 +24,15 @@ struct nsl_volume {
     uint32_t* occ;                    // occupancy bitmask inside the storage
     nsl::OccGeom og;
     int32_t* aabb;                    // occupied block bounds in the storage tail
+    // TEX3D only: the library-owned body (QUAD float4 texels) and its texture / surface objects
+    cudaArray_t arr = nullptr;
+    cudaTextureObject_t tex = 0;
+    cudaSurfaceObject_t surf = 0;
+    ~nsl_volume() {
+        if (tex) cudaDestroyTextureObject(tex);
+        if (surf) cudaDestroySurfaceObject(surf);
+        if (arr) cudaFreeArray(arr);
+    }
 };
 
 namespace {
@@ -57,10 +66,6 @@ double norm3(const float v[3]) {
 }
 
 constexpr size_t kTail = 256;  // counter area after the layout (keeps 16-B alignment)
-// In the tail: +0 invalid-value counter, +16 occupied block box, +kZeroElem a 32-B all-zero
-// element (written by occ_finalize_kernel) that the march's branch-free gathers read for
-// samples in empty blocks.
-constexpr size_t kZeroElem = 128;
 
 size_t body_bytes(const nsl_grid_desc* g, int layout) {
     return layout_elems(layout, g->nx, g->ny, g->nz) * layout_elem_bytes(layout);
@@ -90,7 +95,7 @@ nsl_status check_grid(const nsl_grid_desc* g) {
 
 nsl_status check_layout(int layout) {
     if (layout != kLinearF32 && layout != kQuadF32 && layout != kCornerF16 && layout != kOctF32 &&
-        layout != kBrickOctF32)
+        layout != kBrickOctF32 && layout != kTex3dF32 && layout != kMortonOctF32)
         return fail(NSL_ERR_INVALID_ARG, "unknown layout %d", layout);
     return NSL_OK;
 }
@@ -195,7 +200,8 @@ VolDesc desc_of(const nsl_volume* v) {
     d.occ = v->occ;
     d.og = v->og;
     d.aabb = v->aabb;
-    d.zero_e = (int32_t)((tail_offset(&v->g, v->layout) + kZeroElem) / 32);
+    if (v->layout == kTex3dF32) d.data = reinterpret_cast<const void*>((uintptr_t)v->tex);   // kernels: the texture
+    d.surf = v->surf;
     return d;
 }
 
@@ -299,7 +305,7 @@ static nsl_status volume_handle(const nsl_grid_desc* g, int32_t layout, void* de
     if (nsl_status st = check_grid(g)) return st;
     if (nsl_status st = check_layout(layout)) return st;
     if (!device_storage) return fail(NSL_ERR_INVALID_ARG, "NULL storage");
-    const int align = layout == kOctF32 || layout == kBrickOctF32 ? 32 : 16;
+    const int align = layout == kOctF32 || layout == kBrickOctF32 || layout == kMortonOctF32 ? 32 : 16;
     if (reinterpret_cast<uintptr_t>(device_storage) % align)
         return fail(NSL_ERR_INVALID_ARG, "storage must be %d-B aligned", align);
     const size_t need = nsl_volume_bytes(g, layout);
@@ -312,6 +318,30 @@ static nsl_status volume_handle(const nsl_grid_desc* g, int32_t layout, void* de
     v->occ = reinterpret_cast<uint32_t*>(static_cast<char*>(device_storage) + mask_offset(g, layout));
     v->og = occ_geom(g->nx, g->ny, g->nz);
     v->aabb = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(v->invalid) + 16);
+    if (layout == kTex3dF32) {
+        // the body: (nx+1) x (ny+1) x (nz+2) QUAD float4 texels in a 3-D cudaArray (block-linear),
+        // written by the build through a surface, read by the march through a point-sampled,
+        // unnormalised texture (clamp addressing: every fetch is in range by construction)
+        const cudaChannelFormatDesc cd = cudaCreateChannelDesc<float4>();
+        cudaError_t e = cudaMalloc3DArray(&v->arr, &cd, make_cudaExtent(g->nx + 1, g->ny + 1, g->nz + 2),
+                                          cudaArraySurfaceLoadStore);
+        cudaResourceDesc rd;
+        memset(&rd, 0, sizeof rd);
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = v->arr;
+        cudaTextureDesc td;
+        memset(&td, 0, sizeof td);
+        td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        if (e == cudaSuccess) e = cudaCreateTextureObject(&v->tex, &rd, &td, nullptr);
+        if (e == cudaSuccess) e = cudaCreateSurfaceObject(&v->surf, &rd);
+        if (e != cudaSuccess) {
+            delete v;
+            return cuda_fail(e, "TEX3D array / texture");
+        }
+    }
     *out = v;
     return NSL_OK;
 }
@@ -396,6 +426,33 @@ nsl_status nsl_volume_check(const nsl_volume* v, nsl_stream stream, uint64_t* n_
 
 nsl_status nsl_volume_release(nsl_volume* v) {
     delete v;
+    return NSL_OK;
+}
+
+nsl_status nsl_volume_rebuild(nsl_volume* v, const float* density, int32_t density_on_device, nsl_stream stream) {
+    g_err.clear();
+    if (!v || !density) return fail(NSL_ERR_INVALID_ARG, "NULL volume/density");
+    const size_t n = (size_t)v->g.nx * v->g.ny * v->g.nz;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (density_on_device) {
+        NSL_CUDA(enqueue_build(v, density, s), "volume build launch");
+        return NSL_OK;
+    }
+    for (size_t i = 0; i < n; ++i)
+        if (!(density[i] >= 0.0f) || !std::isfinite(density[i]))
+            return fail(NSL_ERR_INVALID_ARG, "density[%zu] = %g is not finite and >= 0", i, (double)density[i]);
+    void* staging = nullptr;
+    NSL_CUDA(pool_malloc(&staging, n * sizeof(float), s), "cudaMallocAsync(staging)");
+    cudaError_t e = cudaMemcpyAsync(staging, density, n * sizeof(float), cudaMemcpyHostToDevice, s);
+    cudaEvent_t copied = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(copied, s);
+    if (e == cudaSuccess) e = enqueue_build(v, static_cast<const float*>(staging), s);
+    cudaError_t e2 = cudaFreeAsync(staging, s);
+    if (e == cudaSuccess && copied) e = cudaEventSynchronize(copied);   // host buffer reusable on return
+    if (copied) cudaEventDestroy(copied);
+    if (e != cudaSuccess) return cuda_fail(e, "volume rebuild");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(staging)");
     return NSL_OK;
 }
 
@@ -1115,7 +1172,6 @@ nsl_status nsl_bench_l1_gather(const nsl_volume* vol, int32_t waves, int32_t rep
     p.occ_nbx = vol->og.nbx;
     p.occ_nby = vol->og.nby;
     p.slab_off = vol->og.words;
-    p.zero_e = desc_of(vol).zero_e;
     NSL_CUDA(launch_l1_gather(p, (int)blocks, reps, sink, reinterpret_cast<cudaStream_t>(stream)),
              "l1_gather_kernel launch");
     *samples = (uint64_t)threads * reps * l1_gather_line();

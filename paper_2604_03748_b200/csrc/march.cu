@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
     v.mask_words = sp.slab_off;
-    v.zero_e = sp.zero_e;
     if (PROJ == 0 && (cflag & (DEBUG || COUNT ? 2 : 1))) {
         if (valid) {                   // the empty map: L = 0, T = 1, D = 0, counters 0
             out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
@@ -469,6 +468,8 @@ cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int
         case kCornerF16: return launch_l<kCornerF16>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
         case kOctF32: return launch_l<kOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
         case kBrickOctF32: return launch_l<kBrickOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
+        case kTex3dF32: return launch_l<kTex3dF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
+        case kMortonOctF32: return launch_l<kMortonOctF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
     }
     return cudaErrorInvalidValue;
 }

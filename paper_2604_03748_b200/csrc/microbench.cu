@@ -100,13 +100,14 @@ cudaError_t launch_l1_gather(const FrameParams& p, int blocks, int reps, float* 
     v.sy1 = p.supp[1];
     v.sz1 = p.supp[2];
     v.mask_words = p.slab_off;
-    v.zero_e = p.zero_e;
     switch (p.layout) {
         case kLinearF32: l1_gather_kernel<kLinearF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
         case kQuadF32: l1_gather_kernel<kQuadF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
         case kCornerF16: l1_gather_kernel<kCornerF16><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
         case kOctF32: l1_gather_kernel<kOctF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
         case kBrickOctF32: l1_gather_kernel<kBrickOctF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
+        case kTex3dF32: l1_gather_kernel<kTex3dF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
+        case kMortonOctF32: l1_gather_kernel<kMortonOctF32><<<blocks, kMbThreads, 0, s>>>(v, reps, sink); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -120,6 +121,8 @@ int l1_gather_max_blocks_per_sm(int layout) {
         case kCornerF16: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, l1_gather_kernel<kCornerF16>, kMbThreads, 0); break;
         case kOctF32: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, l1_gather_kernel<kOctF32>, kMbThreads, 0); break;
         case kBrickOctF32: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, l1_gather_kernel<kBrickOctF32>, kMbThreads, 0); break;
+        case kTex3dF32: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, l1_gather_kernel<kTex3dF32>, kMbThreads, 0); break;
+        case kMortonOctF32: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, l1_gather_kernel<kMortonOctF32>, kMbThreads, 0); break;
     }
     return n;
 }

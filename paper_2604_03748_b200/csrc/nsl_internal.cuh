@@ -35,7 +35,7 @@ struct VolDesc {
     const uint32_t* occ;
     OccGeom og;
     const int32_t* aabb;       // occupied block bounds: bmin xyz, bmax xyz (bmin > bmax: empty volume)
-    int32_t zero_e;            // OCT layouts: element index (from data) of a 32-B all-zero element
+    unsigned long long surf;   // TEX3D: surface object of the library-owned array (the build writes it)
 };
 
 // Raw per-frame input (host -> device, one memcpy per call).
@@ -73,8 +73,7 @@ struct FrameParams {
     float alim[4][3];          // light march exit plane of the occupied box per axis
     int32_t slab_off;          // word offset of the slab boxes in the staged occupancy region
     int32_t lz0;               // bit l: L_g,l,z == 0 exactly (the march of light l stays in its z slab)
-    int32_t zero_e;            // OCT layouts: element index of the all-zero element (VolDesc)
-    int32_t pad2[2];
+    int32_t pad2[3];
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 
@@ -87,6 +86,9 @@ __host__ __device__ inline void layout_strides(int layout, int nx, int ny, int32
     } else if (layout == NSL_LAYOUT_BRICK_OCT_F32) {  // strides in bricks of 4^3 cells
         sy = (nx + 4) / 4;
         sz = ((nx + 4) / 4) * ((ny + 4) / 4);
+    } else if (layout == NSL_LAYOUT_MORTON_OCT_F32) { // strides in tiles of 8^3 cells
+        sy = (nx + 8) / 8;
+        sz = ((nx + 8) / 8) * ((ny + 8) / 8);
     } else {
         sy = nx + 1;
         sz = (nx + 1) * (ny + 1);
@@ -202,6 +204,8 @@ constexpr int kQuadF32 = NSL_LAYOUT_QUAD_F32;
 constexpr int kCornerF16 = NSL_LAYOUT_CORNER_F16;
 constexpr int kOctF32 = NSL_LAYOUT_OCT_F32;
 constexpr int kBrickOctF32 = NSL_LAYOUT_BRICK_OCT_F32;
+constexpr int kTex3dF32 = NSL_LAYOUT_TEX3D_F32;
+constexpr int kMortonOctF32 = NSL_LAYOUT_MORTON_OCT_F32;
 
 // Launch helpers implemented in the .cu files.
 // layout + occupancy + AABB + invalid-voxel count from the raw grid (two launches, no memsets)

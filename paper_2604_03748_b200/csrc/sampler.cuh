@@ -75,7 +75,6 @@ struct Vol {
     int shift, nbx, nby;
     float sx1, sy1, sz1;          // support upper bounds n+1
     int mask_words;               // NSL_CHECK only: occupancy mask words
-    int zero_e;                   // OCT layouts: the all-zero element (branch-free gathers)
 };
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return __fmaf_rn(t, b - a, a); }
@@ -111,7 +110,7 @@ __device__ __forceinline__ float gather_interp(const Vol& v, int e, float fx, fl
         const float x00 = __fmaf_rn(fx, q0.y, q0.x), x10 = __fmaf_rn(fx, q0.w, q0.z);
         const float x01 = __fmaf_rn(fx, q1.y, q1.x), x11 = __fmaf_rn(fx, q1.w, q1.z);
         return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
-    } else if (LAYOUT == kOctF32 || LAYOUT == kBrickOctF32) {
+    } else if (LAYOUT == kOctF32 || LAYOUT == kBrickOctF32 || LAYOUT == kMortonOctF32) {
         // one 256-bit gather: (c000, c100 - c000, c010, c110 - c010 | the same for plane k+1)
         float a0, a1, a2, a3, b0, b1, b2, b3;
 #if NSL_VOL_EVF
@@ -138,31 +137,38 @@ __device__ __forceinline__ float gather_interp(const Vol& v, int e, float fx, fl
     }
 }
 
-// OCT / BRICK_OCT gather issued under a predicate (no branch): an empty sample's load is not
-// issued and its lerps run on whatever the registers hold; the select returns exactly 0.
-template <int LAYOUT>
-__device__ __forceinline__ float gather_interp_pred(const Vol& v, int e, float fx, float fy, float fz, bool occ) {
-    static_assert(LAYOUT == kOctF32 || LAYOUT == kBrickOctF32, "predicated gather: OCT layouts only");
-    float a0, a1, a2, a3, b0, b1, b2, b3;
-    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %9, 0;\n\t"
-        "@p ld.global.nc.L1::evict_first.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
-        : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
-        : "l"(static_cast<const float*>(v.data) + 8 * (size_t)e), "r"((uint32_t)occ));
-    const float x00 = __fmaf_rn(fx, a1, a0), x10 = __fmaf_rn(fx, a3, a2);
-    const float x01 = __fmaf_rn(fx, b1, b0), x11 = __fmaf_rn(fx, b3, b2);
-    const float r = lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
-    return occ ? r : 0.0f;
+// Element index of cell (ix, iy, iz) for the element-addressed layouts (z part zpart, zlow
+// precomputed by zplane for horizontal lines; TEX3D has no element index).
+__device__ __forceinline__ int spread3(int a) {   // bits b2 b1 b0 -> b2 0 0 b1 0 0 b0
+    return (a & 1) | ((a & 2) << 2) | ((a & 4) << 4);
 }
-#ifndef NSL_PRED
-#define NSL_PRED 0
-#endif
-__host__ __device__ constexpr bool kPredOct(int layout) { return NSL_PRED && (layout == kOctF32 || layout == kBrickOctF32); }
-// NSL_ZSEL: branch-free OCT samples -- an empty sample gathers the tail's all-zero element (an L1
-// hit) instead of branching around the gather; its trilinear of zeros is exactly +0.
-#ifndef NSL_ZSEL
-#define NSL_ZSEL 0
-#endif
-__host__ __device__ constexpr bool kZsel(int layout) { return NSL_ZSEL && (layout == kOctF32 || layout == kBrickOctF32); }
+template <int LAYOUT>
+__device__ __forceinline__ int elem_index(const Vol& v, int ix, int iy, int zpart, int zlow) {
+    if (LAYOUT == kBrickOctF32) return ((zpart + (iy >> 2) * v.sy + (ix >> 2)) << 6) | zlow | ((iy & 3) << 2) | (ix & 3);
+    if (LAYOUT == kMortonOctF32) return ((zpart + (iy >> 3) * v.sy + (ix >> 3)) << 9) | zlow | (spread3(iy & 7) << 1) |
+                                        spread3(ix & 7);
+    return ix + iy * v.sy + zpart;
+}
+template <int LAYOUT>
+__device__ __forceinline__ int zpart_of(const Vol& v, int iz) {
+    return LAYOUT == kBrickOctF32 ? (iz >> 2) * v.sz : LAYOUT == kMortonOctF32 ? (iz >> 3) * v.sz : iz * v.sz;
+}
+template <int LAYOUT>
+__device__ __forceinline__ int zlow_of(int iz) {
+    return LAYOUT == kBrickOctF32 ? (iz & 3) << 4 : LAYOUT == kMortonOctF32 ? spread3(iz & 7) << 2 : 0;
+}
+
+// TEX3D: the QUAD float4 of cells (ix, iy, iz) and (ix, iy, iz + 1) by two point-sampled fetches
+// (texel t covers [t, t + 1): the coordinate floor + 0.5 selects it exactly), then QUAD's lerps.
+__device__ __forceinline__ float gather_tex3d(const Vol& v, float flx, float fly, float flz, float fx, float fy,
+                                              float fz) {
+    const cudaTextureObject_t t = (cudaTextureObject_t) reinterpret_cast<uintptr_t>(v.data);
+    const float cx = __fadd_rn(flx, 0.5f), cy = __fadd_rn(fly, 0.5f), cz = __fadd_rn(flz, 0.5f);
+    const float4 q0 = tex3D<float4>(t, cx, cy, cz), q1 = tex3D<float4>(t, cx, cy, __fadd_rn(cz, 1.0f));
+    const float x00 = __fmaf_rn(fx, q0.y, q0.x), x10 = __fmaf_rn(fx, q0.w, q0.z);
+    const float x01 = __fmaf_rn(fx, q1.y, q1.x), x11 = __fmaf_rn(fx, q1.w, q1.z);
+    return lerpf(lerpf(x00, x10, fy), lerpf(x01, x11, fy), fz);
+}
 
 template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z, uint32_t& gathers) {
@@ -174,18 +180,13 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
     NSL_ASSERT(ix >= 0 && iy >= 0 && iz >= 0 && (float)ix < v.sx1 && (float)iy < v.sy1 && (float)iz < v.sz1);
     NSL_ASSERT(b >= 0 && (b >> 5) < v.mask_words);
     const uint32_t word = __ldg(v.occ + (b >> 5));
-    const bool occ = (word >> (b & 31)) & 1u;
-    if (!kPredOct(LAYOUT) && !kZsel(LAYOUT) && !occ) return 0.0f;
-    if (COUNT) gathers += occ;
-    const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias)),
-                fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
-    const int e = LAYOUT == kBrickOctF32
-                      ? (((iz >> 2) * v.sz + (iy >> 2) * v.sy + (ix >> 2)) << 6) | ((iz & 3) << 4) | ((iy & 3) << 2) |
-                            (ix & 3)
-                      : ix + iy * v.sy + iz * v.sz;
-    if constexpr (kZsel(LAYOUT)) return gather_interp<LAYOUT>(v, occ ? e : v.zero_e, fx, fy, fz);
-    if constexpr (kPredOct(LAYOUT)) return gather_interp_pred<LAYOUT>(v, e, fx, fy, fz, occ);
-    else return gather_interp<LAYOUT>(v, e, fx, fy, fz);
+    if (!((word >> (b & 31)) & 1u)) return 0.0f;
+    if (COUNT) ++gathers;
+    const float flx = __fsub_rn(rx, kFloorBias), fly = __fsub_rn(ry, kFloorBias), flz = __fsub_rn(rz, kFloorBias);
+    const float fx = __fsub_rn(x, flx), fy = __fsub_rn(y, fly), fz = __fsub_rn(z, flz);
+    if constexpr (LAYOUT == kTex3dF32) return gather_tex3d(v, flx, fly, flz, fx, fy, fz);
+    else return gather_interp<LAYOUT>(v, elem_index<LAYOUT>(v, ix, iy, zpart_of<LAYOUT>(v, iz), zlow_of<LAYOUT>(iz)),
+                                      fx, fy, fz);
 }
 
 // A horizontal light line (L_z == 0 bit-exactly: every Y_j keeps U_z, since fma(s, 0, u_z) ==
@@ -193,9 +194,9 @@ __device__ __forceinline__ float sample(const Vol& v, float x, float y, float z,
 // instead of per light sample.  sample_hz(v, zp, x, y) == sample(v, x, y, z) bit for bit.
 struct ZPlane {
     int zb;      // (iz >> shift) * nby: the block row base
-    int ze;      // the z part of the element index (BRICK: the brick plane, times sz)
-    int zl;      // BRICK: the z part inside the brick
-    float fz;
+    int ze;      // the z part of the element index (zpart_of)
+    int zl;      // the z bits inside a brick / tile (zlow_of)
+    float flz, fz;
 };
 template <int LAYOUT>
 __device__ __forceinline__ ZPlane zplane(const Vol& v, float z) {
@@ -203,9 +204,10 @@ __device__ __forceinline__ ZPlane zplane(const Vol& v, float z) {
     const int iz = __float_as_int(rz) - 0x4B400000;
     ZPlane p;
     p.zb = (iz >> v.shift) * v.nby;
-    p.ze = LAYOUT == kBrickOctF32 ? (iz >> 2) * v.sz : iz * v.sz;
-    p.zl = LAYOUT == kBrickOctF32 ? (iz & 3) << 4 : 0;
-    p.fz = __fsub_rn(z, __fsub_rn(rz, kFloorBias));
+    p.ze = zpart_of<LAYOUT>(v, iz);
+    p.zl = zlow_of<LAYOUT>(iz);
+    p.flz = __fsub_rn(rz, kFloorBias);
+    p.fz = __fsub_rn(z, p.flz);
     return p;
 }
 template <int LAYOUT, bool COUNT>
@@ -216,16 +218,12 @@ __device__ __forceinline__ float sample_hz(const Vol& v, const ZPlane& zp, float
     NSL_ASSERT(ix >= 0 && iy >= 0 && (float)ix < v.sx1 && (float)iy < v.sy1);
     NSL_ASSERT(b >= 0 && (b >> 5) < v.mask_words);
     const uint32_t word = __ldg(v.occ + (b >> 5));
-    const bool occ = (word >> (b & 31)) & 1u;
-    if (!kPredOct(LAYOUT) && !kZsel(LAYOUT) && !occ) return 0.0f;
-    if (COUNT) gathers += occ;
-    const float fx = __fsub_rn(x, __fsub_rn(rx, kFloorBias)), fy = __fsub_rn(y, __fsub_rn(ry, kFloorBias));
-    const int e = LAYOUT == kBrickOctF32
-                      ? ((zp.ze + (iy >> 2) * v.sy + (ix >> 2)) << 6) | zp.zl | ((iy & 3) << 2) | (ix & 3)
-                      : ix + iy * v.sy + zp.ze;
-    if constexpr (kZsel(LAYOUT)) return gather_interp<LAYOUT>(v, occ ? e : v.zero_e, fx, fy, zp.fz);
-    if constexpr (kPredOct(LAYOUT)) return gather_interp_pred<LAYOUT>(v, e, fx, fy, zp.fz, occ);
-    else return gather_interp<LAYOUT>(v, e, fx, fy, zp.fz);
+    if (!((word >> (b & 31)) & 1u)) return 0.0f;
+    if (COUNT) ++gathers;
+    const float flx = __fsub_rn(rx, kFloorBias), fly = __fsub_rn(ry, kFloorBias);
+    const float fx = __fsub_rn(x, flx), fy = __fsub_rn(y, fly);
+    if constexpr (LAYOUT == kTex3dF32) return gather_tex3d(v, flx, fly, zp.flz, fx, fy, zp.fz);
+    else return gather_interp<LAYOUT>(v, elem_index<LAYOUT>(v, ix, iy, zp.ze, zp.zl), fx, fy, zp.fz);
 }
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t h) {

@@ -68,14 +68,13 @@ __global__ void __launch_bounds__(32 * kSetupWarps) frame_setup_kernel(const Fra
         p.H = cam.height;
         p.frame_id = fr.frame_id;
         p.occ = fr.vol.occ;
-        p.zero_e = fr.vol.zero_e;
         p.occ_shift = fr.vol.og.shift;
         p.occ_nbx = fr.vol.og.nbx;
         p.occ_nby = fr.vol.og.nby;
         p.occ_words = fr.vol.og.words_total;   // mask + slab boxes
         p.slab_off = fr.vol.og.words;
         p.occ_nbz = fr.vol.og.nbz;
-        p.pad2[0] = p.pad2[1] = 0;
+        p.pad2[0] = p.pad2[1] = p.pad2[2] = 0;
     }
 
     // ---- camera basis (C3), every lane

@@ -138,7 +138,6 @@ __global__ void __launch_bounds__(128) tv_sweep_kernel(const FrameParams* __rest
     v.sy1 = sp.supp[1];
     v.sz1 = sp.supp[2];
     v.mask_words = sp.slab_off;
-    v.zero_e = sp.zero_e;
     const float af = t.a0 + (float)i, bf = t.b0 + (float)j;
     float base[3];
 #pragma unroll
@@ -224,6 +223,8 @@ cudaError_t launch_tv_sweep(const FrameParams* fps, const TvParams* tvp, int F, 
         case kCornerF16: tv_sweep_kernel<kCornerF16><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
         case kOctF32: tv_sweep_kernel<kOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
         case kBrickOctF32: tv_sweep_kernel<kBrickOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
+        case kTex3dF32: tv_sweep_kernel<kTex3dF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
+        case kMortonOctF32: tv_sweep_kernel<kMortonOctF32><<<grid, 128, smem, s>>>(fps, tvp, slots, Astr, Kstr, slot_elems, smem_k, buf); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -20,6 +20,8 @@ size_t layout_elems(int layout, int nx, int ny, int nz) {
         case kCornerF16: return (size_t)(nx + 1) * (ny + 1) * (nz + 1);
         case kOctF32: return (size_t)(nx + 1) * (ny + 1) * (nz + 1);
         case kBrickOctF32: return (size_t)((nx + 4) / 4) * ((ny + 4) / 4) * ((nz + 4) / 4) * 64;
+        case kMortonOctF32: return (size_t)((nx + 8) / 8) * ((ny + 8) / 8) * ((nz + 8) / 8) * 512;
+        case kTex3dF32: return 0;      // the body lives in the library-owned cudaArray
     }
     return 0;
 }
@@ -31,6 +33,8 @@ size_t layout_elem_bytes(int layout) {
         case kCornerF16: return 16;
         case kOctF32: return 32;
         case kBrickOctF32: return 32;
+        case kMortonOctF32: return 32;
+        case kTex3dF32: return 16;
     }
     return 0;
 }
@@ -186,6 +190,46 @@ __device__ __forceinline__ void layout_brick_oct_cta(const Raw& r, float* __rest
     st256(out + 8 * e, c);
 }
 
+// MORTON_OCT: element e = tile * 512 + morton(i & 7, j & 7, k & 7) (bit b of the x offset at bit
+// 3b, y at 3b + 1, z at 3b + 2), tile = ((k >> 3) nty + (j >> 3)) ntx + (i >> 3); one thread per
+// element, cells beyond (n_x, n_y, n_z) in the last tiles hold zeros (never sampled).
+__device__ __forceinline__ void layout_morton_oct_cta(const Raw& r, float* __restrict__ out, int pb) {
+    const int ntx = (r.nx + 8) / 8, nty = (r.ny + 8) / 8, ntz = (r.nz + 8) / 8;
+    const int64_t e = (int64_t)pb * 256 + threadIdx.x;
+    if (e >= (int64_t)ntx * nty * ntz * 512) return;
+    const int m = (int)(e & 511);
+    const int64_t t = e >> 9;
+    const int tx = (int)(t % ntx), ty = (int)((t / ntx) % nty), tz = (int)(t / ((int64_t)ntx * nty));
+    const int ox = (m & 1) | ((m >> 2) & 2) | ((m >> 4) & 4);
+    const int oy = ((m >> 1) & 1) | ((m >> 3) & 2) | ((m >> 5) & 4);
+    const int oz = ((m >> 2) & 1) | ((m >> 4) & 2) | ((m >> 6) & 4);
+    const int i = tx * 8 + ox, j = ty * 8 + oy, k = tz * 8 + oz;
+    float c[8];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const float c0 = r.at(i, j, k + q), c1 = r.at(i + 1, j, k + q);
+        const float c2 = r.at(i, j + 1, k + q), c3 = r.at(i + 1, j + 1, k + q);
+        c[4 * q + 0] = c0;
+        c[4 * q + 1] = __fsub_rn(c1, c0);
+        c[4 * q + 2] = c2;
+        c[4 * q + 3] = __fsub_rn(c3, c2);
+    }
+    st256(out + 8 * e, c);
+}
+
+// TEX3D: the QUAD float4 of padded cell (i, j, k) written through the array's surface object
+// (texel (i, j, k); x in bytes), one thread per cell of a z-plane, planes k = kb, kb + kstep, ...
+__device__ __forceinline__ void layout_tex3d_cta(const Raw& r, cudaSurfaceObject_t surf, int pb, int kb, int kstep) {
+    const int qx = r.nx + 1, qy = r.ny + 1, plane = qx * qy;
+    const int e2 = pb * 256 + threadIdx.x;
+    if (e2 >= plane) return;
+    const int i = e2 % qx, j = e2 / qx;
+    for (int k = kb; k < r.nz + 2; k += kstep) {
+        const float c0 = r.at(i, j, k), c1 = r.at(i + 1, j, k), c2 = r.at(i, j + 1, k), c3 = r.at(i + 1, j + 1, k);
+        surf3Dwrite(make_float4(c0, __fsub_rn(c1, c0), c2, __fsub_rn(c3, c2)), surf, i * (int)sizeof(float4), j, k);
+    }
+}
+
 // ---------------------------------------------------------------- occupancy role
 // Block (bx, by, bz) is non-empty iff some padded voxel in [b*B, b*B + B]^3 (the corners of
 // its cells) is nonzero; voxel i is a corner of the cells i-1 and i, i.e. of the blocks
@@ -313,6 +357,9 @@ __global__ void __launch_bounds__(256, 6) volume_build_kernel(Raw r, void* __res
     if (LAYOUT == kCornerF16) layout_corner_f16_cta(r, static_cast<uint4*>(out), pb, kb, kstep);
     if (LAYOUT == kOctF32) layout_oct_cta(r, static_cast<float*>(out), pb, kb, kstep);
     if (LAYOUT == kBrickOctF32) layout_brick_oct_cta(r, static_cast<float*>(out), pb);
+    if (LAYOUT == kMortonOctF32) layout_morton_oct_cta(r, static_cast<float*>(out), pb);
+    if (LAYOUT == kTex3dF32)             // `out` carries the array's surface object
+        layout_tex3d_cta(r, (cudaSurfaceObject_t)reinterpret_cast<uintptr_t>(out), pb, kb, kstep);
 }
 
 // The occupancy region [mask: words][slab_min: nbz x (bx, by)][slab_max: nbz x (bx, by)], the
@@ -383,8 +430,6 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
     __syncthreads();
     if (threadIdx.x < 6) aabb[threadIdx.x] = am[threadIdx.x];
     if (threadIdx.x == 0) *invalid = nbad;
-    // the all-zero element of the tail (capi.cu kZeroElem = tail + 128 B), read by branch-free gathers
-    if (threadIdx.x < 8) reinterpret_cast<float*>(reinterpret_cast<char*>(invalid) + 128)[threadIdx.x] = 0.0f;
 }
 
 }  // namespace
@@ -434,13 +479,13 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
     Raw r{raw, v.nx, v.ny, v.nz};
     const int plane = v.layout == kLinearF32 ? (v.nx + 2) * (v.ny + 2) : (v.nx + 1) * (v.ny + 1);
     const int planes = v.layout == kCornerF16 || v.layout == kOctF32 ? v.nz + 1 : v.nz + 2;
-    const int plane_blocks = v.layout == kBrickOctF32
-                                 ? (int)((layout_elems(kBrickOctF32, v.nx, v.ny, v.nz) + 255) / 256)
-                                 : (plane + 255) / 256;
-    int kstep = v.layout == kQuadF32       ? (planes + kQuadPlanes - 1) / kQuadPlanes
-                : v.layout == kOctF32      ? (planes + kOctRun - 1) / kOctRun
-                : v.layout == kBrickOctF32 ? 1
-                                           : planes;
+    const bool per_elem = v.layout == kBrickOctF32 || v.layout == kMortonOctF32;   // one thread per element
+    const int plane_blocks = per_elem ? (int)((layout_elems(v.layout, v.nx, v.ny, v.nz) + 255) / 256)
+                                      : (plane + 255) / 256;
+    int kstep = v.layout == kQuadF32  ? (planes + kQuadPlanes - 1) / kQuadPlanes
+                : v.layout == kOctF32 ? (planes + kOctRun - 1) / kOctRun
+                : per_elem            ? 1
+                                      : planes;
     const long max_layout_ctas = 2000000000L - v.og.rows;
     if ((long)plane_blocks * kstep > max_layout_ctas) kstep = (int)(max_layout_ctas / plane_blocks);
     const unsigned grid = (unsigned)(v.og.rows + (long)plane_blocks * kstep);
@@ -466,6 +511,14 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
         case kBrickOctF32:
             volume_build_kernel<kBrickOctF32><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks, kstep,
                                                                           occ_stride);
+            break;
+        case kMortonOctF32:
+            volume_build_kernel<kMortonOctF32><<<grid, 256, smem, s>>>(r, storage, v.og, scratch, plane_blocks,
+                                                                           kstep, occ_stride);
+            break;
+        case kTex3dF32:
+            volume_build_kernel<kTex3dF32><<<grid, 256, smem, s>>>(
+                r, reinterpret_cast<void*>((uintptr_t)v.surf), v.og, scratch, plane_blocks, kstep, occ_stride);
             break;
         default:
             return cudaErrorInvalidValue;

@@ -59,7 +59,7 @@ def test_bake_parity_C2_subsampled_and_layouts(nsl):
     pix = np.arange(0, 512 * 512, 61)
     ref = [oracle.sixway_bake(w.grid, w.volume(0), w.cameras[f], w.medium, b, frame_id=w.frame_ids[f],
                               pixels=pix)["out"] for f in range(2)]
-    for layout in (0, 1, 3):
+    for layout in (0, 1, 3, 5, 6):
         g = bake_gpu(nsl, w, b, layout)
         for f in range(2):
             check(g[f][pix], ref[f], f"C2 f{f} layout {layout}")

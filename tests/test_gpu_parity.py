@@ -113,7 +113,7 @@ def test_jitter_matches_golden_and_oracle(nsl):
 
 
 # ------------------------------------------------------------------ C1 full frames
-@pytest.mark.parametrize("layout", [0, 1, 3])
+@pytest.mark.parametrize("layout", [0, 1, 3, 5, 6])
 @pytest.mark.parametrize("kw", [{}, {"single_light": True}, {"perspective": True},
                                 {"perspective": True, "single_light": True}])
 def test_parity_C1(nsl, layout, kw):
@@ -142,9 +142,11 @@ def test_parity_C1_corner_f16(nsl):
 
 
 def test_layouts_agree_bitwise(nsl):
+    """Every fp32 layout (LINEAR, QUAD, OCT, BRICK_OCT, TEX3D, MORTON_OCT) stores the input values
+    and x-differences exactly, so the march gives bit-identical maps and counters."""
     w = I.make_workload("C2", frames=[3])
     a = run(nsl, w, layout=0)
-    for lay in (1, 3, 4):
+    for lay in (1, 3, 4, 5, 6):
         b = run(nsl, w, layout=lay)
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
@@ -286,6 +288,32 @@ def test_host_api_equals_device_api(nsl, frames, layout):
                          hr, hd)
     assert np.array_equal(hr.numpy(), dev[0])
     assert np.array_equal(hd.numpy(), dev[1])
+
+
+def test_volume_rebuild_in_place(nsl):
+    """nsl_volume_rebuild refills a volume slot (storage, TEX3D array) with new density; a plan
+    created on the slot marches the new values (== a fresh upload + batch), for every layout."""
+    import torch
+    w = I.make_workload("C4", frames=[0, 1])
+    wa, wb = w.subset([0]), w.subset([1])
+    ref_b = run(nsl, wb, layout=3, debug=False)
+    for lay in (3, 4, 5, 6):
+        vol = nsl.Volume(w.grid, torch.from_numpy(wa.volume(0)).cuda(), lay)
+        plan = nsl.Plan([vol], [0], wb.cameras, wb.lights, wb.light_mode, wb.medium, wb.march, wb.frame_ids)
+        vol.rebuild(torch.from_numpy(wb.volume(0)).cuda())          # device density
+        outs = nsl.alloc_outputs(1, w.height, w.width)
+        plan.execute(outs[0], outs[1])
+        torch.cuda.synchronize()
+        assert np.array_equal(outs[0].cpu().numpy(), ref_b[0]) and np.array_equal(outs[1].cpu().numpy(), ref_b[1])
+        vol.rebuild(wa.volume(0))                                    # host density: back to frame 0
+        vol.rebuild(wb.volume(0))
+        plan.execute(outs[0], outs[1])
+        torch.cuda.synchronize()
+        assert np.array_equal(outs[0].cpu().numpy(), ref_b[0])
+    bad = wb.volume(0).copy()
+    bad[3, 4, 5] = np.nan
+    with pytest.raises(nsl.NslError):
+        vol.rebuild(bad)
 
 
 def test_host_api_rejects_invalid_density(nsl):

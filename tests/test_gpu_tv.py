@@ -71,7 +71,7 @@ def test_tv_differs_from_march_only_in_light_transmittance(nsl):
     assert 0 < d.max() < 0.1 * np.abs(a[0][..., :3]).max()
 
 
-@pytest.mark.parametrize("layout", [1, 3])
+@pytest.mark.parametrize("layout", [1, 3, 5, 6])
 def test_tv_parity_C2_subsampled(nsl, layout):
     w = tv(I.make_workload("C2", frames=[0, 21, 40]))
     g, gd, gdbg = run(nsl, w, layout=layout)
