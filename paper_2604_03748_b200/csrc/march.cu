@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
         }
         r.h = mc.h;
         const uint32_t pix = (uint32_t)py * (uint32_t)W + (uint32_t)px;
-        r.delta = mc.jitter ? jitter_delta(jitter_hash(mc.seed_lo, mc.seed_hi, sp.frame_id, pix), mc.h) : 0.0f;
+        r.delta = mc.jitter ? jitter_delta(fmix32(sp.jh ^ pix), mc.h) : 0.0f;   // C4 (per-frame prefix sp.jh)
 
         // ---- C5: the steps actually marched are the in-support steps of [1, N] whose
         //      positions lie in the occupied box (every other sample is exactly 0).
@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
                 // kernel variant (FAST, DEBUG, COUNTED; any light set) takes the same decisions
                 const float sig_t = __fmul_rn(mc.kappa, rho);
                 const float sig_s = __fmul_rn(mc.alpha, sig_t);
-                if (n_hit == 0 && sig_s > mc.tau_d) {   // C6
+                // C6 (t_n >= h > 0, so D == 0 <=> no hit yet: the FAST kernels keep no n_hit)
+                if ((DEBUG ? n_hit == 0 : Dout == 0.0f) && sig_s > mc.tau_d) {
                     n_hit = n;
                     Dout = t;
                 }
@@ -353,11 +354,13 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
                 L2 += sp.rgb[l][2] * w;
             }
         }
-        out_rgbt[o] = make_float4(L0, L1, L2, T);
-        out_depth[o] = Dout;
+        // the output offset again (cheaper than keeping it live through the march)
+        const size_t oo = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
+        out_rgbt[oo] = make_float4(L0, L1, L2, T);
+        out_depth[oo] = Dout;
         const bool hit_support = n_lo > 0 && n_hi >= n_lo;
         if (DEBUG) {
-            uint32_t* dbg = out_debug + o * 6;
+            uint32_t* dbg = out_debug + oo * 6;
             dbg[0] = hit_support ? (uint32_t)n_lo : 0u;
             dbg[1] = hit_support ? (uint32_t)n_hi : 0u;
             dbg[2] = (uint32_t)n_hit;

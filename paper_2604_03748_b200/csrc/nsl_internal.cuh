@@ -73,7 +73,8 @@ struct FrameParams {
     float alim[4][3];          // light march exit plane of the occupied box per axis
     int32_t slab_off;          // word offset of the slab boxes in the staged occupancy region
     int32_t lz0;               // bit l: L_g,l,z == 0 exactly (the march of light l stays in its z slab)
-    int32_t pad2[3];
+    uint32_t jh;               // C4: the per-frame prefix of the jitter chain, fmix32^3 of (seed, frame)
+    int32_t pad2[2];
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 

@@ -74,7 +74,18 @@ __global__ void __launch_bounds__(32 * kSetupWarps) frame_setup_kernel(const Fra
         p.occ_words = fr.vol.og.words_total;   // mask + slab boxes
         p.slab_off = fr.vol.og.words;
         p.occ_nbz = fr.vol.og.nbz;
-        p.pad2[0] = p.pad2[1] = p.pad2[2] = 0;
+        p.pad2[0] = p.pad2[1] = 0;
+        // C4: h32 = fmix32(jh ^ pixel) with jh = fmix32(fmix32(fmix32(lo32(seed) ^ 0x9E3779B9) ^
+        // hi32(seed)) ^ frame_id): the first three rounds depend on the frame only
+        auto fmix = [](uint32_t h) {
+            h ^= h >> 16;
+            h *= 0x85ebca6bu;
+            h ^= h >> 13;
+            h *= 0xc2b2ae35u;
+            h ^= h >> 16;
+            return h;
+        };
+        p.jh = fmix(fmix(fmix(mc.seed_lo ^ 0x9E3779B9u) ^ mc.seed_hi) ^ fr.frame_id);
     }
 
     // ---- camera basis (C3), every lane
