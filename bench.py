@@ -242,10 +242,13 @@ def sampler_ceiling(layout, counts, march_s):
 def l1_patterns(w, nsl):
     """Lane element offsets [16, 32] for the hardware L1/TEX ceiling (nsl_bench_l1_peak), all in
     the OCT layout of w's grid (one 32-B element per trilinear sample):
-      footprint: the march's own gathers for one warp -- 8 x 4 pixels at the image centre of
-        frame 0, patterns 0-7 at 8 consecutive primary steps through the volume centre, 8-15 at
-        light steps 1..8 of the guide set's first side light (else the only light) from the
-        middle sample;
+      footprint: the march's warp footprint -- the 8 x 4 pixels at the image centre of frame 0,
+        every lane at the same ray parameter, patterns 0-7 at 8 consecutive primary steps
+        through the volume centre, 8-15 at light steps 1..8 of the guide set's first side light
+        (else the only light) from the middle sample (the roofline's peak: the larger, stricter
+        denominator);
+      footprint_jitter: the same with each lane at its own C4 jitter (t = delta_lane + n h),
+        i.e. the march's actual gathers: ~19-22 distinct 128-B lines per warp load;
       coalesced: 32 consecutive elements per pattern (8 distinct 128-B lines per load);
       broadcast: one element for every lane."""
     g = w.grid
@@ -261,23 +264,31 @@ def l1_patterns(w, nsl):
     hidx = w.march.step / g.voxel_width                                   # h in index units
     dlen = np.linalg.norm(Dg)
     tc = float(np.dot(centre - O[0], Dg) / dlen ** 2)                     # ray parameter at the centre
-    pos = []
-    for k in range(8):
-        pos.append(O + (tc + (k - 4) * hidx / dlen) * Dg[None, :])
+    h = w.march.step
+    tc = h * round(tc / h)
+    import torch
+    hh = torch.empty(W * H, dtype=torch.int32, device="cuda")
+    dd = torch.empty(W * H, dtype=torch.float32, device="cuda")
+    nsl.debug_jitter(w.march, w.frame_ids[0], hh, dd)                     # C4 delta of every pixel
+    delta = dd.cpu().numpy().astype(np.float64)[py * W + px]
     li = 1 if len(fc["Lg"]) > 1 else 0                                    # a side light, else the only light
-    L = np.asarray(fc["Lg"][li], np.float64) * w.march.step              # one light step (index units)
-    for j in range(1, 9):
-        pos.append(pos[4] + j * L[None, :])
+    L = np.asarray(fc["Lg"][li], np.float64) * h                          # one light step (index units)
     lim = np.array([g.nx, g.ny, g.nz], np.float64)
-    e = []
-    for u in pos:
-        c = np.clip(np.floor(u), 0, lim).astype(np.int64)
-        e.append(c[:, 0] + c[:, 1] * sy + c[:, 2] * sz)
-    e = np.stack(e)
-    foot = e - e.min()
+
+    def offsets(dl):
+        pos = [O + (tc + (k - 4) * h + dl)[:, None] * Dg[None, :] for k in range(8)]
+        pos += [pos[4] + j * L[None, :] for j in range(1, 9)]
+        e = []
+        for u in pos:
+            c = np.clip(np.floor(u), 0, lim).astype(np.int64)
+            e.append(c[:, 0] + c[:, 1] * sy + c[:, 2] * sz)
+        e = np.stack(e)
+        return e - e.min()
+
     coal = np.arange(16)[:, None] * 32 + lane[None, :]
     bcast = np.zeros((16, 32), np.int64)
-    return {"footprint": foot, "coalesced": coal, "broadcast": bcast}
+    return {"footprint": offsets(np.zeros(32)), "footprint_jitter": offsets(delta), "coalesced": coal,
+            "broadcast": bcast}
 
 
 def l1_hw_ceiling(w, nsl, patterns=("footprint",), stride=0, span=1, reps=256, waves=8, iters=7):
@@ -587,7 +598,7 @@ def main():
     alg_bytes = counts["canonical_samples"] * 32
     l1_achieved = alg_bytes / march_s / 1e9
     try:
-        hw = l1_hw_ceiling(w, nsl, patterns=("footprint", "coalesced"))
+        hw = l1_hw_ceiling(w, nsl, patterns=("footprint", "footprint_jitter", "coalesced"))
         l1_peak = hw["footprint"]["lane_gbs"]
         peak_src = ("measured: nsl_bench_l1_peak, ld.global.nc.v8.f32 at the march's 8x4 warp footprint "
                     "(C2 frame 0 geometry), L1-resident, this run")
@@ -613,6 +624,14 @@ def main():
             "kernel_ms": march_s * 1e3, "algorithmic_bytes_per_launch": alg_bytes,
             "canonical_samples_per_launch": counts["canonical_samples"],
             "l1_ceiling": hw,
+            "jitter_footprint_view": ({
+                "peak_gbs": hw["footprint_jitter"]["lane_gbs"],
+                "frac_algorithmic": l1_achieved / hw["footprint_jitter"]["lane_gbs"],
+                "frac_executed_gathers": counts["gathers"] * bytes_per_sample / march_s / 1e9
+                                         / hw["footprint_jitter"]["lane_gbs"],
+                "note": "ceiling of the march's actual jittered lane addresses (C4): the L1 delivers about one "
+                        "128-B line per cycle, so ~19 lines per warp gather halve the rate"}
+                if "footprint_jitter" in hw else None),
             "fp32_view": {"achieved_gflops": flops / march_s / 1e9, "peak_gflops": fp32_peak,
                           "frac": flops / march_s / 1e9 / fp32_peak,
                           "per_unit": "25 flops per canonical sample (SURVEY 8(d), lerp = 2); peak 148 x 128 "

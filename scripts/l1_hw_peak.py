@@ -1,6 +1,6 @@
 """Hardware L1/TEX gather ceiling (nsl_bench_l1_peak; DESIGN.md §7 roofline): lane bytes/s of
-ld.global.nc.v8.f32 loads with no sampler arithmetic, for the march's own warp footprint
-(C2 frame 0), fully coalesced lanes and a broadcast, L1-resident (stride 0) and streamed
+ld.global.nc.v8.f32 loads with no sampler arithmetic, for the march's warp footprint (frame 0
+of the config; without and with the per-lane C4 jitter), fully coalesced lanes and a broadcast, L1-resident (stride 0) and streamed
 through L2 (the same lane pattern shifted by `--l2-stride` elements per repetition over a
 64 MB span).
 
@@ -26,11 +26,11 @@ if __name__ == "__main__":
     w = I.make_workload(a.config, frames=[0])
     import torch
     torch.cuda.set_device(0)
-    res = bench.l1_hw_ceiling(w, nsl, patterns=("footprint", "coalesced", "broadcast"), reps=a.reps, waves=a.waves)
+    res = bench.l1_hw_ceiling(w, nsl, patterns=("footprint", "footprint_jitter", "coalesced", "broadcast"), reps=a.reps, waves=a.waves)
     for k, v in res.items():
         print(json.dumps({"pattern": k, "source": "L1 (stride 0)", **v}), flush=True)
     span = (64 << 20) // 32
-    res = bench.l1_hw_ceiling(w, nsl, patterns=("footprint", "coalesced"), stride=a.l2_stride, span=span,
+    res = bench.l1_hw_ceiling(w, nsl, patterns=("footprint", "footprint_jitter", "coalesced"), stride=a.l2_stride, span=span,
                               reps=a.reps, waves=a.waves)
     for k, v in res.items():
         print(json.dumps({"pattern": k, "source": f"L2 (stride {a.l2_stride} x 32 B over 64 MB)", **v}), flush=True)
