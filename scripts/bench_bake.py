@@ -51,22 +51,17 @@ line = {"metric": "six-way bake pixel-samples/s (NEXT-1)", "value": px_samples /
         "ms_per_frame": 1e3 * t / w.n_frames, "frames": w.n_frames, "spp": a.spp, "map": "512x512",
         "grid": "128^3 plume (C2)", "gathers_per_s": gathers / t, "gathers_per_launch": gathers,
         "l1tex_gather_gbs": gathers * 32 / t / 1e9, "steps": a.steps}
-# roofline as for the march (bench.py): 25 FP32/INT ops per executed (occupied) sample -- a lower
-# bound on the algorithmic work, empty-block samples are not counted -- against 148 SMs x 128
-# lanes x the max SM clock; the L1 view: 32 B per gather against 148 x 128 B/clk
-clk = 1965
-try:
-    import pynvml
-    pynvml.nvmlInit()
-    clk = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(0), pynvml.NVML_CLOCK_SM)
-except Exception:
-    pass
-peak = 148 * 128 * clk * 1e6
-line["roofline"] = {"bound": "alu", "achieved": gathers * 25 / t / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
-                    "frac": gathers * 25 / t / peak, "traffic": None,
-                    "per_unit": "25 ops per executed gather (occupied light/primary sample)",
-                    "l1tex_view": {"achieved_gbs": gathers * 32 / t / 1e9, "peak_gbs": peak / 1e9,
-                                   "frac": gathers * 32 / t / peak}}
+# roofline: the bake's lanes (16 sub-pixel-jittered samples of one pixel) gather
+# near-coalesced, so its L1/TEX ceiling is the measured coalesced rate of nsl_bench_l1_peak (32-B
+# elements, L1-resident); achieved = the executed gathers x 32 B per second (a lower bound on
+# the algorithmic bytes: empty-block samples are not counted)
+import bench as _bench  # noqa: E402
+hw = _bench.l1_hw_ceiling(I.make_workload("C2", frames=[0]), nsl, patterns=("coalesced",))
+peak = hw["coalesced"]["lane_gbs"]
+line["roofline"] = {"bound": "l1tex", "achieved": gathers * 32 / t / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": gathers * 32 / t / 1e9 / peak, "traffic": None,
+                    "per_unit": "32 B per executed trilinear gather (occupied primary or light sample)",
+                    "peak_source": "measured: nsl_bench_l1_peak, coalesced 32-B lanes, L1-resident, this run"}
 if not a.no_oracle:
     import oracle
     pix = np.arange(0, 512 * 512, 509)
