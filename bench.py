@@ -692,6 +692,28 @@ def main():
                            "h2d_bytes_per_step": int(hd.numel() * 4 + F * (40 + 24 * w.n_lights + 8)),
                            "d2h_bytes_per_step": int(hr.numel() * 4 + hdep.numel() * 4),
                            "ms_per_step": 1e3 * te / ke, "api": "nsl_guiding_map_host"}
+            # the compact download (nsl_guiding_map_host_f16: fp16 maps, 10 B/pixel; not the parity path)
+            hr16 = torch.empty((F, H, W, 4), dtype=torch.float16).pin_memory()
+            hd16 = torch.empty((F, H, W), dtype=torch.float16).pin_memory()
+            nsl.guiding_map_host_f16(w.grid, hd, layout, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                                     w.frame_ids, hr16, hd16)
+            torch.cuda.synchronize()
+            es.record(stream)
+            for _ in range(ke):
+                nsl.guiding_map_host_f16(w.grid, hd, layout, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                                         w.frame_ids, hr16, hd16)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            te16 = es.elapsed_time(ee) / 1e3
+            if world > 1:
+                t = torch.tensor([te16], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                te16 = float(t.item())
+            line["e2e_f16"] = {"value": W * H * F * world * ke / te16, "unit": "rays/s",
+                               "h2d_bytes_per_step": int(hd.numel() * 4 + F * (40 + 24 * w.n_lights + 8)),
+                               "d2h_bytes_per_step": int(hr16.numel() * 2 + hd16.numel() * 2),
+                               "ms_per_step": 1e3 * te16 / ke, "api": "nsl_guiding_map_host_f16",
+                               "note": "fp16 (RNE) download of the fp32 maps; not the 1e-4 parity path"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res = time_oracle(cfg, args.cpu_seconds)

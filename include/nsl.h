@@ -317,6 +317,16 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
                                 int32_t light_mode, const nsl_medium* med, const nsl_march* m,
                                 const uint32_t* frame_ids, int32_t F,
                                 float* host_rgbt, float* host_depth, nsl_stream stream);
+/* The same with a compact download: the fp32 maps are rounded to IEEE binary16 (RNE) on the
+ * device and host_rgbt_h (F*H*W*4 halves) / host_depth_h (F*H*W halves) receive 10 B per
+ * pixel instead of 20 -- half the PCIe traffic that bounds the host call.  The march and its
+ * fp32 results are unchanged; only the delivered values are rounded (relative error <= 2^-11,
+ * so this output is NOT the 1e-4 parity path: use nsl_guiding_map_host for that). */
+nsl_status nsl_guiding_map_host_f16(const nsl_grid_desc* g, const float* host_density, int32_t layout,
+                                    const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
+                                    int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                                    const uint32_t* frame_ids, int32_t F, uint16_t* host_rgbt_h,
+                                    uint16_t* host_depth_h, nsl_stream stream);
 
 /* Animated volumes (SURVEY §8(a) rows a1 + a9, config C4; the simulator's
  * density is "streamed directly into the guiding map generation", one grid per frame).

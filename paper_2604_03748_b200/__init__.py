@@ -106,7 +106,8 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_plan_create", "nsl_plan_execute", "nsl_plan_destroy",
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
            "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
-           "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak", "nsl_volume_rebuild"]
+           "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak", "nsl_volume_rebuild",
+           "nsl_guiding_map_host_f16"]
 
 
 class BakeS(ctypes.Structure):
@@ -148,6 +149,7 @@ def lib():
     L.nsl_plan_destroy.argtypes = [vp]
     L.nsl_guiding_map_host.argtypes = [P(GridDesc), vp, i32, P(CameraS), P(LightS), i32, i32, P(MediumS),
                                        P(MarchS), P(u32), i32, vp, vp, vp]
+    L.nsl_guiding_map_host_f16.argtypes = L.nsl_guiding_map_host.argtypes
     L.nsl_guiding_map_animated.argtypes = [P(GridDesc), P(vp), i32, P(vp), ctypes.c_size_t, P(CameraS), P(LightS),
                                            i32, i32, P(MediumS), P(MarchS), P(u32), i32, i32, vp, vp,
                                            P(ctypes.c_uint64), vp]
@@ -474,6 +476,22 @@ def guiding_map_host(grid, host_density, layout, cams, lights, light_mode, mediu
                                       lights_s(lights), len(lights[0]), light_mode, ctypes.byref(medium_s(medium)),
                                       ctypes.byref(march_s(march)), fid, F, host_rgbt.data_ptr(),
                                       host_depth.data_ptr(), _stream_handle(stream)), "nsl_guiding_map_host")
+
+
+def guiding_map_host_f16(grid, host_density, layout, cams, lights, light_mode, medium, march, frame_ids,
+                         host_rgbt_h, host_depth_h, stream=None):
+    """guiding_map_host with the compact download (nsl_guiding_map_host_f16): host_rgbt_h /
+    host_depth_h are torch.float16 CPU tensors [F,H,W,4] / [F,H,W] (the fp32 maps rounded RNE)."""
+    import torch
+    assert host_rgbt_h.dtype == torch.float16 and host_depth_h.dtype == torch.float16
+    F = len(cams)
+    cs = (CameraS * F)(*[camera_s(c) for c in cams])
+    fid = (ctypes.c_uint32 * F)(*[int(x) & 0xFFFFFFFF for x in frame_ids])
+    _check(lib().nsl_guiding_map_host_f16(ctypes.byref(grid_desc(grid)), host_density.data_ptr(), layout, cs,
+                                          lights_s(lights), len(lights[0]), light_mode,
+                                          ctypes.byref(medium_s(medium)), ctypes.byref(march_s(march)), fid, F,
+                                          host_rgbt_h.data_ptr(), host_depth_h.data_ptr(), _stream_handle(stream)),
+           "nsl_guiding_map_host_f16")
 
 
 class Animated:

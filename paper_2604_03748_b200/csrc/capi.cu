@@ -644,10 +644,11 @@ nsl_status nsl_guiding_map(const nsl_volume* vol, const nsl_camera* cam, const n
                                  out_depth, out_debug, stream);
 }
 
-nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_density, int32_t layout,
-                                const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
-                                const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
-                                float* host_rgbt, float* host_depth, nsl_stream stream) {
+// host_half: outputs are packed to fp16 on the device (pack_half_kernel) before the download
+static nsl_status host_impl(const nsl_grid_desc* g, const float* host_density, int32_t layout, const nsl_camera* cams,
+                            const nsl_light* lights, int32_t n_lights, int32_t light_mode, const nsl_medium* med,
+                            const nsl_march* m, const uint32_t* frame_ids, int32_t F, void* host_rgbt, void* host_depth,
+                            bool host_half, nsl_stream stream) {
     g_err.clear();
     if (nsl_status st = check_grid(g)) return st;
     if (nsl_status st = check_layout(layout)) return st;
@@ -658,13 +659,15 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     const size_t npix = (size_t)F * cams[0].width * cams[0].height;
     void *vstore = nullptr, *dout = nullptr;
     NSL_CUDA(pool_malloc(&vstore, vb, s), "cudaMallocAsync(volume)");
-    cudaError_t e = pool_malloc(&dout, npix * 20, s);
+    cudaError_t e = pool_malloc(&dout, npix * (host_half ? 30 : 20), s);
     if (e != cudaSuccess) {
         cudaFreeAsync(vstore, s);
         return cuda_fail(e, "cudaMallocAsync(outputs)");
     }
     float* d_rgbt = static_cast<float*>(dout);
     float* d_depth = d_rgbt + npix * 4;
+    uint16_t* h_rgbt = reinterpret_cast<uint16_t*>(d_depth + npix);      // fp16 staging (host_half)
+    uint16_t* h_depth = h_rgbt + npix * 4;
     nsl_volume* vol = nullptr;
     std::vector<int32_t> fv((size_t)F, 0);
     nsl_status st = volume_upload_impl(g, host_density, 0, layout, vstore, vb, stream, &vol, false);
@@ -694,12 +697,23 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
             e = cudaEventRecord(ev, s);
         }
         if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev, 0);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(host_rgbt + (size_t)f0 * npf * 4, d_rgbt + (size_t)f0 * npf * 4, (size_t)n * npf * 16,
-                                cudaMemcpyDeviceToHost, side);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(host_depth + (size_t)f0 * npf, d_depth + (size_t)f0 * npf, (size_t)n * npf * 4,
-                                cudaMemcpyDeviceToHost, side);
+        const size_t p0 = (size_t)f0 * npf, pn = (size_t)n * npf;
+        if (host_half) {                          // pack on the side stream, then download 10 B/pixel
+            if (e == cudaSuccess) e = launch_pack_half(d_rgbt + p0 * 4, d_depth + p0, h_rgbt + p0 * 4, h_depth + p0, pn, side);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(static_cast<uint16_t*>(host_rgbt) + p0 * 4, h_rgbt + p0 * 4, pn * 8,
+                                    cudaMemcpyDeviceToHost, side);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(static_cast<uint16_t*>(host_depth) + p0, h_depth + p0, pn * 2,
+                                    cudaMemcpyDeviceToHost, side);
+        } else {
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(static_cast<float*>(host_rgbt) + p0 * 4, d_rgbt + p0 * 4, pn * 16,
+                                    cudaMemcpyDeviceToHost, side);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(static_cast<float*>(host_depth) + p0, d_depth + p0, pn * 4,
+                                    cudaMemcpyDeviceToHost, side);
+        }
         if (e != cudaSuccess) st = cuda_fail(e, "result download");
     }
     if (side) {                                   // `stream` resumes after the last copy
@@ -724,6 +738,23 @@ nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_densit
     if (es != cudaSuccess) return cuda_fail(es, "cudaStreamSynchronize");
     if (n_invalid) return fail(NSL_ERR_INVALID_ARG, "density has %llu non-finite or negative values", n_invalid);
     return NSL_OK;
+}
+
+nsl_status nsl_guiding_map_host(const nsl_grid_desc* g, const float* host_density, int32_t layout,
+                                const nsl_camera* cams, const nsl_light* lights, int32_t n_lights, int32_t light_mode,
+                                const nsl_medium* med, const nsl_march* m, const uint32_t* frame_ids, int32_t F,
+                                float* host_rgbt, float* host_depth, nsl_stream stream) {
+    return host_impl(g, host_density, layout, cams, lights, n_lights, light_mode, med, m, frame_ids, F, host_rgbt,
+                     host_depth, false, stream);
+}
+
+nsl_status nsl_guiding_map_host_f16(const nsl_grid_desc* g, const float* host_density, int32_t layout,
+                                    const nsl_camera* cams, const nsl_light* lights, int32_t n_lights,
+                                    int32_t light_mode, const nsl_medium* med, const nsl_march* m,
+                                    const uint32_t* frame_ids, int32_t F, uint16_t* host_rgbt_h,
+                                    uint16_t* host_depth_h, nsl_stream stream) {
+    return host_impl(g, host_density, layout, cams, lights, n_lights, light_mode, med, m, frame_ids, F, host_rgbt_h,
+                     host_depth_h, true, stream);
 }
 
 // Animated volumes: frame f's density is laid out into its own storage and marched with its

@@ -214,6 +214,8 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
                                 unsigned long long* invalid, cudaStream_t s);
 // sampler microbenchmark (microbench.cu): volume fields of p only
 cudaError_t launch_l1_gather(const FrameParams& p, int blocks, int reps, float* sink, cudaStream_t s);
+cudaError_t launch_pack_half(const float* rgbt, const float* depth, uint16_t* rgbt_h, uint16_t* depth_h, size_t n,
+                             cudaStream_t s);
 int l1_gather_threads();
 int l1_gather_line();
 int l1_gather_max_blocks_per_sm(int layout);

@@ -4,6 +4,8 @@
 // smoke-shell depth vs the obstacle's shadow map).  One thread per pixel,
 // grid-stride, HBM-streaming: two float4 of maps + the depth in, one float4 out
 // (the shadow-map texels are few and L2-resident).
+#include <cuda_fp16.h>
+
 #include "nsl_internal.cuh"
 
 namespace nsl {
@@ -246,6 +248,32 @@ cudaError_t launch_relight(const RelightIn* in, int F, int n_lights, RelightFram
         relight_kernel<NSL_RL_SH_PPT, NSL_RL_SH_MINB><<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
     else
         relight_kernel<4, 1><<<(unsigned)(bpf * F), kRelightThreads, 0, s>>>(frames, rc, (int)bpf, maps, depth, out);
+    return cudaGetLastError();
+}
+
+// Compact host output (nsl_guiding_map_host_f16): the fp32 guiding map packed to fp16 (RNE) on
+// the device before the PCIe download, 10 B per pixel instead of 20.  One thread per pixel,
+// 16-B loads / 8-B stores, HBM-bound.
+__global__ void __launch_bounds__(256) pack_half_kernel(const float4* __restrict__ rgbt, const float* __restrict__ depth,
+                                                        uint2* __restrict__ rgbt_h, __half* __restrict__ depth_h,
+                                                        size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 v = __ldcs(rgbt + i);
+    const __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+    uint2 o;
+    o.x = *reinterpret_cast<const uint32_t*>(&a);
+    o.y = *reinterpret_cast<const uint32_t*>(&b);
+    __stcs(rgbt_h + i, o);
+    depth_h[i] = __float2half_rn(__ldcs(depth + i));
+}
+
+cudaError_t launch_pack_half(const float* rgbt, const float* depth, uint16_t* rgbt_h, uint16_t* depth_h, size_t n,
+                             cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    pack_half_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const float4*>(rgbt), depth,
+                                                                  reinterpret_cast<uint2*>(rgbt_h),
+                                                                  reinterpret_cast<__half*>(depth_h), n);
     return cudaGetLastError();
 }
 

@@ -316,6 +316,23 @@ def test_volume_rebuild_in_place(nsl):
         vol.rebuild(bad)
 
 
+def test_host_api_f16_is_the_rounded_fp32_result(nsl):
+    """nsl_guiding_map_host_f16 delivers exactly the RNE fp16 rounding of nsl_guiding_map_host's
+    fp32 maps (the march is the same; only the download is compact)."""
+    import torch
+    w = I.make_workload("C2", frames=list(range(0, 60, 7)))
+    hd = torch.from_numpy(w.volume(0))
+    F, H, W = w.n_frames, w.height, w.width
+    r32, d32 = torch.empty((F, H, W, 4)), torch.empty((F, H, W))
+    nsl.guiding_map_host(w.grid, hd, 3, w.cameras, w.lights, w.light_mode, w.medium, w.march, w.frame_ids, r32, d32)
+    r16 = torch.empty((F, H, W, 4), dtype=torch.float16).pin_memory()
+    d16 = torch.empty((F, H, W), dtype=torch.float16).pin_memory()
+    nsl.guiding_map_host_f16(w.grid, hd.pin_memory(), 3, w.cameras, w.lights, w.light_mode, w.medium, w.march,
+                             w.frame_ids, r16, d16)
+    assert np.array_equal(r16.numpy().view(np.uint16), r32.numpy().astype(np.float16).view(np.uint16))
+    assert np.array_equal(d16.numpy().view(np.uint16), d32.numpy().astype(np.float16).view(np.uint16))
+
+
 def test_host_api_rejects_invalid_density(nsl):
     import torch
     w = I.make_workload("C1")
