@@ -51,8 +51,9 @@ def parse():
     p.add_argument("--impl", default="nsl", choices=["nsl", "reference"])
     p.add_argument("--config", default="C2")
     p.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
-    p.add_argument("--layout", default="oct_f32", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32",
-                                                           "brick_oct_f32", "tex3d_f32", "morton_oct_f32"])
+    p.add_argument("--layout", default="auto", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32",
+                                                        "brick_oct_f32", "tex3d_f32", "morton_oct_f32", "auto"],
+                   help="auto (default): the library's size-based choice (nsl_layout_resolve)")
     p.add_argument("--light-model", default="march", choices=["march", "tv"],
                    help="march: canonical C8 (the headline); tv: NEXT-4 transmittance volume (DESIGN.md §12)")
     p.add_argument("--no-e2e", action="store_true")
@@ -379,6 +380,7 @@ def run_sharded(args, rank, world, local):
     else:
         w = rank_workload(cfg, rank, world, args.frames)
         F_total = w.n_frames * world
+    layout = nsl.layout_resolve(w.grid, layout)
     if args.light_model == "tv":
         from dataclasses import replace
         w = replace(w, march=replace(w.march, light_model=1))
@@ -475,7 +477,7 @@ def run_sharded(args, rank, world, local):
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f16" if layout == 2 else "f32",
             "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[cfg], "frames_total": F_total, "frames_per_rank": L,
-                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": args.layout,
+                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": nsl.LAYOUT_NAMES[layout] + (" (auto)" if args.layout == "auto" else ""),
                        "light_model": args.light_model, "chunk_frames": chunk,
                        "l2": "flushed (512 MiB write) before each timed step, outside the events",
                        "parallelism": f"frame-sharded x{world} (cyclic), results gathered to rank 0 "
@@ -517,9 +519,9 @@ def main():
             dist.barrier()
             dist.destroy_process_group()
         return
-    layout = nsl.LAYOUTS[args.layout]
     cfg = args.config
     w = rank_workload(cfg, rank, world, args.frames)
+    layout = nsl.layout_resolve(w.grid, nsl.LAYOUTS[args.layout])
     if args.light_model == "tv":
         from dataclasses import replace
         w = replace(w, march=replace(w.march, light_model=1))
@@ -613,7 +615,7 @@ def main():
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("config") == cfg and tj.get("layout") == args.layout and tj.get("frames") == F:
+            if tj.get("config") == cfg and tj.get("layout") == nsl.LAYOUT_NAMES[layout] and tj.get("frames") == F:
                 traffic = tj["dram_bytes_per_launch"]
         except Exception:
             traffic = None
@@ -654,7 +656,7 @@ def main():
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f16" if layout == 2 else "f32", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[cfg], "frames_per_rank": F, "frames_total": F * world,
-                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": args.layout, "light_model": args.light_model,
+                       "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": nsl.LAYOUT_NAMES[layout] + (" (auto)" if args.layout == "auto" else ""), "light_model": args.light_model,
                        "l2": "flushed (512 MiB write) between timed steps, outside the events",
                        "parallelism": f"frame-sharded x{world}, no data-path collective"},
             "samples_per_s": counts["canonical_samples"] * world * K / t_loop,

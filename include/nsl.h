@@ -82,7 +82,7 @@ typedef struct {
  *               the array; nsl_volume_rebuild refills it in place.
  *  MORTON_OCT_F32: the OCT elements in 8x8x8-cell tiles (16 KB, tiles x-fastest), Morton
  *               (z-order) inside a tile; one 256-bit gather/sample; 32-B aligned storage.
- *  DEFAULT = OCT_F32. */
+ *  AUTO       : chosen from the grid size (nsl_layout_resolve).  DEFAULT = AUTO. */
 typedef enum {
     NSL_LAYOUT_LINEAR_F32 = 0,
     NSL_LAYOUT_QUAD_F32 = 1,
@@ -91,8 +91,16 @@ typedef enum {
     NSL_LAYOUT_BRICK_OCT_F32 = 4,
     NSL_LAYOUT_TEX3D_F32 = 5,
     NSL_LAYOUT_MORTON_OCT_F32 = 6,
-    NSL_LAYOUT_DEFAULT = 3
+    NSL_LAYOUT_AUTO = 7,
+    NSL_LAYOUT_DEFAULT = NSL_LAYOUT_AUTO
 } nsl_layout;
+
+/* The concrete layout NSL_LAYOUT_AUTO stands for on grid g (any other layout is returned as
+ * is; -1 on an invalid grid): BRICK_OCT_F32 when the OCT body (n_x+1)(n_y+1)(n_z+1) x 32 B
+ * exceeds 2 GiB, else OCT_F32 -- chosen by measurement.  Every entry point
+ * taking a layout resolves AUTO this way (nsl_guiding_map_animated: OCT_F32, since its
+ * per-frame builds favour the cheaper OCT build). */
+int32_t nsl_layout_resolve(const nsl_grid_desc* g, int32_t layout);
 
 typedef struct nsl_volume nsl_volume;             /* opaque, immutable after upload */
 

@@ -26,10 +26,11 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
 
 LAYOUT_LINEAR_F32, LAYOUT_QUAD_F32, LAYOUT_CORNER_F16, LAYOUT_OCT_F32, LAYOUT_BRICK_OCT_F32 = 0, 1, 2, 3, 4
-LAYOUT_TEX3D_F32, LAYOUT_MORTON_OCT_F32 = 5, 6
-LAYOUT_DEFAULT = LAYOUT_OCT_F32
+LAYOUT_TEX3D_F32, LAYOUT_MORTON_OCT_F32, LAYOUT_AUTO = 5, 6, 7
+LAYOUT_DEFAULT = LAYOUT_AUTO
 LAYOUTS = {"linear_f32": 0, "quad_f32": 1, "corner_f16": 2, "oct_f32": 3, "brick_oct_f32": 4, "tex3d_f32": 5,
-           "morton_oct_f32": 6}
+           "morton_oct_f32": 6, "auto": 7}
+LAYOUT_NAMES = {v: k for k, v in LAYOUTS.items()}
 LIGHTS_EXPLICIT, LIGHTS_GUIDE = 0, 1
 LIGHT_MARCH, LIGHT_TV = 0, 1
 
@@ -107,7 +108,7 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
            "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
            "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak", "nsl_volume_rebuild",
-           "nsl_guiding_map_host_f16"]
+           "nsl_guiding_map_host_f16", "nsl_layout_resolve"]
 
 
 class BakeS(ctypes.Structure):
@@ -132,6 +133,7 @@ def lib():
     L.nsl_last_error.restype = ctypes.c_char_p
     L.nsl_version.restype = ctypes.c_char_p
     L.nsl_volume_bytes.argtypes = [P(GridDesc), i32]
+    L.nsl_layout_resolve.argtypes = [P(GridDesc), i32]
     L.nsl_volume_bytes.restype = ctypes.c_size_t
     L.nsl_volume_upload.argtypes = [P(GridDesc), vp, i32, i32, vp, ctypes.c_size_t, vp, P(vp)]
     L.nsl_volume_check.argtypes = [vp, vp, P(ctypes.c_uint64)]
@@ -220,6 +222,14 @@ def _stream_handle(stream) -> int:
     return s.cuda_stream
 
 
+def layout_resolve(grid, layout: int = LAYOUT_DEFAULT) -> int:
+    """The concrete layout `layout` stands for on `grid` (nsl_layout_resolve: AUTO by size)."""
+    r = lib().nsl_layout_resolve(ctypes.byref(grid_desc(grid)), layout)
+    if r < 0:
+        raise NslError("nsl_layout_resolve: invalid grid")
+    return r
+
+
 def volume_bytes(grid, layout: int = LAYOUT_DEFAULT) -> int:
     n = lib().nsl_volume_bytes(ctypes.byref(grid_desc(grid)), layout)
     if n == 0:
@@ -233,7 +243,7 @@ class Volume:
     def __init__(self, grid, density, layout: int = LAYOUT_DEFAULT, stream=None, storage=None):
         import torch
         self.grid = grid
-        self.layout = layout
+        self.layout = layout_resolve(grid, layout)
         nbytes = volume_bytes(grid, layout)
         if storage is None:
             storage = torch.empty(nbytes, dtype=torch.uint8, device="cuda")

@@ -93,6 +93,17 @@ nsl_status check_grid(const nsl_grid_desc* g) {
     return NSL_OK;
 }
 
+// NSL_LAYOUT_AUTO (the default): the layout chosen from the grid size by measurement (DESIGN.md §6,
+// profiles/r2_per_config): BRICK_OCT_F32 once the OCT body exceeds 2 GiB (C5's 512^3 static
+// volume: march -6.7 % over the 1024-frame batch), OCT_F32 below (C2 128^3: BRICK +3 %; C3 256^3:
+// equal, and BRICK's build costs 2x).  Animated volumes (a build per frame) resolve to OCT_F32.
+int resolve_layout(const nsl_grid_desc* g, int layout, bool animated = false) {
+    if (layout != NSL_LAYOUT_AUTO || !g) return layout;
+    if (animated) return kOctF32;
+    const double body = (double)(g->nx + 1) * (g->ny + 1) * (g->nz + 1) * 32.0;
+    return body > 2147483648.0 ? kBrickOctF32 : kOctF32;
+}
+
 nsl_status check_layout(int layout) {
     if (layout != kLinearF32 && layout != kQuadF32 && layout != kCornerF16 && layout != kOctF32 &&
         layout != kBrickOctF32 && layout != kTex3dF32 && layout != kMortonOctF32)
@@ -290,7 +301,13 @@ extern "C" {
 const char* nsl_last_error(void) { return g_err.c_str(); }
 const char* nsl_version(void) { return "nsl-b200 0.1 (sm_100a)"; }
 
+int32_t nsl_layout_resolve(const nsl_grid_desc* g, int32_t layout) {
+    if (check_grid(g) != NSL_OK) return -1;
+    return resolve_layout(g, layout);
+}
+
 size_t nsl_volume_bytes(const nsl_grid_desc* g, int32_t layout) {
+    layout = resolve_layout(g, layout);
     if (check_grid(g) != NSL_OK || check_layout(layout) != NSL_OK) return 0;
     return tail_offset(g, layout) + kTail;
 }
@@ -302,6 +319,7 @@ static nsl_status volume_upload_impl(const nsl_grid_desc* g, const float* densit
 // Host-only part of an upload: argument checks and the handle (no device work).
 static nsl_status volume_handle(const nsl_grid_desc* g, int32_t layout, void* device_storage, size_t storage_bytes,
                                 nsl_volume** out) {
+    layout = resolve_layout(g, layout);
     if (nsl_status st = check_grid(g)) return st;
     if (nsl_status st = check_layout(layout)) return st;
     if (!device_storage) return fail(NSL_ERR_INVALID_ARG, "NULL storage");
@@ -651,6 +669,7 @@ static nsl_status host_impl(const nsl_grid_desc* g, const float* host_density, i
                             bool host_half, nsl_stream stream) {
     g_err.clear();
     if (nsl_status st = check_grid(g)) return st;
+    layout = resolve_layout(g, layout);
     if (nsl_status st = check_layout(layout)) return st;
     if (!host_density || !cams || !host_rgbt || !host_depth) return fail(NSL_ERR_INVALID_ARG, "NULL host buffer");
     if (F < 1) return fail(NSL_ERR_INVALID_ARG, "F must be >= 1");
@@ -769,6 +788,7 @@ nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* 
                                     nsl_stream stream) {
     g_err.clear();
     if (nsl_status st = check_grid(g)) return st;
+    layout = resolve_layout(g, layout, true);
     if (nsl_status st = check_layout(layout)) return st;
     if (!densities || !storage || !cams) return fail(NSL_ERR_INVALID_ARG, "NULL densities/storage/cameras");
     if (F < 1) return fail(NSL_ERR_INVALID_ARG, "F must be >= 1");

@@ -71,7 +71,13 @@ def test_volume_bytes(nsl):
     assert oct_ == up(5 * 6 * 7 * 32) + tail
     L = nsl.lib()
     assert L.nsl_volume_bytes(ctypes.byref(nsl.grid_desc(I.Grid(0, 5, 6, (0, 0, 0), 0.25))), 1) == 0
-    assert L.nsl_volume_bytes(ctypes.byref(nsl.grid_desc(g)), 7) == 0
+    assert L.nsl_volume_bytes(ctypes.byref(nsl.grid_desc(g)), 99) == 0
+    # NSL_LAYOUT_AUTO (the default) resolves by size: OCT here, BRICK_OCT once the OCT body > 2 GiB
+    assert nsl.layout_resolve(g, nsl.LAYOUT_AUTO) == nsl.LAYOUT_OCT_F32
+    assert nsl.volume_bytes(g, nsl.LAYOUT_AUTO) == oct_
+    assert nsl.layout_resolve(I.Grid(512, 512, 512, (0, 0, 0), 1 / 512), nsl.LAYOUT_AUTO) == nsl.LAYOUT_BRICK_OCT_F32
+    assert nsl.layout_resolve(I.Grid(256, 256, 256, (0, 0, 0), 1 / 256), nsl.LAYOUT_AUTO) == nsl.LAYOUT_OCT_F32
+    assert nsl.layout_resolve(g, nsl.LAYOUT_TEX3D_F32) == nsl.LAYOUT_TEX3D_F32
     with pytest.raises(nsl.NslError):
         nsl.volume_bytes(I.Grid(4, 5, 6, (0, 0, 0), -1.0), 1)
 
