@@ -605,6 +605,26 @@ def test_guide_axis_fallback_closed_form(orc):
     assert np.abs(gm - wrong).max() > 1e-3 * np.abs(gm).max()
 
 
+def test_depth_threshold_is_strict(orc):
+    """C6 / Alg. 1 line "if D = 0 and sigma_n > tau": strict.  A constant grid
+    with sigma_s exactly tau on its plateau (rho 0.5, kappa 2, alpha 1: sigma_s = 1.0 exactly,
+    P13's exact interior) never hits at tau = 1.0, and hits at the first plateau sample once tau is
+    one fp32 ulp lower -- there D equals the t of the first sample with rho = 0.5 exactly."""
+    g = grid64(16)
+    vals = np.full((16, 16, 16), 0.5, np.float32)
+    cam = cam_down(W=8, H=8, extent=0.5)
+    med = I.Medium(2.0, 1.0, 0.0)
+    r = orc.guiding_map(g, vals, cam, FRONT_DOWN, I.LIGHTS_EXPLICIT, med, march(1.0 / 64, depth_tau=1.0))
+    assert np.all(r["depth"] == 0.0) and np.all(r["debug"][:, 2] == 0)
+    tau = float(np.nextafter(np.float32(1.0), np.float32(0.0)))
+    r = orc.guiding_map(g, vals, cam, FRONT_DOWN, I.LIGHTS_EXPLICIT, med, march(1.0 / 64, depth_tau=tau))
+    assert np.all(r["depth"] > 0.0)
+    # the first hit: sample n at z = 2 - n/64 has padded index u_z = 16 (2 - n/64) + 1/2, and the
+    # trilinear value is exactly 0.5 once u_z <= 16 (at u_z = 16 the weight of the apron corner is
+    # 0): 16 (2 - n/64) + 1/2 <= 16  <=>  n >= 66, so D = 66 h = 1.03125 for every pixel
+    assert np.all(r["debug"][:, 2] == 66) and np.all(r["depth"] == np.float32(66 / 64))
+
+
 def test_golden_hash_table_is_current(orc):
     """tests/golden/jitter_hash.txt was written by tests/golden/make_golden.py from the oracle."""
     import os
