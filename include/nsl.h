@@ -390,6 +390,14 @@ nsl_status nsl_bench_l1_peak(const float* buf, size_t buf_floats, const int32_t*
                              int64_t stride_elems, int64_t span_elems, int32_t waves, int32_t reps, float* sink,
                              size_t sink_floats, uint64_t* bytes, nsl_stream stream);
 
+/* The paper's "3D texture" sampling with HARDWARE trilinear filtering, for measuring
+ * its precision against the canonical fp32 sampler: the padded grid of
+ * `density` (device, x-fastest) in a float cudaArray with cudaFilterModeLinear and border
+ * (zero) addressing, sampled at n padded-index positions (device float[3n]) into out (device
+ * float[n]).  Synchronous; allocates and frees its own array. */
+nsl_status nsl_debug_tex_filter(const nsl_grid_desc* g, const float* density, const float* positions, int32_t n,
+                                float* out, nsl_stream stream);
+
 /* ------------------------------------------------------------------ debug / verification
  * Frame constants of DESIGN.md C3/C3b/C10 as the device computes them
  * (fp64 evaluation rounded once to fp32), for bitwise comparison with the

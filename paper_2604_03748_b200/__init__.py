@@ -108,7 +108,7 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
            "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
            "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak", "nsl_volume_rebuild",
-           "nsl_guiding_map_host_f16", "nsl_layout_resolve"]
+           "nsl_guiding_map_host_f16", "nsl_layout_resolve", "nsl_debug_tex_filter"]
 
 
 class BakeS(ctypes.Structure):
@@ -134,6 +134,7 @@ def lib():
     L.nsl_version.restype = ctypes.c_char_p
     L.nsl_volume_bytes.argtypes = [P(GridDesc), i32]
     L.nsl_layout_resolve.argtypes = [P(GridDesc), i32]
+    L.nsl_debug_tex_filter.argtypes = [P(GridDesc), vp, vp, i32, vp, vp]
     L.nsl_volume_bytes.restype = ctypes.c_size_t
     L.nsl_volume_upload.argtypes = [P(GridDesc), vp, i32, i32, vp, ctypes.c_size_t, vp, P(vp)]
     L.nsl_volume_check.argtypes = [vp, vp, P(ctypes.c_uint64)]
@@ -564,6 +565,17 @@ def bench_l1_peak(buf, lane_off, stride: int = 0, span: int = 1, waves: int = 4,
                                    reps, sink.data_ptr(), sink.numel(), ctypes.byref(n), _stream_handle(stream)),
            "nsl_bench_l1_peak")
     return n.value
+
+
+def debug_tex_filter(grid, density, positions, stream=None):
+    """Hardware trilinear (texture) filtering of `density` (cuda float32 [nz,ny,nx]) at padded-index
+    positions (cuda float32 [n,3]) -> cuda float32 [n] (nsl_debug_tex_filter)."""
+    import torch
+    out = torch.empty(positions.shape[0], dtype=torch.float32, device="cuda")
+    _check(lib().nsl_debug_tex_filter(ctypes.byref(grid_desc(grid)), density.data_ptr(), positions.data_ptr(),
+                                      positions.shape[0], out.data_ptr(), _stream_handle(stream)),
+           "nsl_debug_tex_filter")
+    return out
 
 
 def debug_frame_constants(grid, cam, lights, light_mode, medium, march, stream=None) -> dict:

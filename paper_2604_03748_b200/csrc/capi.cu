@@ -1254,6 +1254,56 @@ nsl_status nsl_bench_l1_peak(const float* buf, size_t buf_floats, const int32_t*
     return NSL_OK;
 }
 
+nsl_status nsl_debug_tex_filter(const nsl_grid_desc* g, const float* density, const float* positions, int32_t n,
+                                float* out, nsl_stream stream) {
+    g_err.clear();
+    if (nsl_status st = check_grid(g)) return st;
+    if (!density || !positions || !out || n < 0) return fail(NSL_ERR_INVALID_ARG, "bad arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int px = g->nx + 2, py = g->ny + 2, pz = g->nz + 2;
+    // the padded grid (zero apron, C1) on the host, then a float cudaArray with linear filtering
+    std::vector<float> pad((size_t)px * py * pz, 0.0f);
+    std::vector<float> raw((size_t)g->nx * g->ny * g->nz);
+    NSL_CUDA(cudaMemcpyAsync(raw.data(), density, raw.size() * sizeof(float), cudaMemcpyDeviceToHost, s), "density read");
+    NSL_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    for (int k = 0; k < g->nz; ++k)
+        for (int j = 0; j < g->ny; ++j)
+            for (int i = 0; i < g->nx; ++i)
+                pad[((size_t)(k + 1) * py + (j + 1)) * px + (i + 1)] = raw[((size_t)k * g->ny + j) * g->nx + i];
+    cudaArray_t arr = nullptr;
+    cudaTextureObject_t tex = 0;
+    const cudaChannelFormatDesc cd = cudaCreateChannelDesc<float>();
+    cudaError_t e = cudaMalloc3DArray(&arr, &cd, make_cudaExtent(px, py, pz));
+    if (e == cudaSuccess) {
+        cudaMemcpy3DParms cp;
+        memset(&cp, 0, sizeof cp);
+        cp.srcPtr = make_cudaPitchedPtr(pad.data(), px * sizeof(float), px, py);
+        cp.dstArray = arr;
+        cp.extent = make_cudaExtent(px, py, pz);
+        cp.kind = cudaMemcpyHostToDevice;
+        e = cudaMemcpy3D(&cp);
+    }
+    if (e == cudaSuccess) {
+        cudaResourceDesc rd;
+        memset(&rd, 0, sizeof rd);
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = arr;
+        cudaTextureDesc td;
+        memset(&td, 0, sizeof td);
+        td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeBorder;   // zero outside
+        td.filterMode = cudaFilterModeLinear;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
+    }
+    if (e == cudaSuccess) e = launch_tex_filter(tex, positions, n, out, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (tex) cudaDestroyTextureObject(tex);
+    if (arr) cudaFreeArray(arr);
+    if (e != cudaSuccess) return cuda_fail(e, "texture filtering");
+    return NSL_OK;
+}
+
 nsl_status nsl_debug_jitter(const nsl_march* m, uint32_t frame_id, int32_t n, uint32_t* out_hash, float* out_delta,
                             nsl_stream stream) {
     g_err.clear();

@@ -69,7 +69,23 @@ __global__ void __launch_bounds__(kPkThreads) l1_peak_kernel(const float* __rest
     sink[(size_t)blockIdx.x * kPkThreads + threadIdx.x] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
+// Hardware trilinear filtering of a float 3-D texture at index-space positions (the
+// paper's "3D texture", filtered by the texture unit): one thread per position.
+__global__ void tex_filter_kernel(cudaTextureObject_t t, const float* __restrict__ pos, int n, float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // padded index u = texel coordinate + 1/2 (texel c of the padded array holds padded voxel c,
+    // sampled at its centre c + 1/2 in unnormalised texture coordinates)
+    out[i] = tex3D<float>(t, pos[3 * i] + 0.5f, pos[3 * i + 1] + 0.5f, pos[3 * i + 2] + 0.5f);
+}
+
 }  // namespace
+
+cudaError_t launch_tex_filter(cudaTextureObject_t t, const float* pos, int n, float* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    tex_filter_kernel<<<(n + 255) / 256, 256, 0, s>>>(t, pos, n, out);
+    return cudaGetLastError();
+}
 
 int l1_peak_threads() { return kPkThreads; }
 int l1_peak_patterns() { return kPkPat; }

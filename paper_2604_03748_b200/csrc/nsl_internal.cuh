@@ -219,6 +219,7 @@ cudaError_t launch_pack_half(const float* rgbt, const float* depth, uint16_t* rg
 int l1_gather_threads();
 int l1_gather_line();
 int l1_gather_max_blocks_per_sm(int layout);
+cudaError_t launch_tex_filter(cudaTextureObject_t t, const float* pos, int n, float* out, cudaStream_t s);
 int l1_peak_threads();
 int l1_peak_patterns();
 int l1_peak_max_blocks_per_sm();
