@@ -218,7 +218,8 @@ VolDesc desc_of(const nsl_volume* v) {
 
 // Stream-ordered allocations of the library (frame tables, host-API staging, TV lattices) come
 // from a library-private pool per device, never the device's default pool that torch and other
-// libraries share.  Up to NSL_POOL_RETAIN_MB (default 1024) of it is retained across
+// libraries share.  Up to NSL_POOL_RETAIN_MB (default 4096, ~2 % of the B200's 180 GB) of it
+// is retained across
 // synchronisations, so per-call tables and the host API's staging are recycled instead of
 // re-mapped each call; anything above is released at the next synchronisation (e.g. the
 // transient TV lattices of up to NSL_TV_BUDGET_MB).
@@ -242,7 +243,10 @@ cudaError_t pool_malloc_v(void** p, size_t bytes, cudaStream_t s) {
             cudaMemPool_t np = nullptr;
             e = cudaMemPoolCreate(&np, &props);
             if (e != cudaSuccess) return e;
-            double mb = 1024.0;
+            // 4 GiB: the host API's transient buffers for C3-size batches (1.3 GB of fp32 maps,
+            // 1.9 GB with the fp16 staging) stay mapped between calls; at 1 GiB they were re-mapped
+            // every call (C3 e2e varied 10x between runs)
+            double mb = 4096.0;
             if (const char* env = getenv("NSL_POOL_RETAIN_MB")) mb = atof(env);
             uint64_t thr = mb <= 0.0 ? 0 : (uint64_t)(mb * 1048576.0);
             cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &thr);
