@@ -511,3 +511,40 @@ def test_hardware_texture_filtering_misses_the_parity_bar(nsl):
     ref_q = np.array([oracle.sample(w.grid, vals, tuple(p)) for p in us.astype(np.float32)])
     relq = np.abs(hw[big] - ref_q[big]) / ref_q[big]
     assert np.median(relq) < np.median(rel)
+
+
+def test_pinned_host_upload_is_complete_on_return(nsl):
+    """nsl_volume_upload from PINNED host memory returns only once the density has been
+    copied, so the caller may refill the buffer at once: the volume keeps the values it was given."""
+    import torch
+    w = I.make_workload("C2", frames=[0])
+    vals = torch.from_numpy(w.volume(0)).pin_memory()
+    ref = run(nsl, w, layout=3, debug=False)
+    vol = nsl.Volume(w.grid, vals, 3)
+    vals.fill_(7.0)                                  # immediately overwrite the pinned source
+    outs = nsl.alloc_outputs(1, w.height, w.width)
+    nsl.guiding_map(vol, w.cameras[0], w.lights[0], w.light_mode, w.medium, w.march, w.frame_ids[0], outs[0][0],
+                    outs[1][0])
+    torch.cuda.synchronize()
+    assert np.array_equal(outs[0].cpu().numpy(), ref[0]) and np.array_equal(outs[1].cpu().numpy(), ref[1])
+
+
+def test_tv_many_frames_small_grid(nsl):
+    """the TV sweep's grid.y is frames-per-group x lattice slots (<= 65535); a tiny grid
+    with 4 explicit lights and 17000 frames would put 68000 there -- the group is clamped, and the
+    results match the oracle on sampled frames."""
+    import torch
+    rng = np.random.default_rng(3)
+    grid = I.Grid(8, 8, 8, (0.0, 0.0, 0.0), 0.125)
+    vals = (rng.random((8, 8, 8)) * 0.8).astype(np.float32)
+    F = 17000
+    cams = [I.orbit_camera(0.02 * f, 2, 2, extent=1.2) for f in range(F)]
+    lights = [I.Light(I._f32t(I._unit(d)), (1.0, 0.5, 0.25)) for d in [(1, 0, 0.2), (0, 1, 0.5), (-1, -1, 1), (0.3, -0.2, 1)]]
+    med = I.Medium(8.0, 0.9, 0.0)
+    m = I.March(step=float(np.float32(0.125 * 2.5)), depth_tau=0.05, light_model=1)
+    w = I.Workload(name="tv_many", grid=grid, volume_specs=[("const", 0.0)], frame_vol=[0] * F, cameras=cams,
+                   light_mode=I.LIGHTS_EXPLICIT, lights=[lights] * F, medium=med, march=m,
+                   frame_ids=list(range(F)), _cache={0: vals})
+    g, gd, _ = run(nsl, w, layout=3, debug=False)
+    for f in (0, 9999, F - 1):
+        compare_frame(w, f, g[f], gd[f], None)
