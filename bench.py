@@ -338,6 +338,15 @@ def launches_per_step(w, args) -> int:
     return n + 1 + 3 * math.ceil(w.n_frames / group)
 
 
+def max_over_ranks(x: float, backend: str) -> float:
+    """Max of a host float over all ranks (device tensor for NCCL, host tensor for gloo)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def self_launch(args) -> int:
     """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this command as N ranks
     under torch.distributed.run on 127.0.0.1 (one process per GPU) and return its exit code."""
@@ -466,11 +475,7 @@ def run_sharded(args, rank, world, local):
     clk = clocks.stop()
     t_loop = sum(times)
     if world > 1:
-        t = torch.tensor([t_loop], device="cuda")
-        if args.backend == "gloo":
-            t = t.cpu()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_loop = float(t.item())
+        t_loop = max_over_ranks(t_loop, args.backend)
     rays = W * H * F_total * K
     line = {"metric": METRIC, "value": rays / t_loop, "unit": "rays/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_loop / K, "higher_is_better": True,
@@ -578,9 +583,7 @@ def main():
     layout_ms = [a.elapsed_time(b) for a, b, c in ev]
     t_loop = sum(step_ms) / 1e3
     if world > 1:
-        t = torch.tensor([t_loop], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_loop = float(t.item())
+        t_loop = max_over_ranks(t_loop, args.backend)
     total_rays = W * H * F * world * K
     value = total_rays / t_loop
     ms_step = 1e3 * t_loop / K
@@ -690,9 +693,7 @@ def main():
             torch.cuda.synchronize()
             te = es.elapsed_time(ee) / 1e3
             if world > 1:
-                t = torch.tensor([te], device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                te = float(t.item())
+                te = max_over_ranks(te, args.backend)
             line["e2e"] = {"value": W * H * F * world * ke / te, "unit": "rays/s",
                            "h2d_bytes_per_step": int(hd.numel() * 4 + F * (40 + 24 * w.n_lights + 8)),
                            "d2h_bytes_per_step": int(hr.numel() * 4 + hdep.numel() * 4),
@@ -711,9 +712,7 @@ def main():
             torch.cuda.synchronize()
             te16 = es.elapsed_time(ee) / 1e3
             if world > 1:
-                t = torch.tensor([te16], device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                te16 = float(t.item())
+                te16 = max_over_ranks(te16, args.backend)
             line["e2e_f16"] = {"value": W * H * F * world * ke / te16, "unit": "rays/s",
                                "h2d_bytes_per_step": int(hd.numel() * 4 + F * (40 + 24 * w.n_lights + 8)),
                                "d2h_bytes_per_step": int(hr16.numel() * 2 + hd16.numel() * 2),

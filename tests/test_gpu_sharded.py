@@ -107,3 +107,21 @@ def test_bench_self_launches_two_ranks_strong_scaling():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["frames_total"] == 12 and d["gather_bytes_to_rank0_per_step"] == 6 * 512 * 512 * 20
+
+
+def test_bench_self_launches_two_ranks_weak_default():
+    """The default (weak-scaling) bench path under two self-launched ranks: one JSON line,
+    n_gpus = 2, frames_total = 2 x frames_per_rank, max-over-ranks timing."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--backend", "gloo",
+                        "--frames", "6", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
+                        "--no-sampler-ceiling"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["frames_total"] == 12 and d["config"]["frames_per_rank"] == 6
