@@ -220,6 +220,16 @@ def test_parity_C4_subsampled(nsl):
         compare_frame(w, f, g[f], gd[f], gdbg[f], pixels=pix)
 
 
+def test_parity_C5_brick_auto_layout_sampled(nsl):
+    """C5's volume (512^3: a 4.3 GB OCT body) resolves NSL_LAYOUT_AUTO to BRICK_OCT (what bench.py
+    times for C5); the FAST march over it is checked against the oracle on a 1/256 sample."""
+    assert nsl.layout_resolve(I.make_workload("C5", frames=[0]).grid, nsl.LAYOUT_AUTO) == nsl.LAYOUT_BRICK_OCT_F32
+    w = I.make_workload("C5", frames=[300])
+    pix = _subsample(w.height, w.width, 16)
+    g, gd, dec = run_fast(nsl, w, layout=nsl.LAYOUT_AUTO, pixels=pix)
+    compare_frame(w, 0, g[0], gd[0], None, pixels=pix, dec=dec[0])
+
+
 def test_parity_C5_subsampled_full_size(nsl):
     """512^3, 2048^2 in the bench launch configuration (no debug), sampled 1/64."""
     w = I.make_workload("C5", frames=[0, 512])
