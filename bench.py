@@ -68,6 +68,8 @@ def parse():
                         "(C4: 240, C5: 1024 frames) split cyclically over the ranks")
     p.add_argument("--chunk", type=int, default=0,
                    help="sharded runs: frames per chunk (a gathered chunk's send overlaps the next chunk's march)")
+    p.add_argument("--graph", action="store_true",
+                   help="time replays of the step captured as a CUDA graph (volume rebuild + plan execute)")
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                    help="process group backend (gloo: functional runs of ranks sharing one GPU, host-staged gather)")
     return p.parse_args()
@@ -559,6 +561,19 @@ def main():
     torch.cuda.synchronize()
 
     K = args.steps
+    graph = None
+    if args.graph:                          # the step as one CUDA graph (its PDL edges captured)
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            for v, r in zip(vols, raw):
+                v.rebuild(r, stream=gs)
+            plan.execute(outputs[0], outputs[1], stream=gs)
+        torch.cuda.synchronize()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     # the timed steps: events only around the whole step, so the frame setup's programmatic
     # dependent launch overlaps the volume build's finalize as it does in production
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -570,9 +585,12 @@ def main():
         flush.zero_()                       # L2 flushed between timed iterations (outside the events)
         e0, e2 = ev[i]
         e0.record(stream)
-        for v, r in zip(vols, raw):
-            v.rebuild(r)                    # a1
-        plan.execute(outputs[0], outputs[1])   # a2-a9
+        if graph is not None:
+            graph.replay()
+        else:
+            for v, r in zip(vols, raw):
+                v.rebuild(r)                    # a1
+            plan.execute(outputs[0], outputs[1])   # a2-a9
         e2.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -679,6 +697,7 @@ def main():
             "config": {"workload": CONFIG_TEXT[cfg], "frames_per_rank": F, "frames_total": F * world,
                        "map": f"{W}x{H}", "grid": f"{w.grid.nx}^3", "layout": nsl.LAYOUT_NAMES[layout] + (" (auto)" if args.layout == "auto" else ""), "light_model": args.light_model,
                        "l2": "flushed (512 MiB write) between timed steps, outside the events",
+                       "step": "CUDA-graph replay" if args.graph else "eager launches (PDL-chained)",
                        "parallelism": f"frame-sharded x{world}, no data-path collective"},
             "samples_per_s": counts["canonical_samples"] * world * K / t_loop,
             "ms_per_frame": ms_step / F, "frames_per_s": F * world * K / t_loop,
