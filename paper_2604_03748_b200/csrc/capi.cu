@@ -267,7 +267,7 @@ struct Workspace {
     FrameIn* in = nullptr;
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
-    uint8_t* cull = nullptr;           // march_cull_bytes workspace (march calls only)
+    TileCull* cull = nullptr;          // march_cull_bytes workspace (march calls only)
 };
 
 // The frame tables (FrameIn, lights) uploaded into a fresh stream-ordered workspace, plus the
@@ -283,7 +283,7 @@ nsl_status upload_frames(const std::vector<FrameIn>& frames, const nsl_light* li
     ws.in = reinterpret_cast<FrameIn*>(ws.base);
     ws.lights = reinterpret_cast<nsl_light*>(static_cast<char*>(ws.base) + b_in);
     ws.params = reinterpret_cast<FrameParams*>(static_cast<char*>(ws.base) + b_in + b_l);
-    ws.cull = b_c ? reinterpret_cast<uint8_t*>(ws.base) + b_in + b_l + b_p : nullptr;
+    ws.cull = b_c ? reinterpret_cast<TileCull*>(static_cast<char*>(ws.base) + b_in + b_l + b_p) : nullptr;
     std::vector<char> host(b_in + b_l);
     memcpy(host.data(), frames.data(), sizeof(FrameIn) * F);
     memcpy(host.data() + b_in, lights, sizeof(nsl_light) * (size_t)F * n_lights);
@@ -534,7 +534,7 @@ static void tv_geometry(const nsl_volume* const* vols, int n_vols, Prepared& P) 
 // The march of a prepared batch: one launch, or (light_model TV) the lattice setup, then per
 // frame group the sweep and the march of that group.  tvp/tvbuf: P.tv_params_bytes() and
 // P.tv_buf_bytes() of device workspace (unused otherwise).
-static cudaError_t run_march(const Prepared& P, const FrameParams* params, uint8_t* cull,
+static cudaError_t run_march(const Prepared& P, const FrameParams* params, TileCull* cull,
                              TvParams* tvp, float2* tvbuf, float* out_rgbt, float* out_depth, uint32_t* out_debug,
                              unsigned long long* counters, cudaStream_t s) {
     float4* rgbt = reinterpret_cast<float4*>(out_rgbt);
@@ -543,7 +543,7 @@ static cudaError_t run_march(const Prepared& P, const FrameParams* params, uint8
                             cull, nullptr, s);
     cudaError_t e = launch_tv_setup(params, P.F, P.tv_slots, P.mc, tvp, s);
     const size_t npf = (size_t)P.W * P.H;
-    const size_t tiles = march_cull_bytes(1, P.W, P.H);
+    const size_t tiles = march_cull_bytes(1, P.W, P.H) / sizeof(TileCull);
     for (int g0 = 0; e == cudaSuccess && g0 < P.F; g0 += P.tv_group) {
         const int n = P.F - g0 < P.tv_group ? P.F - g0 : P.tv_group;
         const TvParams* gp = tvp + (size_t)g0 * P.tv_slots;
@@ -839,7 +839,7 @@ nsl_status nsl_guiding_map_animated(const nsl_grid_desc* g, const float* const* 
     // frame tables of all F frames in one upload; per chunk only frame setup + march
     Workspace ws;
     void* tvws = nullptr;
-    const size_t tiles = march_cull_bytes(1, P.W, P.H);
+    const size_t tiles = march_cull_bytes(1, P.W, P.H) / sizeof(TileCull);
     Prepared Pc = P;                             // a chunk's view of P (F = frames of the chunk)
     Pc.tv_group = P.tv_group < per ? P.tv_group : per;
     if (st == NSL_OK) st = upload_frames(P.frames, lights, n_lights, true, s, ws);
@@ -897,7 +897,7 @@ struct nsl_plan {
     FrameIn* in = nullptr;
     nsl_light* lights = nullptr;
     FrameParams* params = nullptr;
-    uint8_t* cull = nullptr;
+    TileCull* cull = nullptr;
     TvParams* tvp = nullptr;     // NEXT-4 workspace (light_model TV)
     float2* tvbuf = nullptr;
 };
@@ -926,7 +926,7 @@ nsl_status nsl_plan_create(const nsl_volume* const* vols, int32_t n_vols, const 
     p->in = reinterpret_cast<FrameIn*>(p->dev);
     p->lights = reinterpret_cast<nsl_light*>(static_cast<char*>(p->dev) + b_in);
     p->params = reinterpret_cast<FrameParams*>(static_cast<char*>(p->dev) + b_in + b_l);
-    p->cull = reinterpret_cast<uint8_t*>(p->dev) + b_in + b_l + b_p;
+    p->cull = reinterpret_cast<TileCull*>(static_cast<char*>(p->dev) + b_in + b_l + b_p);
     p->tvp = reinterpret_cast<TvParams*>(static_cast<char*>(p->dev) + b_in + b_l + b_p + b_c);
     p->tvbuf = reinterpret_cast<float2*>(static_cast<char*>(p->dev) + b_in + b_l + b_p + b_c + b_tp);
     std::vector<char> host(b_in + b_l);

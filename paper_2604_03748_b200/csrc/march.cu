@@ -26,36 +26,130 @@ namespace {
 // r, no sample of the tile lies in the box.  bit 0: misses the occupied box (FAST:
 // every sample outside it is exactly 0); bit 1: misses the support box (DEBUG/COUNTED,
 // which report n_lo/n_hi: C5).  One thread per (frame, tile).
-__global__ void tile_cull_kernel(const FrameParams* __restrict__ fps, int F, int tiles_x, int tiles,
-                                 uint8_t* __restrict__ cull) {
-    pdl_trigger();
-    pdl_wait();                        // the FrameParams of frame_setup_kernel
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)F * tiles) return;
-    const int f = (int)(idx / (unsigned)tiles), t = (int)(idx - (size_t)f * tiles);
-    const int tx = t % tiles_x, ty = t / tiles_x;
+// One thread per (frame, tile); grid (tile blocks, frame), so a CTA's tiles share one frame and its
+// volume's slab boxes are staged once in shared memory.
+constexpr int kCullThreads = 256, kCullSlabs = 128;
+__global__ void __launch_bounds__(kCullThreads) tile_cull_kernel(const FrameParams* __restrict__ fps, int F,
+                                                                 int tiles_x, int tiles, TileCull* __restrict__ cull,
+                                                                 int early_trigger) {
+    __shared__ int4 s_box[kCullSlabs];                  // (x0, y0, x1, y1) blocks of each z-slab
+    // PDL: for small batches the march may launch at once (its launch latency hides under this
+    // grid); for large ones the trigger is implicit at exit, so the march's CTAs -- which would
+    // wait, resident, on this grid -- do not take the SMs this kernel's CTAs still need
+    // (measured: C2 -0.9 % late vs early, C1 +10 % late)
+    if (early_trigger) pdl_trigger();
+    pdl_wait();                        // the FrameParams of frame_setup_kernel (after the volume build)
+    const int f = blockIdx.y, t = blockIdx.x * kCullThreads + threadIdx.x;
     const FrameParams& sp = fps[f];
+    const int nbz = sp.occ_nbz;
+    const bool staged = nbz <= kCullSlabs;
+    const int* sl = reinterpret_cast<const int*>(sp.occ) + sp.slab_off;
+    if (staged) {
+        for (int bz = threadIdx.x; bz < nbz; bz += kCullThreads) {
+            const int2 mn = __ldg(reinterpret_cast<const int2*>(sl + 2 * bz));
+            const int2 mx = __ldg(reinterpret_cast<const int2*>(sl + 2 * nbz + 2 * bz));
+            s_box[bz] = make_int4(mn.x, mn.y, mx.x, mx.y);
+        }
+    }
+    __syncthreads();
+    if (t >= tiles) return;
+    const int tx = t % tiles_x, ty = t / tiles_x;
     const float cx = (float)(tx * kTileW) + 0.5f * (kTileW - 1), cy = (float)(ty * kTileH) + 0.5f * (kTileH - 1);
-    const float c[3] = {fmaf(cy, sp.Ey[0], fmaf(cx, sp.Ex[0], sp.B[0])), fmaf(cy, sp.Ey[1], fmaf(cx, sp.Ex[1], sp.B[1])),
-                        fmaf(cy, sp.Ey[2], fmaf(cx, sp.Ex[2], sp.B[2]))};
-    // tile radius in index units: half extents of the tile (+1 pixel) along E_x, E_y, +1 for rounding
+    float c[3], D[3], iD[3];
     float rr = 0.0f;
+#pragma unroll
     for (int q = 0; q < 3; ++q) {
+        c[q] = fmaf(cy, sp.Ey[q], fmaf(cx, sp.Ex[q], sp.B[q]));
+        D[q] = sp.Dg[q];
+        iD[q] = sp.invD[q];
+        // tile radius in index units: half extents of the tile (+1 pixel) along E_x, E_y, +1 for rounding
         const float e = (0.5f * kTileW + 1.0f) * fabsf(sp.Ex[q]) + (0.5f * kTileH + 1.0f) * fabsf(sp.Ey[q]);
         rr = fmaf(e, e, rr);
     }
     rr = sqrtf(rr) * 1.001f + 1.0f;
-    uint8_t bits = 0;
+    uint32_t bits = 0;
     for (int box = 0; box < 2; ++box) {
         float t0 = -3.0e38f, t1 = 3.0e38f;
         bool miss = false;
+#pragma unroll
         for (int q = 0; q < 3; ++q) {
             const float lo = box == 0 ? sp.alo[q] : 0.0f, hi = box == 0 ? sp.ahi[q] : sp.supp[q];
-            slab(c[q] - lo + rr, sp.Dg[q], sp.invD[q], hi - lo + 2.0f * rr, 0.0f, t0, t1, miss);
+            slab(c[q] - lo + rr, D[q], iD[q], hi - lo + 2.0f * rr, 0.0f, t0, t1, miss);
         }
-        if (miss || !(t0 <= t1) || t1 < 0.0f) bits |= (uint8_t)(1u << box);
+        if (miss || !(t0 <= t1) || t1 < 0.0f) bits |= 1u << box;
     }
-    cull[idx] = bits;
+    // [t0, t1]: the union of the centre ray's hits on every z-slab's 2-D box of occupied blocks,
+    // each grown by rr on all sides.  A tile ray is the centre ray shifted by <= rr across the view,
+    // so a sample of it inside an occupied block (hence inside its slab's box) has its t inside
+    // the grown box's hit of the centre ray: samples outside [t0, t1] are exactly 0 (C1).  Only
+    // the slabs the bundle crosses inside the occupied box are visited (its z extent +- rr there).
+    float lo = 3.0e38f, hi = -3.0e38f;
+    if (!(bits & 1u)) {
+        const float B = (float)(1 << sp.occ_shift);
+        // the bundle's z range inside the occupied box -> the slabs to visit
+        float ta = -3.0e38f, tb = 3.0e38f;
+        bool m2 = false;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            slab(c[q] - sp.alo[q] + rr, D[q], iD[q], sp.ahi[q] - sp.alo[q] + 2.0f * rr, 0.0f, ta, tb, m2);
+        const float za = fmaf(ta, D[2], c[2]), zb = fmaf(tb, D[2], c[2]);
+        const float zlo = (D[2] == 0.0f ? c[2] : fminf(za, zb)) - rr - 1.0f;
+        const float zhi = (D[2] == 0.0f ? c[2] : fmaxf(za, zb)) + rr + 1.0f;
+        const int bz0 = max(0, (int)floorf(zlo / B)), bz1 = min(nbz - 1, (int)floorf(zhi / B));
+        // per-axis affine forms of the grown slab faces: t(face) = (face - c) / D
+        float k0[3], k1[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            k1[q] = B * iD[q];
+            k0[q] = (-rr - c[q]) * iD[q];
+        }
+        const float w[3] = {2.0f * rr * iD[0], 2.0f * rr * iD[1], 2.0f * rr * iD[2]};
+        for (int bz = bz0; bz <= bz1; ++bz) {
+            int4 b4;
+            if (staged) {
+                b4 = s_box[bz];
+            } else {
+                const int2 mn = __ldg(reinterpret_cast<const int2*>(sl + 2 * bz));
+                const int2 mx = __ldg(reinterpret_cast<const int2*>(sl + 2 * nbz + 2 * bz));
+                b4 = make_int4(mn.x, mn.y, mx.x, mx.y);
+            }
+            if (b4.z < 0) continue;                   // an empty slab
+            const float blo[3] = {(float)b4.x, (float)b4.y, (float)bz};
+            const float bhi[3] = {(float)(b4.z + 1), (float)(b4.w + 1), (float)(bz + 1)};
+            float t0 = -3.0e38f, t1 = 3.0e38f;
+            bool miss = false;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (D[q] != 0.0f) {
+                    float u = fmaf(blo[q], k1[q], k0[q]), v = fmaf(bhi[q], k1[q], k0[q] + w[q]);
+                    if (u > v) {
+                        const float tt = u;
+                        u = v;
+                        v = tt;
+                    }
+                    t0 = fmaxf(t0, u);
+                    t1 = fminf(t1, v);
+                } else {
+                    miss |= !(c[q] > blo[q] * B - rr && c[q] < bhi[q] * B + rr);
+                }
+            }
+            if (!miss && t0 <= t1) {
+                lo = fminf(lo, t0);
+                hi = fmaxf(hi, t1);
+            }
+        }
+        // the affine forms round differently from the slab test: widen by a relative 1e-5 of the
+        // magnitudes plus one index unit of t (|D| = 1/dx: t of one index unit is dx) for safety
+        const float pad = 1e-5f * fmaxf(fabsf(lo), fabsf(hi)) + 1.0f / sp.inv_dx;   // (no hit: stays empty)
+        lo -= pad;
+        hi += pad;
+    }
+    TileCull out;
+    out.t0 = lo;
+    out.t1 = hi;
+    out.bits = bits;
+    out.pad = 0u;
+    cull[(size_t)f * tiles + t] = out;
 }
 
 // NEXT-4 V5: trilinear lookup of (tau+, tau-) at index-space position (x, y, z) in the
@@ -101,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
                                                          float4* __restrict__ out_rgbt, float* __restrict__ out_depth,
                                                          uint32_t* __restrict__ out_debug,
                                                          unsigned long long* __restrict__ counters, int W, int H,
-                                                         const uint8_t* __restrict__ cull, int tiles_x, TvArgs tv) {
+                                                         const TileCull* __restrict__ cull, int tiles_x, TvArgs tv) {
     constexpr bool DEBUG = MODE == kDebug, COUNT = MODE == kCounted;
     // 3-D grid (frame, tile column rank, tile row rank): frames fastest, then the tiles of one
     // tile row, then rows -- rows and columns centre-out (centre_out), so whole tile rows run
@@ -123,7 +217,14 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
     const size_t o = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
 
     // the cull flag and the volume fields are independent loads: issue them together
-    const uint8_t cflag = PROJ == 0 ? __ldg(cull + (size_t)f * (tiles_x * tiles_y) + ty * tiles_x + tx) : 0;
+    float tr0 = -3.0e38f, tr1 = 3.0e38f;               // the tile's occupied-slab range (FAST/COUNTED)
+    uint32_t cflag = 0u;
+    if (PROJ == 0) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(cull + (size_t)f * (tiles_x * tiles_y) + ty * tiles_x + tx));
+        tr0 = q.x;
+        tr1 = q.y;
+        cflag = __float_as_uint(q.z);
+    }
     Vol v;
     v.data = sp.data;
     v.sy = sp.sy;
@@ -208,6 +309,12 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
             slab(r.ox - sp.alo[0], r.dx, inv[0], sp.ahi[0] - sp.alo[0], 1e-3f, u0, u1, miss);
             slab(r.oy - sp.alo[1], r.dy, inv[1], sp.ahi[1] - sp.alo[1], 1e-3f, u0, u1, miss);
             slab(r.oz - sp.alo[2], r.dz, inv[2], sp.ahi[2] - sp.alo[2], 1e-3f, u0, u1, miss);
+#if NSL_TILE_RANGE
+            if (PROJ == 0 && !DEBUG) {               // the tile's occupied-slab range (tile_cull_kernel)
+                u0 = fmaxf(u0, tr0);
+                u1 = fminf(u1, tr1);
+            }
+#endif
             if (miss || !(u0 <= u1)) {
                 m_lo = 1;
                 m_hi = 0;
@@ -399,14 +506,15 @@ __global__ void jitter_debug_kernel(MarchConst mc, uint32_t frame, int n, uint32
 
 template <int LAYOUT, int PROJ, int MODE>
 cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
-                       uint32_t* debug, unsigned long long* counters, uint8_t* cull,
+                       uint32_t* debug, unsigned long long* counters, TileCull* cull,
                        const TvArgs* tv, cudaStream_t s) {
     const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH, tiles = tiles_x * tiles_y;
     if (tiles > 65535) return cudaErrorInvalidConfiguration;
     if (PROJ == 0) {
-        const size_t n = (size_t)F * tiles;
-        cudaError_t e = launch_pdl(tile_cull_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, fp, F, tiles_x,
-                                   tiles, cull);
+        if (F > 65535) return cudaErrorInvalidConfiguration;
+        const int early = (long long)F * tiles <= 8 * kCullThreads;
+        cudaError_t e = launch_pdl(tile_cull_kernel, dim3((unsigned)((tiles + kCullThreads - 1) / kCullThreads), (unsigned)F),
+                                   dim3(kCullThreads), 0, s, fp, F, tiles_x, tiles, cull, early);
         if (e != cudaSuccess) return e;
     }
     const unsigned txn = (unsigned)tiles_x, tyn = (unsigned)tiles_y;
@@ -415,29 +523,29 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
         if constexpr (MODE == kFast) {
             if (NSL_TV_G3 && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
                 return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 3>, grid, dim3(kThreads), 0, s, fp, mc,
-                                  rgbt, depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, *tv);
+                                  rgbt, depth, debug, counters, W, H, (const TileCull*)cull, tiles_x, *tv);
             if (NSL_TV_NL && mc.n_lights == 1)
                 return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 1>, grid, dim3(kThreads), 0, s, fp, mc,
-                                  rgbt, depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, *tv);
+                                  rgbt, depth, debug, counters, W, H, (const TileCull*)cull, tiles_x, *tv);
         }
         return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, true, 0>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
-                          depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, *tv);
+                          depth, debug, counters, W, H, (const TileCull*)cull, tiles_x, *tv);
     }
     if constexpr (MODE == kFast) {
         if (NSL_G3 && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
             return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 3>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
-                              depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, TvArgs{});
+                              depth, debug, counters, W, H, (const TileCull*)cull, tiles_x, TvArgs{});
         if (NSL_L1 && mc.n_lights == 1)
             return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 1>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
-                              depth, debug, counters, W, H, (const uint8_t*)cull, tiles_x, TvArgs{});
+                              depth, debug, counters, W, H, (const TileCull*)cull, tiles_x, TvArgs{});
     }
     return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 0>, grid, dim3(kThreads), 0, s, fp, mc, rgbt, depth,
-                      debug, counters, W, H, (const uint8_t*)cull, tiles_x, TvArgs{});
+                      debug, counters, W, H, (const TileCull*)cull, tiles_x, TvArgs{});
 }
 
 template <int LAYOUT, int PROJ>
 cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, float4* rgbt, float* depth,
-                      uint32_t* debug, unsigned long long* counters, uint8_t* cull,
+                      uint32_t* debug, unsigned long long* counters, TileCull* cull,
                       const TvArgs* tv, cudaStream_t s) {
     if (debug) return launch_lpm<LAYOUT, PROJ, kDebug>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s);
     if (counters)
@@ -447,7 +555,7 @@ cudaError_t launch_lp(const FrameParams* fp, const MarchConst& mc, int F, int W,
 
 template <int LAYOUT>
 cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int proj, float4* rgbt,
-                     float* depth, uint32_t* debug, unsigned long long* counters, uint8_t* cull,
+                     float* depth, uint32_t* debug, unsigned long long* counters, TileCull* cull,
                      const TvArgs* tv, cudaStream_t s) {
     return proj == 0 ? launch_lp<LAYOUT, 0>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s)
                      : launch_lp<LAYOUT, 1>(fp, mc, F, W, H, rgbt, depth, debug, counters, cull, tv, s);
@@ -459,12 +567,12 @@ int march_tile_w() { return kTileW; }
 int march_tile_h() { return kTileH; }
 
 size_t march_cull_bytes(int F, int W, int H) {
-    return (size_t)F * ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
+    return (size_t)F * ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH) * sizeof(TileCull);
 }
 
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection, int layout,
                          float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
-                         uint8_t* cull, const TvArgs* tv, cudaStream_t s) {
+                         TileCull* cull, const TvArgs* tv, cudaStream_t s) {
     switch (layout) {
         case kLinearF32: return launch_l<kLinearF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);
         case kQuadF32: return launch_l<kQuadF32>(fp, mc, F, W, H, projection, rgbt, depth, debug, counters, cull, tv, s);

@@ -96,6 +96,15 @@ __host__ __device__ inline void layout_strides(int layout, int nx, int ny, int32
     }
 }
 
+// Per (frame, 16x8 tile) of an orthographic march, written by tile_cull_kernel: bits (bit 0: the
+// tile's rays miss the occupied box, bit 1: they miss the support box) and [t0, t1], a
+// conservative ray-parameter range outside which every sample of every ray of the tile is
+// exactly 0 (the union of the tile bundle's hits on the z-slabs' 2-D boxes of occupied blocks).
+struct TileCull {
+    float t0, t1;
+    uint32_t bits, pad;
+};
+
 struct MarchConst {
     float h, hl, tau_d, t_min;
     float kappa, alpha, g;
@@ -228,11 +237,11 @@ cudaError_t launch_l1_peak(const float* buf, const int* lane_off, long long stri
 cudaError_t launch_frame_setup(const FrameIn* in, const nsl_light* lights, int F, const MarchConst& mc,
                                FrameParams* out, cudaStream_t s);
 // mode: 0 fast (timed path), 1 debug (canonical counters, no shortcuts), 2 counted fast path.
-// cull: march_cull_bytes(F, W, H) bytes of device workspace (orthographic views: per-tile cull flags).
+// cull: march_cull_bytes(F, W, H) bytes of device workspace (orthographic views: a TileCull per tile).
 // tv: NULL (light_model 0) or the group's transmittance-volume arguments.
 cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int W, int H, int projection,
                          int layout, float4* rgbt, float* depth, uint32_t* debug, unsigned long long* counters,
-                         uint8_t* cull, const TvArgs* tv, cudaStream_t s);
+                         TileCull* cull, const TvArgs* tv, cudaStream_t s);
 size_t march_cull_bytes(int F, int W, int H);
 int march_tile_w();
 int march_tile_h();

@@ -66,6 +66,9 @@ static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (3
 #ifndef NSL_HZ                  // horizontal guide pair: z plane hoisted out of the light loop
 #define NSL_HZ 1
 #endif
+#ifndef NSL_TILE_RANGE          // FAST/COUNTED ortho: primary steps limited to the tile's occupied-slab range
+#define NSL_TILE_RANGE 1
+#endif
 constexpr int kFast = 0, kDebug = 1, kCounted = 2;
 
 struct Vol {
