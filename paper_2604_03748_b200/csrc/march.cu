@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(kCullThreads) tile_cull_kernel(const FramePara
     // PDL: for small batches the march may launch at once (its launch latency hides under this
     // grid); for large ones the trigger is implicit at exit, so the march's CTAs -- which would
     // wait, resident, on this grid -- do not take the SMs this kernel's CTAs still need
-    // (measured: C2 -0.9 % late vs early, C1 +10 % late)
+    // (measured: C2 -0.9 % late vs early).  Small batches also skip the range (below): the cull
+    // kernel is then on a critical path of a few tens of us (C1's single frame: +10 % with it).
     if (early_trigger) pdl_trigger();
     pdl_wait();                        // the FrameParams of frame_setup_kernel (after the volume build)
     const int f = blockIdx.y, t = blockIdx.x * kCullThreads + threadIdx.x;
@@ -84,7 +85,10 @@ __global__ void __launch_bounds__(kCullThreads) tile_cull_kernel(const FramePara
     // the grown box's hit of the centre ray: samples outside [t0, t1] are exactly 0 (C1).  Only
     // the slabs the bundle crosses inside the occupied box are visited (its z extent +- rr there).
     float lo = 3.0e38f, hi = -3.0e38f;
-    if (!(bits & 1u)) {
+    if (early_trigger && !(bits & 1u)) {                 // small batch: no range (the whole box)
+        lo = -3.0e38f;
+        hi = 3.0e38f;
+    } else if (!(bits & 1u)) {
         const float B = (float)(1 << sp.occ_shift);
         // the bundle's z range inside the occupied box -> the slabs to visit
         float ta = -3.0e38f, tb = 3.0e38f;
