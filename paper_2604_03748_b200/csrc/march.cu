@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kCullThreads) tile_cull_kernel(const FramePara
         const float pad = 1e-5f * fmaxf(fabsf(lo), fabsf(hi)) + 1.0f / sp.inv_dx;   // (no hit: stays empty)
         lo -= pad;
         hi += pad;
+        if (!(lo <= hi)) bits |= 1u;       // no slab box on the bundle's path: FAST culls the tile too
     }
     TileCull out;
     out.t0 = lo;
