@@ -1,4 +1,4 @@
-"""Multi-rank frame sharding on the GPU: two ranks that share cuda:0 (gloo
+"""Multi-rank frame sharding on the GPU: two or four ranks that share cuda:0 (gloo
 process group: the 1-GPU test box cannot host NCCL ranks) march their cyclic shards of a
 C2 batch through the C ABI, chunk by chunk, and gather every chunk to rank 0
 (sharding.ChunkedGather, host-staged under gloo).  The gathered maps must equal a
@@ -71,8 +71,8 @@ def _worker(rank, world, port, chunk, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("chunk", [2, 16])
-def test_two_ranks_gathered_equal_single_rank(tmp_path, chunk):
+@pytest.mark.parametrize("world,chunk", [(2, 2), (2, 16), (4, 1)])
+def test_ranks_gathered_equal_single_rank(tmp_path, world, chunk):
     import torch
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
@@ -81,7 +81,7 @@ def test_two_ranks_gathered_equal_single_rank(tmp_path, chunk):
     import paper_2604_03748_b200 as nsl
     out = str(tmp_path / "gathered.npz")
     mp.get_context("spawn")
-    mp.spawn(_worker, args=(2, _free_port(), chunk, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), chunk, out), nprocs=world, join=True)
     got = np.load(out)
     w = I.make_workload("C2", frames=FRAMES)
     rgbt, depth, _ = nsl.run_workload(w, layout=3)

@@ -110,12 +110,13 @@ def _chunk_worker(rank, world, port, F, chunk, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("F,chunk", [(8, 3), (7, 2), (9, 16), (2, 1)])
-def test_chunked_gather_world2_gloo(tmp_path, F, chunk):
+@pytest.mark.parametrize("world,F,chunk", [(2, 8, 3), (2, 7, 2), (2, 9, 16), (2, 2, 1), (3, 10, 2), (4, 9, 1)])
+def test_chunked_gather_gloo(tmp_path, world, F, chunk):
     """ChunkedGather (the bench's overlapped result gather): chunk by chunk, rank 0 receives
-    every peer's rows straight into the rank-major result; unshard_order restores frame order."""
+    every peer's rows straight into the rank-major result; unshard_order restores frame order
+    (world sizes 2-4, ragged F, chunks smaller and larger than the shard)."""
     out = str(tmp_path / "full.pt")
-    mp.spawn(_chunk_worker, args=(2, _free_port(), F, chunk, out), nprocs=2, join=True)
+    mp.spawn(_chunk_worker, args=(world, _free_port(), F, chunk, out), nprocs=world, join=True)
     rgbt, depth = torch.load(out)
     assert rgbt.shape == (F, 3, 5, 4) and depth.shape == (F, 3, 5)
     for f in range(F):
