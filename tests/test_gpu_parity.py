@@ -564,3 +564,38 @@ def test_tv_many_frames_small_grid(nsl):
     g, gd, _ = run(nsl, w, layout=3, debug=False)
     for f in (0, 9999, F - 1):
         compare_frame(w, f, g[f], gd[f], None)
+
+
+def test_tile_range_random_batches(nsl):
+    """The per-tile occupied-slab range and slab-box culling are exactness-critical
+    and only active for batches of > 2048 tiles: random tiny orthographic cases replicated to 2100
+    frames (distinct jitter keys) go through them; FAST must equal the oracle (tie pixels
+    re-verified with DEBUG decisions) on sampled frames, and FAST's T and D must match DEBUG's
+    (which keeps the whole occupied box) on every frame."""
+    rng = np.random.default_rng(777)
+    for trial in range(6):
+        nx, ny, nz = (int(x) for x in rng.integers(6, 20, 3))
+        dxw = float(np.float32(1.0 / max(nx, ny, nz)))
+        grid = I.Grid(nx, ny, nz, (0.0, 0.0, 0.0), dxw)
+        vals = np.zeros((nz, ny, nx), np.float32)           # a few blobs: empty slabs and gaps
+        for _ in range(int(rng.integers(1, 4))):
+            c = rng.random(3) * np.array([nx, ny, nz])
+            r = rng.uniform(1.5, 4.0)
+            zz, yy, xx = np.mgrid[0:nz, 0:ny, 0:nx]
+            d2 = (xx + 0.5 - c[0]) ** 2 + (yy + 0.5 - c[1]) ** 2 + (zz + 0.5 - c[2]) ** 2
+            vals += np.where(d2 < r * r, rng.uniform(0.3, 1.0), 0.0).astype(np.float32)
+        cam = I.orbit_camera(rng.uniform(0, 360), int(rng.integers(17, 40)), int(rng.integers(9, 30)),
+                             elev_deg=rng.uniform(-50, 50), extent=float(rng.uniform(0.8, 1.6)))
+        mode = int(rng.integers(0, 2))
+        lights = (I.guide_lights() if mode == I.LIGHTS_GUIDE else
+                  [I.Light(I._f32t(I._unit(tuple(rng.normal(size=3)))), (1.0, 0.8, 0.6))])
+        med = I.Medium(float(np.float32(rng.uniform(4, 60))), 1.0, 0.0)
+        m = I.March(step=float(np.float32(dxw * rng.choice([2.5, 10.0]))), depth_tau=0.1, t_min=1e-3, jitter=1,
+                    seed=int(rng.integers(0, 2 ** 40)))
+        F = 2100
+        w = I.Workload(name="tr", grid=grid, volume_specs=[("const", 0.0)], frame_vol=[0] * F, cameras=[cam] * F,
+                       light_mode=mode, lights=[lights] * F, medium=med, march=m, frame_ids=list(range(F)),
+                       _cache={0: vals})
+        g, gd, dec = run_fast(nsl, w, layout=3)
+        for f in (0, 1049, F - 1):
+            compare_frame(w, f, g[f], gd[f], None, dec=dec[f])
