@@ -40,7 +40,16 @@ CONFIG_TEXT = {
     "C3": "C3: obstacle-carved plume 256^3, 60 frames x 1024x1024, moving light",
     "C4": "C4: animated plume 256^3 (distinct volume per frame), 1024x1024, guide lights",
     "C5": "C5: plume 512^3, 2048x2048 frames, guide lights",
+    "P482": "P482: the paper's timed workload (PAPER.md:482): plume 400^3, one 512x512 frame per step "
+            "(a fresh volume layout every step, as when the simulation streams density in), guide lights",
 }
+# frames on each config's camera path, and the frames one step marches by default
+N_PATH = {"C1": 1, "C2": 60, "C3": 60, "C4": 240, "C5": 1024, "P482": 60}
+N_STEP = dict(N_PATH, P482=1)
+# the paper's only number for this path: ~2 ms per 512^2 frame over 400^3 (an
+# unnamed 16,384-core 24 GB GPU, RTX-4090 class) = 131 M rays/s
+PAPER_P482 = {"ms_per_frame": 2.0, "rays_per_s": 512 * 512 / 2e-3, "source": "PAPER.md:482 (§5 Performance)",
+              "hardware": "a GPU with 16,384 cores and 24 GB (RTX-4090 class, inferred)"}
 
 
 def parse():
@@ -49,7 +58,8 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="nsl", choices=["nsl", "reference"])
-    p.add_argument("--config", default="C2")
+    p.add_argument("--config", default="C2", choices=sorted(CONFIG_TEXT),
+                   help="C1-C5: BASELINE.json's configs (C2 = the headline); P482: the paper's own timed workload")
     p.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
     p.add_argument("--layout", default="auto", choices=["linear_f32", "quad_f32", "corner_f16", "oct_f32",
                                                         "brick_oct_f32", "tex3d_f32", "morton_oct_f32", "auto"],
@@ -125,11 +135,11 @@ def rank_workload(cfg, rank, world, frames_per_rank):
     """Weak scaling: rank r marches frames_per_rank frames with global ids r + world*k."""
     import nsl_inputs as I
     base = I.make_workload(cfg, frames=[0])
-    n_cfg = {"C1": 1, "C2": 60, "C3": 60, "C4": 240, "C5": 1024}[cfg]
-    F = frames_per_rank or n_cfg
+    n_cfg = N_PATH[cfg]
+    F = frames_per_rank or N_STEP[cfg]
     gids = [rank + world * k for k in range(F)]
-    full = I.make_workload(cfg, frames=None) if cfg in ("C1", "C2", "C3") else None
-    if cfg in ("C2", "C3") or cfg == "C1":
+    full = I.make_workload(cfg, frames=None) if cfg in ("C1", "C2", "C3", "P482") else None
+    if cfg in ("C1", "C2", "C3", "P482"):
         # extend the camera/light path periodically to world*F global frames
         idx = [g % n_cfg for g in gids]
         w = full.subset(idx)
@@ -153,7 +163,7 @@ def time_oracle(cfg, seconds, max_frames=None, stride=1):
     import oracle
     import nsl_inputs as I
     w = I.make_workload(cfg, frames=[0])
-    n_cfg = {"C1": 1, "C2": 60, "C3": 60, "C4": 240, "C5": 1024}[cfg]
+    n_cfg = N_PATH[cfg]
     rays = samples = 0
     t_total = 0.0
     frames = []
@@ -380,9 +390,9 @@ def run_sharded(args, rank, world, local):
 
     cfg = args.config
     layout = nsl.LAYOUTS[args.layout]
-    n_cfg = {"C1": 1, "C2": 60, "C3": 60, "C4": 240, "C5": 1024}[cfg]
+    n_cfg = N_PATH[cfg]
     if args.scaling == "strong":
-        F_total = args.frames or n_cfg
+        F_total = args.frames or N_STEP[cfg]
         mine = sharding.shard_frames(F_total, world, rank)
         full = I.make_workload(cfg, frames=[0]) if cfg in ("C4", "C5") else I.make_workload(cfg)
         w = (I.make_workload(cfg, frames=[g % n_cfg for g in mine]) if cfg in ("C4", "C5")
@@ -705,6 +715,10 @@ def main():
             "counts_per_rank_step": counts, "gpu_launches": launches_per_step(w, args) * K, "clocks": clk,
             "roofline": roof}
 
+    if cfg == "P482":                       # the paper's own workload: its number is context (other GPU)
+        line["vs_baseline"] = value / PAPER_P482["rays_per_s"]
+        line["paper_context"] = dict(PAPER_P482, note="vs_baseline = rays/s / the paper's 512^2 / 2 ms; a "
+                                     "different GPU, density field and (unstated) amount of work per frame")
     # end-to-end through the public host API: pinned host density in, pinned host guiding maps out
     if not args.no_e2e:
         hd = torch.from_numpy(w.volume(0)).pin_memory() if len(raw) == 1 else None

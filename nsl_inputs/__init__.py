@@ -238,9 +238,12 @@ def guide_lights(rgb=(WHITE, WHITE, WHITE)) -> List[Light]:
 def make_workload(cfg: str, frames: Optional[Sequence[int]] = None, kappa: float = 32.0,
                   perspective: bool = False, single_light: bool = False,
                   light_set: str = "guide") -> Workload:
-    """The configs of BASELINE.json (C1..C5) per DESIGN.md §"Input recipe"."""
+    """The configs of BASELINE.json (C1..C5) per DESIGN.md §"Input recipe", and P482: the
+    paper's own timed workload (§5 Performance: a 512^2 guiding map over a 400^3
+    density grid, h = 10 dx, the three surrogate lights; one frame per simulation step), on the
+    C2 plume recipe and camera path."""
     medium = Medium(extinction=kappa, albedo=1.0, hg_g=0.0)
-    idx = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}[cfg]
+    idx = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4, "P482": 5}[cfg]
     seed = 0x26040374 + idx
     if cfg == "C1":
         n, res, F = 64, 128, 1
@@ -271,6 +274,11 @@ def make_workload(cfg: str, frames: Optional[Sequence[int]] = None, kappa: float
         n, res, F = 256, 1024, 240
         cams = [orbit_camera(1.5 * f, res, res) for f in range(F)]
         specs, fvol = [("plume", float(f)) for f in range(F)], list(range(F))
+        mode, lights = LIGHTS_GUIDE, [guide_lights() for _ in range(F)]
+    elif cfg == "P482":
+        n, res, F = 400, 512, 60
+        cams = [orbit_camera(6.0 * f, res, res) for f in range(F)]
+        specs, fvol = [("plume", 0.0)], [0] * F
         mode, lights = LIGHTS_GUIDE, [guide_lights() for _ in range(F)]
     elif cfg == "C5":
         n, res, F = 512, 2048, 1024

@@ -434,18 +434,20 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
 
 }  // namespace
 
-// Occupancy block size: the smallest 2^shift (shift >= 1) whose bitmask fits
-// the per-CTA shared-memory budget (default 16 KB; NSL_OCC_BUDGET / NSL_OCC_SHIFT
-// override for experiments).
+// Occupancy block size: the smallest 2^shift, shift >= 2 (4^3-cell blocks), whose bitmask fits
+// a 64 KB budget (NSL_OCC_BUDGET / NSL_OCC_SHIFT override for experiments).  Measured with the
+// per-tile ranges (round 2, step ms): 128^3 (C2) 4^3 blocks best (2^3: march -2 % but build
+// +43 %); 256^3 (C3) 4^3 vs 8^3: march -5.2 %, step -5.0 %; C4 step -0.3 %; 512^3 (C5) 8^3 vs
+// 16^3: march -5.3 % (4^3 would need a 268 KB mask).
 OccGeom occ_geom(int nx, int ny, int nz) {
     constexpr long kMaxMask = 256 * 1024;   // hard cap (the march reads the mask through L1)
-    long budget = 16 * 1024;   // ~33 blocks per axis; measured best on C2 (profiles/r1_sweep.txt)
+    long budget = 64 * 1024;
     if (const char* e = getenv("NSL_OCC_BUDGET")) budget = atol(e);
     if (budget > kMaxMask) budget = kMaxMask;
     int forced = 0;
     if (const char* e = getenv("NSL_OCC_SHIFT")) forced = atoi(e);
     OccGeom g{};
-    for (int s = forced > 0 ? forced : 1; s <= 10; ++s) {
+    for (int s = forced > 0 ? forced : 2; s <= 10; ++s) {
         const int B = 1 << s;
         g.shift = s;
         g.nbx = (nx + 1 + B - 1) / B;

@@ -12,3 +12,4 @@ timeout 600 python bench.py --config C4 --frames 60 --steps 5 --warmup 3 > $out/
 timeout 900 python bench.py --config C4 --scaling strong --steps 3 --warmup 2 > $out/bench_C4_strong240.json 2> $out/bench_C4_strong240.err
 timeout 600 python bench.py --config C5 --steps 3 --warmup 3 --no-e2e --cpu-seconds 20 > $out/bench_C5.json 2> $out/bench_C5.err
 timeout 600 python bench.py --config C5 --layout brick_oct_f32 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $out/bench_C5_brick.json 2> $out/bench_C5_brick.err
+timeout 300 python bench.py --config P482 --steps 50 --warmup 5 > $out/bench_P482.json 2> $out/bench_P482.err

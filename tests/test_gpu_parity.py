@@ -239,6 +239,18 @@ def test_parity_C5_subsampled_full_size(nsl):
         compare_frame(w, f, g[f], gd[f], None, pixels=pix, dec=dec[f])
 
 
+def test_parity_P482_paper_workload(nsl):
+    """The paper's timed workload (512^2 over 400^3, the three surrogate lights) in
+    bench.py's launch configuration (one frame, AUTO layout, FAST), every 4th pixel against the
+    oracle, plus a DEBUG launch whose bookkeeping is compared bitwise on the same pixels."""
+    w = I.make_workload("P482", frames=[0])
+    pix = _subsample(w.height, w.width, 2)
+    g, gd, dec = run_fast(nsl, w, layout=nsl.LAYOUT_AUTO, pixels=pix)
+    compare_frame(w, 0, g[0], gd[0], None, pixels=pix, dec=dec[0])
+    d = run(nsl, w, layout=nsl.LAYOUT_AUTO, debug=True)
+    compare_frame(w, 0, d[0][0], d[1][0], d[2][0], pixels=pix)
+
+
 # ------------------------------------------------------------------ batch / determinism / sharding / host API
 @pytest.mark.parametrize("cfg,frames", [("C2", [0, 7, 30]), ("C4", [0, 1, 120])])
 def test_march_grid_order_is_bitwise_invariant(nsl, monkeypatch, cfg, frames):
