@@ -331,11 +331,12 @@ def l1_hw_ceiling(w, nsl, patterns=("footprint",), stride=0, span=1, reps=256, w
     return out
 
 
-def launches_per_step(w, args) -> int:
-    """Kernels of one timed step: volume_build + occ_finalize per distinct volume, then
-    frame_setup, tile_cull and march_kernel; the TV light model adds tv_setup and, per frame
-    group (NSL_TV_BUDGET_MB, the library's host bound), tv_sweep + tile_cull + march_kernel."""
-    n = 2 * len(w.volume_specs) + 1
+def launches_per_step(w, args, nsl, layout) -> int:
+    """Kernels of one timed step: the volume build per distinct volume (nsl_volume_build_launches:
+    occ_reset + oct_build + occ_finalize, or volume_build + occ_finalize), then frame_setup,
+    tile_cull and march_kernel; the TV light model adds tv_setup and, per frame group
+    (NSL_TV_BUDGET_MB, the library's host bound), tv_sweep + tile_cull + march_kernel."""
+    n = nsl.volume_build_launches(w.grid, layout) * len(w.volume_specs) + 1
     if args.light_model != "tv":
         return n + 2
     g = w.grid
@@ -409,6 +410,7 @@ def run_sharded(args, rank, world, local):
     n_real, H, W = w.n_frames, w.height, w.width
     animated = len(w.volume_specs) > 1
     chunk = args.chunk or (max(1, min(L, 8 if animated else 16)))
+    nbl = nsl.volume_build_launches(w.grid, layout)
     bounds = sharding.chunk_bounds(L, chunk)
     stream = torch.cuda.current_stream()
 
@@ -501,8 +503,8 @@ def run_sharded(args, rank, world, local):
                                       f"inside the step ({args.backend}, chunked, overlapped)"},
             "frames_per_s": F_total * K / t_loop, "ms_per_frame": 1e3 * t_loop / (K * F_total),
             "gather_bytes_to_rank0_per_step": int((world - 1) * L * H * W * 20),
-            "gpu_launches": K * sum(2 * (len(p._vols) if animated else 0) + 3 for p in plans if p is not None)
-                            + (K * 2 if not animated else 0),
+            "gpu_launches": K * sum(nbl * (len(p._vols) if animated else 0) + 3 for p in plans if p is not None)
+                            + (K * nbl if not animated else 0),
             "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -712,7 +714,7 @@ def main():
             "samples_per_s": counts["canonical_samples"] * world * K / t_loop,
             "ms_per_frame": ms_step / F, "frames_per_s": F * world * K / t_loop,
             "march_ms_per_step": statistics.mean(march_ms), "layout_ms_per_step": statistics.mean(layout_ms),
-            "counts_per_rank_step": counts, "gpu_launches": launches_per_step(w, args) * K, "clocks": clk,
+            "counts_per_rank_step": counts, "gpu_launches": launches_per_step(w, args, nsl, layout) * K, "clocks": clk,
             "roofline": roof}
 
     if cfg == "P482":                       # the paper's own workload: its number is context (other GPU)

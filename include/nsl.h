@@ -66,7 +66,10 @@ typedef struct {
  *               fp16 (1 x 16-B gather/sample); values rounded RNE to fp16
  *  OCT_F32    : per padded cell (i,j,k), i<=nx, j<=ny, k<=nz, the QUAD float4 of
  *               planes k and k+1 side by side (32 B: one 256-bit gather/sample),
- *               exact fp32 values; storage must be 32-B aligned
+ *               exact fp32 values; storage must be 32-B aligned.  With 4^3 / 8^3
+ *               occupancy blocks (grids up to ~640^3) only the elements of occupied
+ *               blocks are written -- the march never reads the others -- so the
+ *               bytes of empty blocks keep whatever the storage held before
  *  BRICK_OCT_F32: the OCT elements in 4x4x4-cell bricks (2 KB each, x fastest inside
  *               a brick): one 256-bit gather/sample, 3-D locality per 128-B line;
  *               storage must be 32-B aligned.  Measured against OCT: the
@@ -101,6 +104,12 @@ typedef enum {
  * taking a layout resolves AUTO this way (nsl_guiding_map_animated: OCT_F32, since its
  * per-frame builds favour the cheaper OCT build). */
 int32_t nsl_layout_resolve(const nsl_grid_desc* g, int32_t layout);
+
+/* Kernel launches one volume build (nsl_volume_upload / nsl_volume_rebuild) enqueues for grid g
+ * and layout (AUTO resolved): 3 for OCT_F32 with 4^3 / 8^3 occupancy blocks (occupancy reset,
+ * staged occupancy-gated layout, finalize), else 2 (fused layout + occupancy, finalize).
+ * -1 on an invalid grid or layout.  For launch accounting and graph sizing. */
+int32_t nsl_volume_build_launches(const nsl_grid_desc* g, int32_t layout);
 
 typedef struct nsl_volume nsl_volume;             /* opaque, immutable after upload */
 

@@ -108,7 +108,8 @@ EXPORTS = ["nsl_last_error", "nsl_version", "nsl_volume_bytes", "nsl_volume_uplo
            "nsl_guiding_map_host", "nsl_debug_frame_constants", "nsl_debug_jitter",
            "nsl_sixway_bake", "nsl_debug_bake_lights", "nsl_relight", "nsl_guide_lights",
            "nsl_guiding_map_animated", "nsl_bench_l1_gather", "nsl_bench_l1_peak", "nsl_volume_rebuild",
-           "nsl_guiding_map_host_f16", "nsl_layout_resolve", "nsl_debug_tex_filter"]
+           "nsl_guiding_map_host_f16", "nsl_layout_resolve", "nsl_debug_tex_filter",
+           "nsl_volume_build_launches"]
 
 
 class BakeS(ctypes.Structure):
@@ -134,6 +135,8 @@ def lib():
     L.nsl_version.restype = ctypes.c_char_p
     L.nsl_volume_bytes.argtypes = [P(GridDesc), i32]
     L.nsl_layout_resolve.argtypes = [P(GridDesc), i32]
+    L.nsl_volume_build_launches.restype = i32
+    L.nsl_volume_build_launches.argtypes = [P(GridDesc), i32]
     L.nsl_debug_tex_filter.argtypes = [P(GridDesc), vp, vp, i32, vp, vp]
     L.nsl_volume_bytes.restype = ctypes.c_size_t
     L.nsl_volume_upload.argtypes = [P(GridDesc), vp, i32, i32, vp, ctypes.c_size_t, vp, P(vp)]
@@ -229,6 +232,15 @@ def layout_resolve(grid, layout: int = LAYOUT_DEFAULT) -> int:
     if r < 0:
         raise NslError("nsl_layout_resolve: invalid grid")
     return r
+
+
+def volume_build_launches(grid, layout: int = LAYOUT_DEFAULT) -> int:
+    """Kernel launches of one volume build (nsl_volume_build_launches: 3 for the staged OCT
+    build, else 2)."""
+    n = lib().nsl_volume_build_launches(ctypes.byref(grid_desc(grid)), layout)
+    if n < 0:
+        raise NslError("nsl_volume_build_launches: invalid grid/layout")
+    return n
 
 
 def volume_bytes(grid, layout: int = LAYOUT_DEFAULT) -> int:

@@ -310,6 +310,13 @@ int32_t nsl_layout_resolve(const nsl_grid_desc* g, int32_t layout) {
     return resolve_layout(g, layout);
 }
 
+int32_t nsl_volume_build_launches(const nsl_grid_desc* g, int32_t layout) {
+    if (check_grid(g) != NSL_OK) return -1;
+    layout = resolve_layout(g, layout);
+    if (check_layout(layout) != NSL_OK) return -1;
+    return staged_oct_build(layout, occ_geom(g->nx, g->ny, g->nz)) ? 3 : 2;
+}
+
 size_t nsl_volume_bytes(const nsl_grid_desc* g, int32_t layout) {
     layout = resolve_layout(g, layout);
     if (check_grid(g) != NSL_OK || check_layout(layout) != NSL_OK) return 0;

@@ -25,6 +25,9 @@ struct OccGeom {
 //   [mask: words u32][slab_min: nbz x (bx, by) int32][slab_max: nbz x (bx, by) int32]
 // slab box of z-block slab bz = the x/y range of its non-empty blocks (min > max: empty).
 OccGeom occ_geom(int nx, int ny, int nz);
+// OCT volumes with 4^3 / 8^3 occupancy blocks build through the staged, occupancy-gated kernel
+// (3 launches: occ_reset, oct_build, occ_finalize); every other layout through the fused one (2)
+bool staged_oct_build(int layout, const OccGeom& g);
 
 // Per-volume description handed to the frame-setup kernel.
 struct VolDesc {

@@ -6,7 +6,10 @@
 // are fully coalesced, the gathers from the x-fastest raw grid are
 // sector-coalesced along x.  HBM-bound: bytes = raw read + layout write.
 #include <cstdlib>
+#include <cstring>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include "nsl_internal.cuh"
@@ -432,6 +435,148 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
     if (threadIdx.x == 0) *invalid = nbad;
 }
 
+// ---------------------------------------------------------------- OCT, staged and occupancy-gated
+// (blocks of 4^3 or 8^3 cells).  The march reads an element only after its occupancy block's bit
+// is set (sample(), sampler.cuh), and the bit is "some corner of some cell of the block is != 0",
+// so the elements of empty blocks -- ~80 % of a plume's -- are never read and are not written:
+// the build's 32 B/cell of writes drop ~5x.  One CTA = a 32 (x) x 8 (y) tile of cells, one block
+// layer (B cells of z) per iteration: the layer's padded corner voxels, (32+1) x (8+1) x (B+1),
+// are staged in shared memory by cp.async (zero-fill outside 1..n: the apron, no branches),
+// then each thread tests its cell column's corners (the block bit: a warp ballot + a shared OR
+// per block row), counts its own voxels that are negative / non-finite, and writes its B
+// elements if its block is occupied.  The block bits and per-row x extents go to the build
+// scratch by atomics, in the occupancy role's format, so occ_finalize_kernel is unchanged;
+// occ_reset_kernel clears them first (the build waits for it before its first atomic).  The
+// separate latency-bound occupancy scan (one CTA per block row) disappears: the raw grid is
+// read once, through shared memory.
+// staged row: 40 voxels from raw x = i0 - 4 (a TMA box must start 16-B aligned in x): padded
+// x = i0 + t at column t + kStX0
+constexpr int kStTx = 32, kStTy = 8, kStRw = 40, kStX0 = 3;
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const float* src, bool real) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(saddr), "l"(src), "r"(real ? 4 : 0)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(256) occ_reset_kernel(OccGeom g, uint32_t* __restrict__ scratch) {
+    pdl_trigger();
+    const int nbits = g.rows * g.rowwords;
+    for (int t = blockIdx.x * 256 + threadIdx.x; t < nbits + g.rows; t += gridDim.x * 256) {
+        if (t < nbits) scratch[t] = 0u;
+        else reinterpret_cast<int4*>(scratch + g.info_off)[t - nbits] = make_int4(0x7fffffff, -1, 0, 0);
+    }
+}
+
+// TMA: the layer's (40, 9, B+1) raw box at raw (i0-4, j0-1, k0-1), one bulk-tensor copy issued by
+// one thread; out-of-range voxels (the apron and beyond) arrive as zeros (OOB fill NONE).
+__device__ __forceinline__ void tma_box3(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+}
+
+template <int SHIFT, bool TMA>
+__global__ void __launch_bounds__(256) oct_build_kernel(const __grid_constant__ CUtensorMap map, Raw r,
+                                                        float* __restrict__ out, OccGeom g,
+                                                        uint32_t* __restrict__ scratch, int tiles_x) {
+    constexpr int B = 1 << SHIFT, NP = B + 1, RW = kStRw, RH = kStTy + 1, PL = RW * RH;
+    __shared__ __align__(128) float brick[NP * PL];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t s_any[kStTy >> SHIFT > 0 ? kStTy >> SHIFT : 1];
+    pdl_trigger();
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+    const int i0 = (blockIdx.x % tiles_x) * kStTx, j0 = (blockIdx.x / tiles_x) * kStTy;
+    const int i = i0 + lane, j = j0 + wy, qx = r.nx + 1, qy = r.ny + 1;
+    const size_t plane = (size_t)qx * qy;
+    const int nlayers = (r.nz + 1 + B - 1) >> SHIFT;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(brick);
+    const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&bar);
+    const uint32_t group = ((1u << B) - 1u) << (lane & ~(B - 1));
+    const float* bp = brick + wy * RW + kStX0 + lane;
+    if (TMA && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    bool waited = false;
+    uint32_t phase = 0;
+    for (int zb = blockIdx.y; zb < nlayers; zb += gridDim.y, phase ^= 1u) {
+        const int k0 = zb << SHIFT;
+        if (TMA) {
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the last layer's reads
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar),
+                             "r"((uint32_t)(NP * PL * 4))
+                             : "memory");
+                tma_box3(sbase, &map, i0 - 4, j0 - 1, k0 - 1, sbar);
+            }
+        } else {                 // one staged row (c, y) per warp iteration: lanes 0-31 + lane 0's x = 32
+            const bool xr = i >= 1 && i <= r.nx, xr32 = i0 + 32 <= r.nx;
+            for (int row = wy; row < NP * RH; row += 8) {
+                const int c = row / RH, y = row - c * RH, pk = k0 + c, pj = j0 + y;
+                const bool rr = pj >= 1 && pj <= r.ny && pk >= 1 && pk <= r.nz;
+                const float* src = r.v + (rr ? ((size_t)(pk - 1) * r.ny + (pj - 1)) * r.nx + (i0 - 1) : 0);
+                const uint32_t dst = sbase + 4u * (row * RW + kStX0 + lane);
+                cp_async4(dst, rr && xr ? src + lane : r.v, rr && xr);
+                if (lane == 0) cp_async4(dst + 128u, rr && xr32 ? src + 32 : r.v, rr && xr32);
+            }
+        }
+        if (threadIdx.x < (kStTy >> SHIFT > 0 ? kStTy >> SHIFT : 1)) s_any[threadIdx.x] = 0u;
+        if (TMA) mbar_wait(sbar, phase);
+        else asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        bool any = false;
+        int bad = 0;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+            const float* p = bp + c * PL;
+            any |= (p[0] != 0.0f) | (p[1] != 0.0f) | (p[RW] != 0.0f) | (p[RW + 1] != 0.0f);
+            if (c < B) bad += !(p[0] >= 0.0f) || isinf(p[0]);     // own voxel (apron zeros: not bad)
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, any);
+        if (lane == 0 && bal) atomicOr(s_any + (wy >> SHIFT), bal);
+        bad = __reduce_add_sync(0xffffffffu, bad);
+        __syncthreads();
+        if (!waited) {                                             // occ_reset_kernel's writes
+            pdl_wait();
+            waited = true;
+        }
+        const bool occ = (s_any[wy >> SHIFT] & group) != 0;
+        int* info = reinterpret_cast<int*>(scratch + g.info_off);
+        if (occ && (wy & (B - 1)) == 0 && (lane & (B - 1)) == 0) {   // one thread per occupied block
+            const int bx = i >> SHIFT, row = zb * g.nby + (j >> SHIFT);
+            atomicOr(scratch + (size_t)row * g.rowwords + (bx >> 5), 1u << (bx & 31));
+            atomicMin(info + 4 * row, bx);
+            atomicMax(info + 4 * row + 1, bx);
+        }
+        if (lane == 0 && bad) atomicAdd(info + 4 * (zb * g.nby + (j >> SHIFT)) + 2, bad);
+        if (occ && i < qx && j < qy) {
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+                const int k = k0 + c;
+                if (k > r.nz) break;
+                const float* p = bp + c * PL;
+                const float* q = p + PL;
+                // (c000, c100 - c000, c010, c110 - c010 | plane k + 1): as layout_oct_cta
+                const float e[8] = {p[0], __fsub_rn(p[1], p[0]), p[RW], __fsub_rn(p[RW + 1], p[RW]),
+                                    q[0], __fsub_rn(q[1], q[0]), q[RW], __fsub_rn(q[RW + 1], q[RW])};
+                st256(out + 8 * ((size_t)k * plane + (size_t)j * qx + i), e);
+            }
+        }
+        __syncthreads();                                           // brick and s_any are reused
+    }
+}
+
 }  // namespace
 
 // Occupancy block size: the smallest 2^shift, shift >= 2 (4^3-cell blocks), whose bitmask fits
@@ -475,10 +620,70 @@ bool pdl_enabled() {
     return on;
 }
 
-// Volume build: one fused launch (layout + occupancy rows), then the PDL-launched finalize.
+// NSL_OCT_DENSE=1: OCT through the fused dense build (the A/B baseline of the staged build)
+static bool oct_dense_forced() {
+    static const bool on = [] {
+        const char* e = getenv("NSL_OCT_DENSE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+// The raw grid as a 3-D TMA tensor (x fastest) with a (36, 9, B+1) box; false (-> the cp.async
+// staging) when the driver entry point is missing, the base is not 16-B aligned, the x pitch is
+// not a multiple of 16 B (n_x % 4 != 0), or the encode fails.  NSL_BUILD_TMA=0 forces cp.async.
+static bool encode_raw_map(CUtensorMap& map, const float* raw, int nx, int ny, int nz, int B) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        const char* e = getenv("NSL_BUILD_TMA");
+        if (e && e[0] == '0') return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    memset(&map, 0, sizeof map);
+    if (!encode || reinterpret_cast<uintptr_t>(raw) % 16 || nx % 4) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+    const cuuint64_t strides[2] = {(cuuint64_t)nx * 4, (cuuint64_t)nx * ny * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)kStRw, (cuuint32_t)(kStTy + 1), (cuuint32_t)(B + 1)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(raw), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool staged_oct_build(int layout, const OccGeom& g) {
+    return layout == kOctF32 && (g.shift == 2 || g.shift == 3) && !oct_dense_forced();
+}
+
+// Volume build: one fused launch (layout + occupancy rows), then the PDL-launched finalize;
+// OCT with 4^3 / 8^3 blocks: occ_reset, the staged occupancy-gated build (PDL), the finalize.
 cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storage, uint32_t* scratch,
                                 unsigned long long* invalid, cudaStream_t s) {
     Raw r{raw, v.nx, v.ny, v.nz};
+    if (staged_oct_build(v.layout, v.og)) {
+        const int reset_n = v.og.rows * (v.og.rowwords + 1);
+        occ_reset_kernel<<<(reset_n + 255) / 256 < 1024 ? (reset_n + 255) / 256 : 1024, 256, 0, s>>>(v.og, scratch);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const int tiles_x = (v.nx + 1 + kStTx - 1) / kStTx, tiles_y = (v.ny + 1 + kStTy - 1) / kStTy;
+        const int B = 1 << v.og.shift, nlayers = (v.nz + 1 + B - 1) / B, per = 8 / B;   // >= 8 cells of z per CTA
+        const dim3 grid((unsigned)(tiles_x * tiles_y), (unsigned)((nlayers + per - 1) / per));
+        CUtensorMap map;
+        const bool tma = encode_raw_map(map, raw, v.nx, v.ny, v.nz, B);
+        float* o = static_cast<float*>(storage);
+        if (v.og.shift == 2)
+            e = tma ? launch_pdl(oct_build_kernel<2, true>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x)
+                    : launch_pdl(oct_build_kernel<2, false>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x);
+        else
+            e = tma ? launch_pdl(oct_build_kernel<3, true>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x)
+                    : launch_pdl(oct_build_kernel<3, false>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x);
+        if (e != cudaSuccess) return e;
+        const unsigned fin_ctas = 1u + (unsigned)((v.og.words + kFinThreads / 32 - 1) / (kFinThreads / 32));
+        return launch_pdl(occ_finalize_kernel, dim3(fin_ctas), dim3(kFinThreads), (size_t)v.og.nbz * 16, s, v.og,
+                          (const uint32_t*)scratch, const_cast<uint32_t*>(v.occ), const_cast<int32_t*>(v.aabb), invalid);
+    }
     const int plane = v.layout == kLinearF32 ? (v.nx + 2) * (v.ny + 2) : (v.nx + 1) * (v.ny + 1);
     const int planes = v.layout == kCornerF16 || v.layout == kOctF32 ? v.nz + 1 : v.nz + 2;
     const bool per_elem = v.layout == kBrickOctF32 || v.layout == kMortonOctF32;   // one thread per element

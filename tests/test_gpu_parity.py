@@ -611,3 +611,82 @@ def test_tile_range_random_batches(nsl):
         g, gd, dec = run_fast(nsl, w, layout=3)
         for f in (0, 1049, F - 1):
             compare_frame(w, f, g[f], gd[f], None, dec=dec[f])
+
+
+# ------------------------------------------------------------------ occupancy-gated OCT build
+def _oct_reference(vals):
+    """OCT elements [k][j][i][8] of the padded grid, written out from DESIGN.md §6's definition."""
+    nz, ny, nx = vals.shape
+    p = np.zeros((nz + 2, ny + 2, nx + 2), np.float32)
+    p[1:-1, 1:-1, 1:-1] = vals
+    c = lambda dk, dj, di: p[dk:dk + nz + 1, dj:dj + ny + 1, di:di + nx + 1]
+    return np.stack([c(0, 0, 0), c(0, 0, 1) - c(0, 0, 0), c(0, 1, 0), c(0, 1, 1) - c(0, 1, 0),
+                     c(1, 0, 0), c(1, 0, 1) - c(1, 0, 0), c(1, 1, 0), c(1, 1, 1) - c(1, 1, 0)], axis=-1)
+
+
+def _cropped_c1(nx, ny, nz):
+    """C1's workload on an (nx, ny, nz) crop of its puff (a grid whose x pitch is not a multiple
+    of 16 B takes the build's cp.async staging instead of TMA)."""
+    w = I.make_workload("C1")
+    vals = np.ascontiguousarray(w.volume(0)[:nz, :ny, :nx])
+    w2 = replace(w, grid=I.Grid(nx, ny, nz, w.grid.origin, w.grid.voxel_width), _cache={0: vals})
+    return w2, vals
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "C1_crop_61x50x47"])
+def test_oct_build_writes_exactly_the_occupied_blocks(nsl, case):
+    """Storage pre-filled with NaN bytes: after the build, every element of an occupied block
+    (block bit = some corner of the block's cells != 0, recomputed here from the density) equals
+    the OCT definition, the mask equals the recomputed bits, the elements of empty blocks are
+    untouched, and the maps equal those of a zero-filled storage bit for bit (elements of empty
+    blocks are never read)."""
+    import torch
+    if case.startswith("C1_crop"):
+        w, vals = _cropped_c1(61, 50, 47)
+    else:
+        w = I.make_workload(case, frames=[0])
+        vals = w.volume(0)
+    nz, ny, nx = vals.shape
+    assert nsl.volume_build_launches(w.grid, 3) == 3
+    nb_bytes = nsl.volume_bytes(w.grid, 3)
+    st_nan = torch.full((nb_bytes,), 0xFF, dtype=torch.uint8, device="cuda")
+    st_zero = torch.zeros((nb_bytes,), dtype=torch.uint8, device="cuda")
+    raw = torch.from_numpy(vals).cuda()
+    maps = []
+    for st in (st_nan, st_zero):
+        vol = nsl.Volume(w.grid, raw, 3, storage=st)
+        plan = nsl.make_plan(w, [vol])
+        outs = nsl.alloc_outputs(1, w.height, w.width, debug=True)
+        plan.execute(outs[0], outs[1], outs[2])
+        torch.cuda.synchronize()
+        maps.append([o.cpu().numpy() for o in outs])
+    for a, b in zip(*maps):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    compare_frame(w, 0, maps[0][0][0], maps[0][1][0], maps[0][2][0], vals=vals)
+    # block geometry: the smallest shift >= 2 whose mask fits 64 KB (volume.cu occ_geom)
+    s = 2
+    while True:
+        nbx, nby, nbz = ((d + 1 + (1 << s) - 1) >> s for d in (nx, ny, nz))
+        if ((nbx * nby * nbz + 31) // 32 + 3) // 4 * 4 * 4 <= 64 * 1024:
+            break
+        s += 1
+    B = 1 << s
+    p = np.zeros((nbz * B + 1, nby * B + 1, nbx * B + 1), bool)
+    p[1:nz + 1, 1:ny + 1, 1:nx + 1] = vals != 0
+    occ = np.zeros((nbz, nby, nbx), bool)        # block (bz, by, bx) covers voxels [bB, bB + B] per axis
+    for bz in range(nbz):
+        for by in range(nby):
+            for bx in range(nbx):
+                occ[bz, by, bx] = p[bz * B:bz * B + B + 1, by * B:by * B + B + 1, bx * B:bx * B + B + 1].any()
+    host = st_nan.cpu().numpy()
+    ncell = (nx + 1) * (ny + 1) * (nz + 1)
+    body = host[:ncell * 32].view(np.float32).reshape(nz + 1, ny + 1, nx + 1, 8)
+    moff = (ncell * 32 + 255) // 256 * 256
+    nbits = nbx * nby * nbz
+    words = host[moff:moff + (nbits + 31) // 32 * 4].view(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:nbits].astype(bool).reshape(nbz, nby, nbx)
+    assert np.array_equal(bits, occ)
+    cell_occ = np.repeat(np.repeat(np.repeat(occ, B, 0), B, 1), B, 2)[:nz + 1, :ny + 1, :nx + 1]
+    ref = _oct_reference(vals)
+    assert np.array_equal(body[cell_occ].view(np.uint32), ref[cell_occ].view(np.uint32))
+    assert np.isnan(body[~cell_occ]).all()          # never written: the NaN fill survives
