@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
                                                                    uint32_t* __restrict__ mask,
                                                                    int32_t* __restrict__ aabb,
                                                                    unsigned long long* __restrict__ invalid) {
+    // grid = 1 CTA when the mask was written by the build itself (oct_build_kernel)
     pdl_trigger();
     pdl_wait();
     const int32_t* info = reinterpret_cast<const int32_t*>(scratch + g.info_off);
@@ -392,44 +393,49 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
         if (lane == 0) mask[w] = word;
         return;
     }
-    extern __shared__ int32_t sl[];                   // [4][nbz]: x0, y0, x1, y1
+    // CTA 0: one warp per z slab reduces its rows' records (x extent, row occupied, invalid
+    // voxels) with warp reductions into the slab box; the AABB from the slab boxes
     __shared__ int am[6];
     __shared__ unsigned long long nbad;
-    for (int i = threadIdx.x; i < 4 * g.nbz; i += kFinThreads) sl[i] = i < 2 * g.nbz ? 0x7f7f7f7f : -1;
     if (threadIdx.x < 6) am[threadIdx.x] = threadIdx.x < 3 ? 0x7f7f7f7f : -1;
     if (threadIdx.x == 0) nbad = 0ull;
     __syncthreads();
+    int32_t* smin = reinterpret_cast<int32_t*>(mask + g.words);
+    int32_t* smax = smin + 2 * g.nbz;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long mybad = 0ull;
-    for (int rid = threadIdx.x; rid < g.rows; rid += kFinThreads) {
-        const int4 rec = __ldg(reinterpret_cast<const int4*>(info) + rid);
-        mybad += (unsigned long long)rec.z;
-        if (rec.y >= 0) {
-            const int by = rid % g.nby, bz = rid / g.nby;
-            atomicMin(sl + bz, rec.x);
-            atomicMin(sl + g.nbz + bz, by);
-            atomicMax(sl + 2 * g.nbz + bz, rec.y);
-            atomicMax(sl + 3 * g.nbz + bz, by);
+    for (int bz = warp; bz < g.nbz; bz += kFinThreads / 32) {
+        int x0 = 0x7f7f7f7f, y0 = 0x7f7f7f7f, x1 = -1, y1 = -1;
+        for (int by = lane; by < g.nby; by += 32) {
+            const int4 rec = __ldg(reinterpret_cast<const int4*>(info) + bz * g.nby + by);
+            mybad += (unsigned long long)rec.z;
+            if (rec.y >= 0) {
+                x0 = min(x0, rec.x);
+                x1 = max(x1, rec.y);
+                y0 = min(y0, by);
+                y1 = max(y1, by);
+            }
+        }
+        x0 = __reduce_min_sync(0xffffffffu, x0);
+        y0 = __reduce_min_sync(0xffffffffu, y0);
+        x1 = __reduce_max_sync(0xffffffffu, x1);
+        y1 = __reduce_max_sync(0xffffffffu, y1);
+        if (lane == 0) {
+            smin[2 * bz] = x0;
+            smin[2 * bz + 1] = y0;
+            smax[2 * bz] = x1;
+            smax[2 * bz + 1] = y1;
+            if (x1 >= 0) {
+                atomicMin(am + 0, x0);
+                atomicMin(am + 1, y0);
+                atomicMin(am + 2, bz);
+                atomicMax(am + 3, x1);
+                atomicMax(am + 4, y1);
+                atomicMax(am + 5, bz);
+            }
         }
     }
     if (mybad) atomicAdd(&nbad, mybad);
-    __syncthreads();
-    int32_t* smin = reinterpret_cast<int32_t*>(mask + g.words);
-    int32_t* smax = smin + 2 * g.nbz;
-    for (int bz = threadIdx.x; bz < g.nbz; bz += kFinThreads) {
-        const int x0 = sl[bz], y0 = sl[g.nbz + bz], x1 = sl[2 * g.nbz + bz], y1 = sl[3 * g.nbz + bz];
-        smin[2 * bz] = x0;
-        smin[2 * bz + 1] = y0;
-        smax[2 * bz] = x1;
-        smax[2 * bz + 1] = y1;
-        if (x1 >= 0) {
-            atomicMin(am + 0, x0);
-            atomicMin(am + 1, y0);
-            atomicMin(am + 2, bz);
-            atomicMax(am + 3, x1);
-            atomicMax(am + 4, y1);
-            atomicMax(am + 5, bz);
-        }
-    }
     __syncthreads();
     if (threadIdx.x < 6) aabb[threadIdx.x] = am[threadIdx.x];
     if (threadIdx.x == 0) *invalid = nbad;
@@ -444,11 +450,12 @@ __global__ void __launch_bounds__(kFinThreads) occ_finalize_kernel(OccGeom g, co
 // are staged in shared memory by cp.async (zero-fill outside 1..n: the apron, no branches),
 // then each thread tests its cell column's corners (the block bit: a warp ballot + a shared OR
 // per block row), counts its own voxels that are negative / non-finite, and writes its B
-// elements if its block is occupied.  The block bits and per-row x extents go to the build
-// scratch by atomics, in the occupancy role's format, so occ_finalize_kernel is unchanged;
-// occ_reset_kernel clears them first (the build waits for it before its first atomic).  The
-// separate latency-bound occupancy scan (one CTA per block row) disappears: the raw grid is
-// read once, through shared memory.
+// elements if its block is occupied.  The block bits go straight into the occupancy mask and the
+// per-row x extents into the scratch records (the occupancy role's format) by atomics;
+// occ_reset_kernel clears both first (the build waits for it before its first atomic) and
+// occ_finalize_kernel's CTA 0 alone turns the records into slab boxes and the AABB.  The
+// separate latency-bound occupancy scan (one CTA per block row) and the mask assembly
+// disappear: the raw grid is read once, through shared memory (TMA).
 // staged row: 40 voxels from raw x = i0 - 4 (a TMA box must start 16-B aligned in x): padded
 // x = i0 + t at column t + kStX0
 constexpr int kStTx = 32, kStTy = 8, kStRw = 40, kStX0 = 3;
@@ -457,12 +464,12 @@ __device__ __forceinline__ void cp_async4(uint32_t saddr, const float* src, bool
                  : "memory");
 }
 
-__global__ void __launch_bounds__(256) occ_reset_kernel(OccGeom g, uint32_t* __restrict__ scratch) {
+__global__ void __launch_bounds__(256) occ_reset_kernel(OccGeom g, uint32_t* __restrict__ mask,
+                                                        uint32_t* __restrict__ scratch) {
     pdl_trigger();
-    const int nbits = g.rows * g.rowwords;
-    for (int t = blockIdx.x * 256 + threadIdx.x; t < nbits + g.rows; t += gridDim.x * 256) {
-        if (t < nbits) scratch[t] = 0u;
-        else reinterpret_cast<int4*>(scratch + g.info_off)[t - nbits] = make_int4(0x7fffffff, -1, 0, 0);
+    for (int t = blockIdx.x * 256 + threadIdx.x; t < g.words + g.rows; t += gridDim.x * 256) {
+        if (t < g.words) mask[t] = 0u;
+        else reinterpret_cast<int4*>(scratch + g.info_off)[t - g.words] = make_int4(0x7fffffff, -1, 0, 0);
     }
 }
 
@@ -488,7 +495,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 template <int SHIFT, bool TMA>
 __global__ void __launch_bounds__(256) oct_build_kernel(const __grid_constant__ CUtensorMap map, Raw r,
                                                         float* __restrict__ out, OccGeom g,
-                                                        uint32_t* __restrict__ scratch, int tiles_x) {
+                                                        uint32_t* __restrict__ mask, uint32_t* __restrict__ scratch,
+                                                        int tiles_x) {
     constexpr int B = 1 << SHIFT, NP = B + 1, RW = kStRw, RH = kStTy + 1, PL = RW * RH;
     __shared__ __align__(128) float brick[NP * PL];
     __shared__ __align__(8) uint64_t bar;
@@ -554,8 +562,8 @@ __global__ void __launch_bounds__(256) oct_build_kernel(const __grid_constant__ 
         const bool occ = (s_any[wy >> SHIFT] & group) != 0;
         int* info = reinterpret_cast<int*>(scratch + g.info_off);
         if (occ && (wy & (B - 1)) == 0 && (lane & (B - 1)) == 0) {   // one thread per occupied block
-            const int bx = i >> SHIFT, row = zb * g.nby + (j >> SHIFT);
-            atomicOr(scratch + (size_t)row * g.rowwords + (bx >> 5), 1u << (bx & 31));
+            const int bx = i >> SHIFT, row = zb * g.nby + (j >> SHIFT), b = row * g.nbx + bx;
+            atomicOr(mask + (b >> 5), 1u << (b & 31));
             atomicMin(info + 4 * row, bx);
             atomicMax(info + 4 * row + 1, bx);
         }
@@ -663,8 +671,9 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
                                 unsigned long long* invalid, cudaStream_t s) {
     Raw r{raw, v.nx, v.ny, v.nz};
     if (staged_oct_build(v.layout, v.og)) {
-        const int reset_n = v.og.rows * (v.og.rowwords + 1);
-        occ_reset_kernel<<<(reset_n + 255) / 256 < 1024 ? (reset_n + 255) / 256 : 1024, 256, 0, s>>>(v.og, scratch);
+        const int reset_n = v.og.words + v.og.rows;
+        occ_reset_kernel<<<(reset_n + 255) / 256 < 1024 ? (reset_n + 255) / 256 : 1024, 256, 0, s>>>(
+            v.og, const_cast<uint32_t*>(v.occ), scratch);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         const int tiles_x = (v.nx + 1 + kStTx - 1) / kStTx, tiles_y = (v.ny + 1 + kStTy - 1) / kStTy;
@@ -673,15 +682,15 @@ cudaError_t launch_volume_build(const float* raw, const VolDesc& v, void* storag
         CUtensorMap map;
         const bool tma = encode_raw_map(map, raw, v.nx, v.ny, v.nz, B);
         float* o = static_cast<float*>(storage);
+        uint32_t* mask = const_cast<uint32_t*>(v.occ);
         if (v.og.shift == 2)
-            e = tma ? launch_pdl(oct_build_kernel<2, true>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x)
-                    : launch_pdl(oct_build_kernel<2, false>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x);
+            e = tma ? launch_pdl(oct_build_kernel<2, true>, grid, dim3(256), 0, s, map, r, o, v.og, mask, scratch, tiles_x)
+                    : launch_pdl(oct_build_kernel<2, false>, grid, dim3(256), 0, s, map, r, o, v.og, mask, scratch, tiles_x);
         else
-            e = tma ? launch_pdl(oct_build_kernel<3, true>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x)
-                    : launch_pdl(oct_build_kernel<3, false>, grid, dim3(256), 0, s, map, r, o, v.og, scratch, tiles_x);
+            e = tma ? launch_pdl(oct_build_kernel<3, true>, grid, dim3(256), 0, s, map, r, o, v.og, mask, scratch, tiles_x)
+                    : launch_pdl(oct_build_kernel<3, false>, grid, dim3(256), 0, s, map, r, o, v.og, mask, scratch, tiles_x);
         if (e != cudaSuccess) return e;
-        const unsigned fin_ctas = 1u + (unsigned)((v.og.words + kFinThreads / 32 - 1) / (kFinThreads / 32));
-        return launch_pdl(occ_finalize_kernel, dim3(fin_ctas), dim3(kFinThreads), (size_t)v.og.nbz * 16, s, v.og,
+        return launch_pdl(occ_finalize_kernel, dim3(1), dim3(kFinThreads), (size_t)v.og.nbz * 16, s, v.og,
                           (const uint32_t*)scratch, const_cast<uint32_t*>(v.occ), const_cast<int32_t*>(v.aabb), invalid);
     }
     const int plane = v.layout == kLinearF32 ? (v.nx + 2) * (v.ny + 2) : (v.nx + 1) * (v.ny + 1);
