@@ -353,10 +353,11 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
         const bool front_fast = !DEBUG && PROJ == 0 && sp.front_ok && m_lo <= m_hi && !r.in(v, 1);
         const bool paired = NL == 3 || (NL == 0 && sp.pair12 != 0);
         const int n_lights = NL ? NL : mc.n_lights;
-        float nf = (float)m_lo;
-        for (int n = m_lo; n <= m_hi; ++n, nf += 1.0f) {
+        // positions from (float)n (one ALU I2FP per step): a separate float counter is spilled at 40
+        // registers (a local load + load + store per primary step; C2 march -1.3 %)
+        for (int n = m_lo; n <= m_hi; ++n) {
             float t, x, y, z;
-            r.atf(nf, t, x, y, z);
+            r.atf((float)n, t, x, y, z);
             if (COUNT) ++c_tp;
             const float rho = sample<LAYOUT, COUNT>(v, x, y, z, c_gath);
             if (rho > 0.0f) {
