@@ -194,6 +194,8 @@ MarchConst make_const(int n_lights, int light_mode, const nsl_medium* med, const
     mc.axis[1] = m->guide_axis[1];
     mc.axis[2] = m->guide_axis[2];
     mc.light_model = m->light_model;
+    mc.frame_major = 0;
+    mc.split_k = 0;
     return mc;
 }
 
@@ -511,6 +513,36 @@ struct Prepared {
     size_t tv_buf_bytes() const { return sizeof(float2) * tv_slot_elems() * tv_slots * (size_t)tv_group; }
 };
 
+// Split march (march.cu march_split_kernel) for small FAST guide-set orthographic batches, whose
+// one-warp-per-tile grid would leave most SMs idle (at most a third of a wave of warps): returns the
+// bound K on the occupied samples of a ray -- at most the in-support steps, floor(support
+// diagonal / step) + 1 in index units, and at most max_steps -- or 0 (no split: too many warps,
+// another light set or model, perspective, the texture layout, or K above the shared-memory
+// budget).  The split kernel's maps are bitwise those of march_kernel.  NSL_SPLIT=0/1 forces it
+// off / on (when eligible).
+static int32_t march_split_k(const Prepared& P) {
+    const char* e = getenv("NSL_SPLIT");
+    if (e && e[0] == '0') return 0;
+    if (P.proj != 0 || P.layout == kTex3dF32 || P.mc.light_model != NSL_LIGHT_MARCH ||
+        P.mc.light_mode != NSL_LIGHTS_GUIDE || P.n_lights != 3)
+        return 0;
+    const long long warps = (long long)P.F * ((P.W + 7) / 8) * ((P.H + 3) / 4);
+    // measured (profiles/r2_ab6): C1 (512 warps) step 0.043 -> 0.033 ms; the paper's 512^2 x 400^3
+    // frame (8192 warps, over one wave) +4 % (the split's shared memory halves the resident warps)
+    const long long third_wave = 148LL * 16;
+    if (!(e && e[0] == '1') && warps > third_wave) return 0;
+    double kmax = 0.0;
+    for (const FrameIn& f : P.frames) {
+        const double d = std::sqrt((f.vol.nx + 1.0) * (f.vol.nx + 1.0) + (f.vol.ny + 1.0) * (f.vol.ny + 1.0) +
+                                   (f.vol.nz + 1.0) * (f.vol.nz + 1.0));
+        const double k = std::floor(d * (double)f.vol.dx / (double)P.mc.h * (1.0 + 1e-6)) + 2.0;
+        kmax = k > kmax ? k : kmax;
+    }
+    if (kmax > (double)P.mc.Ncap) kmax = (double)P.mc.Ncap;
+    if (kmax < 1.0 || kmax > (double)march_split_max_k()) return 0;
+    return (int32_t)kmax;
+}
+
 // Host bounds of the V2 lattice dims: the projection of the support box on
 // any unit vector is at most its diagonal, so A, B <= diag + 5 and K <= diag / ell + 5 with
 // ell = h_l / voxel_width (unit lights); +6 (and 1e-5 on ell) keeps every device value below.
@@ -601,6 +633,7 @@ static nsl_status prepare(const nsl_volume* const* vols, int32_t n_vols, const i
     }
     P.mc = make_const(n_lights, light_mode, med, m);
     P.mc.frame_major = march_frame_major(P.frames);
+    P.mc.split_k = march_split_k(P);
     tv_geometry(vols, n_vols, P);
     return NSL_OK;
 }

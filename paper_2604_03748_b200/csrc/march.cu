@@ -502,6 +502,170 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
     }
 }
 
+// Small batches (a single frame, the paper's per-frame use): one warp per 8x4 tile leaves
+// most of the GPU idle and the time is the longest ray's serial light marches.  The split march
+// gives each 8x4 tile kSplit warps: every warp runs the tile's primary march (cheap, identical),
+// warp w takes the light marches of the occupied samples k with k % kSplit == w and parks their
+// transmittances T^l_k in shared memory; warp 0 then folds S_l = fma(A_k, T^l_k, S_l) in k order
+// -- the same operations in the same order as march_kernel's FAST guide-set path, so the maps are
+// bitwise those of march_kernel (tests/test_gpu_parity.py test_split_march_is_bitwise_identical).
+constexpr int kSplit = 4;
+constexpr int kSplitMaxK = 96;                     // 4 x 96 x 32 floats = 48 KB of shared memory
+template <int LAYOUT>
+__global__ void __launch_bounds__(32 * kSplit) march_split_kernel(const FrameParams* __restrict__ fps,
+                                                                  const MarchConst mc, float4* __restrict__ out_rgbt,
+                                                                  float* __restrict__ out_depth, int W, int H,
+                                                                  const TileCull* __restrict__ cull, int tiles_x,
+                                                                  int tiles_y) {
+    extern __shared__ float s_split[];            // [4][K][32]: A_k, T^0_k, T^1_k, T^2_k
+    const int K = mc.split_k;
+    const int f = (int)blockIdx.z;
+    pdl_wait();                                    // FrameParams and the cull records
+    const FrameParams& sp = fps[f];
+    const int wv = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x0 = (int)blockIdx.x * kWarpW, y0 = (int)blockIdx.y * kWarpH;
+    const int px = x0 + lane % kWarpW, py = y0 + lane / kWarpW;
+    const int tx = x0 / kTileW, ty = y0 / kTileH;  // the 16x8 cull tile holding this 8x4 tile
+    const bool valid = px < W && py < H;
+    const float4 q = __ldg(reinterpret_cast<const float4*>(cull + (size_t)f * (tiles_x * tiles_y) + ty * tiles_x + tx));
+    if (__float_as_uint(q.z) & 1u) {               // culled (uniform over the CTA): the empty map
+        if (wv == 0 && valid) {
+            const size_t o = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
+            out_rgbt[o] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
+            out_depth[o] = 0.0f;
+        }
+        return;
+    }
+    Vol v;
+    v.data = sp.data;
+    v.sy = sp.sy;
+    v.sz = sp.sz;
+    v.occ = sp.occ;
+    v.shift = sp.occ_shift;
+    v.nbx = sp.occ_nbx;
+    v.nby = sp.occ_nby;
+    v.sx1 = sp.supp[0];
+    v.sy1 = sp.supp[1];
+    v.sz1 = sp.supp[2];
+    v.mask_words = sp.slab_off;
+    float* sA = s_split;
+    float* sT = s_split + (size_t)K * 32;          // T^l_k at sT[(l * K + k) * 32 + lane]
+    float T = 1.0f, Dout = 0.0f;
+    int k = 0;
+    uint32_t gdummy = 0;
+    if (valid) {
+        Ray r;
+        const float fpx = (float)px, fpy = (float)py;
+        r.ox = __fmaf_rn(fpy, sp.Ey[0], __fmaf_rn(fpx, sp.Ex[0], sp.B[0]));
+        r.oy = __fmaf_rn(fpy, sp.Ey[1], __fmaf_rn(fpx, sp.Ex[1], sp.B[1]));
+        r.oz = __fmaf_rn(fpy, sp.Ey[2], __fmaf_rn(fpx, sp.Ex[2], sp.B[2]));
+        r.dx = sp.Dg[0];
+        r.dy = sp.Dg[1];
+        r.dz = sp.Dg[2];
+        const float inv[3] = {sp.invD[0], sp.invD[1], sp.invD[2]};
+        r.h = mc.h;
+        const uint32_t pix = (uint32_t)py * (uint32_t)W + (uint32_t)px;
+        r.delta = mc.jitter ? jitter_delta(fmix32(sp.jh ^ pix), mc.h) : 0.0f;   // C4
+        // C5 as march_kernel's FAST path: the occupied box's step range (tile range applied), exact ends
+        int m_lo = 1, m_hi = 0;
+        {
+            float u0 = -3.0e38f, u1 = 3.0e38f;
+            bool miss = false;
+            slab(r.ox - sp.alo[0], r.dx, inv[0], sp.ahi[0] - sp.alo[0], 1e-3f, u0, u1, miss);
+            slab(r.oy - sp.alo[1], r.dy, inv[1], sp.ahi[1] - sp.alo[1], 1e-3f, u0, u1, miss);
+            slab(r.oz - sp.alo[2], r.dz, inv[2], sp.ahi[2] - sp.alo[2], 1e-3f, u0, u1, miss);
+#if NSL_TILE_RANGE
+            u0 = fmaxf(u0, q.x);
+            u1 = fminf(u1, q.y);
+#endif
+            if (!miss && u0 <= u1) {
+                const float inv_h = 1.0f / mc.h;
+                const float a = fmaxf(floorf((u0 - r.delta) * inv_h) - 1.0f, 1.0f);
+                const float b = fminf(ceilf((u1 - r.delta) * inv_h) + 1.0f, (float)mc.Ncap);
+                if (a <= b) {
+                    m_lo = (int)a;
+                    m_hi = (int)b;
+                    while (m_lo <= m_hi && !r.in(v, m_lo)) ++m_lo;
+                    while (m_hi >= m_lo && !r.in(v, m_hi)) --m_hi;
+                }
+            }
+        }
+        float tau = 0.0f;
+        const bool front_fast = sp.front_ok && m_lo <= m_hi && !r.in(v, 1);   // C9 per ray
+        const float kl = mc.hl * mc.kappa;
+        for (int n = m_lo; n <= m_hi; ++n) {
+            float t, x, y, z;
+            r.atf((float)n, t, x, y, z);
+            const float rho = sample<LAYOUT, false>(v, x, y, z, gdummy);
+            if (rho > 0.0f) {
+                const float sig_t = __fmul_rn(mc.kappa, rho);
+                const float sig_s = __fmul_rn(mc.alpha, sig_t);
+                if (Dout == 0.0f && sig_s > mc.tau_d) Dout = t;           // C6
+                const float s = __fmul_rn(sig_t, mc.h);                  // C7
+                const float Tp = T;
+                tau = __fadd_rn(tau, s);
+                T = __expf(-tau);
+                float A;
+                if (mc.form == NSL_OPACITY_EXP) A = mc.alpha * (Tp - T);
+                else if (mc.form == NSL_OPACITY_RIEMANN) A = mc.alpha * Tp * s;
+                else A = Tp * sig_s;
+                NSL_ASSERT(k < K);
+                if (wv == 0) sA[k * 32 + lane] = A;
+                if (k % kSplit == wv) {                                  // this warp's light marches
+                    float ra[3], rb[3];
+                    pair_regions(sp, v, z, ra, rb);
+                    const int ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.ilh[1], ra);
+                    const int mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.ilh[2], rb);
+                    float sa, sb;
+                    if (NSL_HZ && ((sp.lz0 >> 1) & 3) == 3)
+                        light_sum_pair_hz<LAYOUT, false>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], mc.hl, ma, mb, sa, sb,
+                                                         gdummy);
+                    else
+                        light_sum_pair<LAYOUT, false>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, ma, mb,
+                                                      sa, sb, gdummy);
+                    float T0;
+                    if (front_fast) {
+                        T0 = Tp;                                             // C9
+                    } else {
+                        float rl[3];
+                        march_region(sp, v, 0, z, rl);
+                        const int mm = light_bound(v, x, y, z, sp.Lg[0][0], sp.Lg[0][1], sp.Lg[0][2], mc.hl,
+                                                   sp.ilh[0], rl);
+                        T0 = __expf(-kl * light_sum<LAYOUT, false>(v, x, y, z, sp.Lg[0][0], sp.Lg[0][1], sp.Lg[0][2],
+                                                                    mc.hl, mm, gdummy));
+                    }
+                    sT[(0 * K + k) * 32 + lane] = T0;
+                    sT[(1 * K + k) * 32 + lane] = __expf(-kl * sa);
+                    sT[(2 * K + k) * 32 + lane] = __expf(-kl * sb);
+                }
+                ++k;
+                if (T < mc.t_min) break;                                 // C11
+            }
+        }
+    }
+    __syncthreads();
+    if (wv != 0 || !valid) return;
+    // a6: S_l in k order with march_kernel's operations (light order within a sample is immaterial:
+    // the three sums are independent), then L_c = sum_l rgb_lc P_l S_l and the stores
+    float S[3] = {0.0f, 0.0f, 0.0f};
+    for (int j = 0; j < k; ++j) {
+        const float A = sA[j * 32 + lane];
+#pragma unroll
+        for (int l = 0; l < 3; ++l) S[l] = __fmaf_rn(A, sT[(l * K + j) * 32 + lane], S[l]);
+    }
+    float L0 = 0.0f, L1 = 0.0f, L2 = 0.0f;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        const float w = sp.P[l] * S[l];
+        L0 += sp.rgb[l][0] * w;
+        L1 += sp.rgb[l][1] * w;
+        L2 += sp.rgb[l][2] * w;
+    }
+    const size_t o = ((size_t)f * (size_t)H + (size_t)py) * (size_t)W + px;
+    out_rgbt[o] = make_float4(L0, L1, L2, T);
+    out_depth[o] = Dout;
+}
+
 __global__ void jitter_debug_kernel(MarchConst mc, uint32_t frame, int n, uint32_t* hash, float* delta) {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -518,7 +682,11 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
     if (tiles > 65535) return cudaErrorInvalidConfiguration;
     if (PROJ == 0) {
         if (F > 65535) return cudaErrorInvalidConfiguration;
-        const int early = (long long)F * tiles <= 8 * kCullThreads;
+        static const long long early_tiles = [] {
+            const char* e = getenv("NSL_CULL_EARLY_TILES");
+            return e ? atoll(e) : (long long)(8 * kCullThreads);
+        }();
+        const int early = (long long)F * tiles <= early_tiles;
         cudaError_t e = launch_pdl(tile_cull_kernel, dim3((unsigned)((tiles + kCullThreads - 1) / kCullThreads), (unsigned)F),
                                    dim3(kCullThreads), 0, s, fp, F, tiles_x, tiles, cull, early);
         if (e != cudaSuccess) return e;
@@ -538,6 +706,14 @@ cudaError_t launch_lpm(const FrameParams* fp, const MarchConst& mc, int F, int W
                           depth, debug, counters, W, H, (const TileCull*)cull, tiles_x, *tv);
     }
     if constexpr (MODE == kFast) {
+        if constexpr (PROJ == 0 && LAYOUT != kTex3dF32) {
+            if (mc.split_k > 0 && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3) {
+                const unsigned sx = (unsigned)((W + kWarpW - 1) / kWarpW), sy = (unsigned)((H + kWarpH - 1) / kWarpH);
+                return launch_pdl(march_split_kernel<LAYOUT>, dim3(sx, sy, (unsigned)F), dim3(32 * kSplit),
+                                  (size_t)4 * mc.split_k * 32 * sizeof(float), s, fp, mc, rgbt, depth, W, H,
+                                  (const TileCull*)cull, tiles_x, tiles_y);
+            }
+        }
         if (NSL_G3 && mc.light_mode == NSL_LIGHTS_GUIDE && mc.n_lights == 3)
             return launch_pdl(march_kernel<LAYOUT, PROJ, MODE, false, 3>, grid, dim3(kThreads), 0, s, fp, mc, rgbt,
                               depth, debug, counters, W, H, (const TileCull*)cull, tiles_x, TvArgs{});
@@ -570,6 +746,7 @@ cudaError_t launch_l(const FrameParams* fp, const MarchConst& mc, int F, int W, 
 }  // namespace
 
 int march_tile_w() { return kTileW; }
+int march_split_max_k() { return kSplitMaxK; }
 int march_tile_h() { return kTileH; }
 
 size_t march_cull_bytes(int F, int W, int H) {

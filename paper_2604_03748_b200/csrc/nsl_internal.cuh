@@ -118,6 +118,8 @@ struct MarchConst {
     float axis[3];
     int32_t light_model;       // NSL_LIGHT_MARCH | NSL_LIGHT_TV
     int32_t frame_major;       // march grid order (march.cu): 0 frames fastest, 1 tiles fastest
+    int32_t split_k;           // > 0: small FAST guide-set ortho batch -> march_split_kernel with this
+                               // bound on the occupied samples of a ray (0: the one-warp-per-tile march)
 };
 
 // NEXT-4 transmittance volume: per (frame, lattice slot) constants of the
@@ -247,6 +249,7 @@ cudaError_t launch_march(const FrameParams* fp, const MarchConst& mc, int F, int
                          TileCull* cull, const TvArgs* tv, cudaStream_t s);
 size_t march_cull_bytes(int F, int W, int H);
 int march_tile_w();
+int march_split_max_k();
 int march_tile_h();
 cudaError_t launch_bake_setup(const FrameIn* in, const FrameParams* fps, int F, float hbl, float g, BakeFrame* out,
                               cudaStream_t s);

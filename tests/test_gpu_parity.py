@@ -265,6 +265,22 @@ def test_march_grid_order_is_bitwise_invariant(nsl, monkeypatch, cfg, frames):
         assert (x is None and y is None) or np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("cfg,frames,layout", [("C1", [0], 3), ("P482", [0], 0), ("C2", [7], 3), ("C2", [0, 31], 4),
+                                                ("C3", [5], 1)])
+def test_split_march_is_bitwise_identical(nsl, monkeypatch, cfg, frames, layout):
+    """Small FAST guide-set batches take march_split_kernel (four warps per 8x4 tile, DESIGN.md §6
+    'Split march'); its maps are bitwise those of march_kernel (NSL_SPLIT=0), which the oracle
+    parity tests cover.  C3 (one explicit light) is not split: both runs take march_kernel."""
+    w = I.make_workload(cfg, frames=frames)
+    lay = nsl.LAYOUT_AUTO if layout == 0 else layout
+    outs = []
+    for sp in ("0", "1"):
+        monkeypatch.setenv("NSL_SPLIT", sp)
+        outs.append(run(nsl, w, layout=lay, debug=False))
+    for x, y in zip(outs[0][:2], outs[1][:2]):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
 def test_batch_equals_single_frames_and_is_deterministic(nsl):
     import torch
     w = I.make_workload("C2", frames=[0, 1, 2, 3])
