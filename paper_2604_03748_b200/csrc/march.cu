@@ -21,6 +21,13 @@
 namespace nsl {
 namespace {
 
+#ifndef NSL_PAIRNEG
+#define NSL_PAIRNEG 1
+#endif
+#ifndef NSL_PACKG3
+#define NSL_PACKG3 1
+#endif
+
 // Tile culling (exact, orthographic views): every ray of a tile is parallel to D_g with
 // its origin within the tile radius r of the centre ray; if the centre ray misses a box expanded by
 // r, no sample of the tile lies in the box.  bit 0: misses the occupied box (FAST:
@@ -387,6 +394,8 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
                                     tv.Astr, tv.Kstr, x, y, z);
                 if (!TV && paired) {                       // C8: top/bottom in one loop
                     int Ma, Mb, ma, mb;
+                    float l1x = sp.Lg[1][0], l1y = sp.Lg[1][1], l1z = sp.Lg[1][2];   // (FAST: packed loads)
+                    bool hzp = ((sp.lz0 >> 1) & 3) == 3;
                     if (DEBUG || COUNT) {
                         Ma = light_count(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.lim[1], sp.ilh[1]);
                         Mb = light_count(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.lim[2], sp.ilh[2]);
@@ -396,19 +405,44 @@ __global__ void __launch_bounds__(kThreads, (NL == 3 ? (TV ? NSL_MINB_G3TV : NSL
                         mb = min(Mb, box_count(x, y, z, rb, sp.ilh[2]));
                     } else {
                         Ma = Mb = 0;
+#if NSL_PAIRNEG && NSL_PACKG3
+                        // the pair's constants by three vector loads (FrameParams.pk_*), light 2 = -light 1
+                        // bit for bit (pair12), hence 1/(L2 h_l) = -1/(L1 h_l) exactly where L1 != 0
+                        const int4 pg = sp.pk_geo;
+                        const float4 pl = sp.pk_l1;
+                        const float2 pi = *reinterpret_cast<const float2*>(&sp.pk_i1);
+                        l1x = pl.x;
+                        l1y = pl.y;
+                        l1z = pl.z;
+                        const float i1[3] = {pl.w, pi.x, pi.y};
+                        const float i2[3] = {l1x != 0.0f ? -i1[0] : i1[0], l1y != 0.0f ? -i1[1] : i1[1],
+                                             l1z != 0.0f ? -i1[2] : i1[2]};
+                        float ra[3], rb[3];
+                        pair_regions_pk(sp, v, z, pg, l1x, l1y, ra, rb);
+                        ma = light_bound(v, x, y, z, l1x, l1y, l1z, mc.hl, i1, ra);
+                        mb = light_bound(v, x, y, z, -l1x, -l1y, -l1z, mc.hl, i2, rb);
+                        hzp = ((pg.z >> 1) & 3) == 3;
+#elif NSL_PAIRNEG
+                        float ra[3], rb[3];
+                        pair_regions(sp, v, z, ra, rb);
+                        const float i1[3] = {sp.ilh[1][0], sp.ilh[1][1], sp.ilh[1][2]};
+                        const float i2[3] = {l1x != 0.0f ? -i1[0] : i1[0], l1y != 0.0f ? -i1[1] : i1[1],
+                                             l1z != 0.0f ? -i1[2] : i1[2]};
+                        ma = light_bound(v, x, y, z, l1x, l1y, l1z, mc.hl, i1, ra);
+                        mb = light_bound(v, x, y, z, -l1x, -l1y, -l1z, mc.hl, i2, rb);
+#else
                         float ra[3], rb[3];
                         pair_regions(sp, v, z, ra, rb);
                         ma = light_bound(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, sp.ilh[1], ra);
                         mb = light_bound(v, x, y, z, sp.Lg[2][0], sp.Lg[2][1], sp.Lg[2][2], mc.hl, sp.ilh[2], rb);
+#endif
                     }
                     if (COUNT) c_tl += (uint32_t)(ma + mb);
                     float sa, sb;
-                    if (NSL_HZ && ((sp.lz0 >> 1) & 3) == 3)     // both side lights horizontal: hoisted z plane
-                        light_sum_pair_hz<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], mc.hl, ma, mb, sa, sb,
-                                                         c_gath);
+                    if (NSL_HZ && hzp)                         // both side lights horizontal: hoisted z plane
+                        light_sum_pair_hz<LAYOUT, COUNT>(v, x, y, z, l1x, l1y, mc.hl, ma, mb, sa, sb, c_gath);
                     else
-                        light_sum_pair<LAYOUT, COUNT>(v, x, y, z, sp.Lg[1][0], sp.Lg[1][1], sp.Lg[1][2], mc.hl, ma, mb,
-                                                      sa, sb, c_gath);
+                        light_sum_pair<LAYOUT, COUNT>(v, x, y, z, l1x, l1y, l1z, mc.hl, ma, mb, sa, sb, c_gath);
                     S[1] = __fmaf_rn(A, __expf(-kl * sa), S[1]);
                     S[2] = __fmaf_rn(A, __expf(-kl * sb), S[2]);
                     lsamp += (uint32_t)(Ma + Mb);

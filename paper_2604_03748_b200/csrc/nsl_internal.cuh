@@ -78,6 +78,10 @@ struct FrameParams {
     int32_t lz0;               // bit l: L_g,l,z == 0 exactly (the march of light l stays in its z slab)
     uint32_t jh;               // C4: the per-frame prefix of the jitter chain, fmix32^3 of (seed, frame)
     int32_t pad2[2];
+    // the guide pair's per-occupied-sample constants packed for vector loads (copies of the fields
+    // above): (Lg[1], ilh[1][0]), (ilh[1][1], ilh[1][2], 0, 0), (slab_off, occ_nbz, lz0, pair12)
+    float4 pk_l1, pk_i1;
+    int4 pk_geo;
 };
 static_assert(sizeof(FrameParams) % 16 == 0, "FrameParams must be 16-B multiple");
 

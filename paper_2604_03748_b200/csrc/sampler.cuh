@@ -468,6 +468,33 @@ __device__ __forceinline__ void pair_regions(const FrameParams& sp, const Vol& v
     }
 }
 
+// pair_regions from the packed per-frame constants (FrameParams.pk_geo = (slab_off, occ_nbz, lz0,
+// pair12) and light 1's (Lx, Ly)): the same values, fewer loads.
+__device__ __forceinline__ void pair_regions_pk(const FrameParams& sp, const Vol& v, float uz, int4 geo, float Lx,
+                                                float Ly, float ra[3], float rb[3]) {
+    if ((geo.z >> 1) & 1) {
+        const int iz = __float_as_int(__fadd_rd(uz, kFloorBias)) - 0x4B400000;
+        const int bz = iz >> v.shift;
+        const int* slab = reinterpret_cast<const int*>(v.occ) + geo.x;
+        const int2 mn = __ldg(reinterpret_cast<const int2*>(slab + 2 * bz));
+        const int2 mx = __ldg(reinterpret_cast<const int2*>(slab + 2 * geo.y + 2 * bz));
+        const float B = (float)(1 << v.shift);
+        const float lox = (float)mn.x * B, hix = fminf((float)(mx.x + 1) * B, v.sx1);
+        const float loy = (float)mn.y * B, hiy = fminf((float)(mx.y + 1) * B, v.sy1);
+        ra[0] = Lx > 0.0f ? hix : (Lx < 0.0f ? lox : 3.0e38f);
+        rb[0] = Lx > 0.0f ? lox : (Lx < 0.0f ? hix : 3.0e38f);
+        ra[1] = Ly > 0.0f ? hiy : (Ly < 0.0f ? loy : 3.0e38f);
+        rb[1] = Ly > 0.0f ? loy : (Ly < 0.0f ? hiy : 3.0e38f);
+        ra[2] = rb[2] = 3.0e38f;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            ra[q] = sp.alim[1][q];
+            rb[q] = sp.alim[2][q];
+        }
+    }
+}
+
 __device__ __forceinline__ float hg32(float g, float c) {
     const float d = (1.0f + g * g) - 2.0f * g * c;
     return (1.0f - g * g) / (12.566370614359172f * d * sqrtf(d));

@@ -173,9 +173,15 @@ __global__ void __launch_bounds__(32 * kSetupWarps) frame_setup_kernel(const Fra
         }
         // cos theta = to_light . dir (C10); per frame for ortho (dir = f)
         p.P[l] = on ? (float)hg64((double)mc.g, dot3(Ln, f)) : 0.0f;
+        float ilh[3];
         for (int q = 0; q < 3; ++q) {  // estimate helpers
             p.lim[l][q] = Lg[q] > 0.0f ? supp[q] : (Lg[q] < 0.0f ? 0.0f : 3.0e38f);
-            p.ilh[l][q] = Lg[q] != 0.0f ? 1.0f / (Lg[q] * mc.hl) : 1.0f;
+            ilh[q] = Lg[q] != 0.0f ? 1.0f / (Lg[q] * mc.hl) : 1.0f;
+            p.ilh[l][q] = ilh[q];
+        }
+        if (l == 1) {
+            p.pk_l1 = make_float4(Lg[0], Lg[1], Lg[2], ilh[0]);
+            p.pk_i1 = make_float4(ilh[1], ilh[2], 0.0f, 0.0f);
         }
     }
     // ---- cross-lane predicates: C9 (front light exactly -D_g), the opposite guide pair, L_z == 0
@@ -195,6 +201,11 @@ __global__ void __launch_bounds__(32 * kSetupWarps) frame_setup_kernel(const Fra
         for (int q = 0; q < 3; ++q) pair = pair && (Lg2[q] == -Lg1[q]);
         p.pair12 = pair ? 1 : 0;
         p.lz0 = (int32_t)(lz & 0xfu);   // horizontal light: marches stay in one z slab
+        p.pk_geo = make_int4(fr.vol.og.words, fr.vol.og.nbz, p.lz0, p.pair12);
+        if (mc.n_lights < 2) {
+            p.pk_l1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            p.pk_i1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
     }
     // ---- occupied box in padded-index positions: cells [bmin*B, (bmax+1)*B) -> U in [lo, hi),
     //      clipped to the support
