@@ -371,10 +371,19 @@ __device__ __forceinline__ void light_sum_pair(const Vol& v, float ux, float uy,
 
 // light_sum_pair for a horizontal pair (both lights' L_z == 0 bit-exactly): the same samples
 // through sample_hz, the z plane of U computed once.
+#ifndef NSL_ZPIN
+#define NSL_ZPIN 1
+#endif
 template <int LAYOUT, bool COUNT>
 __device__ __forceinline__ void light_sum_pair_hz(const Vol& v, float ux, float uy, float uz, float lx, float ly,
                                                   float hl, int Ma, int Mb, float& sa, float& sb, uint32_t& gathers) {
+#if NSL_ZPIN
+    // opaque copies: ptxas must keep the plane in registers instead of recomputing it per sample
+    ZPlane zp = zplane<LAYOUT>(v, uz);
+    asm volatile("" : "+r"(zp.zb), "+r"(zp.ze), "+f"(zp.fz));
+#else
     const ZPlane zp = zplane<LAYOUT>(v, uz);
+#endif
     float a = 0.0f, b = 0.0f;
     const int M = max(Ma, Mb);
     float jf = 1.0f;
