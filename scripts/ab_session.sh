@@ -1,5 +1,4 @@
 set -u
-o=gpurun_out/ab13; mkdir -p $o
-python scripts/ab_run.py base ss ssc --reps 3 --steps 100 --bench-args "--config C2" > $o/c2.txt 2>&1
-python scripts/ab_run.py base ss ssc --reps 2 --steps 3 --bench-args "--config C5 --frames 32" > $o/c5.txt 2>&1
-python scripts/ab_run.py base ss ssc --reps 2 --steps 5 --bench-args "--config C4 --frames 16" > $o/c4.txt 2>&1
+o=gpurun_out/ab14; mkdir -p $o
+python scripts/ab_run.py base r36 --reps 3 --steps 100 --bench-args "--config C2" > $o/c2.txt 2>&1
+python scripts/ab_run.py base r36 --reps 2 --steps 3 --bench-args "--config C5 --frames 32" > $o/c5.txt 2>&1
