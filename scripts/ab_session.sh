@@ -1,2 +1,4 @@
-o=gpurun_out/checked; mkdir -p $o
-NSL_LIB=$PWD/abl/libnsl_checked.so timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > $o/tests.log 2>&1; echo rc=$? >> $o/tests.log
+set -u
+o=gpurun_out/ab16; mkdir -p $o
+python scripts/ab_run.py base hzs --reps 3 --steps 100 --bench-args "--config C2" > $o/c2.txt 2>&1
+python scripts/ab_run.py base hzs --reps 2 --steps 3 --bench-args "--config C5 --frames 32" > $o/c5.txt 2>&1
