@@ -1,4 +1,6 @@
 set -u
-o=gpurun_out/ab16; mkdir -p $o
-python scripts/ab_run.py base hzs --reps 3 --steps 100 --bench-args "--config C2" > $o/c2.txt 2>&1
-python scripts/ab_run.py base hzs --reps 2 --steps 3 --bench-args "--config C5 --frames 32" > $o/c5.txt 2>&1
+o=gpurun_out/v18; mkdir -p $o
+timeout 1200 python -m pytest tests -m gpu -q -x > $o/tests.log 2>&1; echo rc=$? >> $o/tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $o/smoke.log 2>&1; echo rc=$? >> $o/smoke.log
+timeout 300 python bench.py > $o/bench.json 2> $o/bench.err
+bash scripts/ab_bake.sh evf1 noal > $o/bake.txt 2>&1
