@@ -42,7 +42,8 @@ static_assert(kThreads % 32 == 0 && NSL_TILEW % NSL_WARPW == 0 && NSL_TILEH % (3
 #ifndef NSL_VOL_EVF
 #define NSL_VOL_EVF 2   // OCT gathers: 2 = L1::no_allocate (the gathers' lines do not displace the mask, frame
                         // constants and spill lines: C2 -1.0 %, C3 -2.1 %, C5 -4.3 % vs evict_first,
-                        // profiles/r2_ab17), 1 = L1::evict_first, 0 = plain
+                        // profiles/r2_ab17), 1 = L1::evict_first, 0 = plain, 3 = no_allocate + L2::evict_last
+                        // (the same as 2, profiles/r2_ab19)
 #endif
 #ifndef NSL_G3
 #define NSL_G3 1    // FAST guide-set (3 lights) launches use the march specialised for it
@@ -118,7 +119,11 @@ __device__ __forceinline__ float gather_interp(const Vol& v, int e, float fx, fl
     } else if (LAYOUT == kOctF32 || LAYOUT == kBrickOctF32 || LAYOUT == kMortonOctF32) {
         // one 256-bit gather: (c000, c100 - c000, c010, c110 - c010 | the same for plane k+1)
         float a0, a1, a2, a3, b0, b1, b2, b3;
-#if NSL_VOL_EVF == 2
+#if NSL_VOL_EVF == 3
+        asm("ld.global.nc.L1::no_allocate.L2::evict_last.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
+            : "l"(static_cast<const float*>(v.data) + 8 * (size_t)e));
+#elif NSL_VOL_EVF == 2
         asm("ld.global.nc.L1::no_allocate.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
             : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
             : "l"(static_cast<const float*>(v.data) + 8 * (size_t)e));
