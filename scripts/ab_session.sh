@@ -1,5 +1,5 @@
 set -u
-o=gpurun_out/v20; mkdir -p $o
-timeout 1200 python -m pytest tests -m gpu -q -x > $o/tests.log 2>&1; echo rc=$? >> $o/tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $o/smoke.log 2>&1; echo rc=$? >> $o/smoke.log
-timeout 300 python bench.py > $o/bench.json 2> $o/bench.err
+o=gpurun_out/ab21; mkdir -p $o
+python scripts/ab_run.py base mel --reps 3 --steps 100 --bench-args "--config C2" > $o/c2.txt 2>&1
+python scripts/ab_run.py base mel --reps 2 --steps 3 --bench-args "--config C5 --frames 32" > $o/c5.txt 2>&1
+python scripts/ab_run.py base mel --reps 2 --steps 20 --bench-args "--config C3 --frames 16" > $o/c3.txt 2>&1
